@@ -1,0 +1,121 @@
+/*
+ * paro_b200 — C ABI of the B200-native ParO hot path (sm_100a).
+ *
+ * The drop-in boundary for the reference's fixed-mesh outer iteration
+ * (arXiv 1405.0260, reference C++ in proj/). Every entry point below replaces
+ * one reference interface, cited as proj/<file>:<line>. Plain pointers and
+ * sizes only; no C++ or torch types cross this boundary.
+ *
+ * Conventions
+ *  - One context per GPU; all work is enqueued on the context's CUDA stream
+ *    (paro_ctx_set_stream) and the calls that return host scalars synchronise it.
+ *  - Vectors live on the DEVICE unless a parameter says "host". A vector is
+ *    the interior-dof coefficient array of the reference (dof order of
+ *    proj/src/fem.cpp:21-28 on create_box_mesh, proj/src/mesh.cpp:411-478):
+ *    n = (s-1)^3 doubles, x fastest. A batch of k vectors is column-major with
+ *    column stride ld >= n (orbital c starts at base + c*ld).
+ *  - Return value: PARO_OK or an error code naming the reference exception
+ *    type (proj/include/paro/errors.hpp:9-80); paro_ctx_last_error() holds the
+ *    message and paro_ctx_last_residual() the IterationLimitError residual.
+ */
+#ifndef PARO_B200_H
+#define PARO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct paro_ctx paro_ctx;
+typedef struct paro_op paro_op;
+
+enum {
+  PARO_OK = 0,
+  PARO_ERROR = 1,             /* paro::Error                 errors.hpp:10-13 */
+  PARO_INVALID_ARGUMENT = 2,  /* paro::InvalidArgumentError  errors.hpp:15-17 */
+  PARO_NOT_SPD = 3,           /* paro::NotSpdError           errors.hpp:25-27 */
+  PARO_ITERATION_LIMIT = 4,   /* paro::IterationLimitError   errors.hpp:30-33 */
+  PARO_DEGENERATE_SPAN = 5,   /* paro::DegenerateSpanError   errors.hpp:70-72 */
+  PARO_PENCIL = 6,            /* paro::PencilError           errors.hpp:60-62 */
+  PARO_EMPTY_BASIS = 7,       /* paro::EmptyBasisError       errors.hpp:65-67 */
+  PARO_CAPACITY = 8,          /* paro::CapacityError         errors.hpp:40-42 */
+  PARO_LINEAGE = 9,           /* paro::LineageError          errors.hpp:35-37 */
+  PARO_CUDA_ERROR = 20        /* CUDA / cuBLAS failure (no reference counterpart) */
+};
+
+/* ------------------------------------------------------------ context ---- */
+int paro_ctx_create(int device, void* cuda_stream, paro_ctx** out);
+int paro_ctx_destroy(paro_ctx* ctx);
+int paro_ctx_set_stream(paro_ctx* ctx, void* cuda_stream);
+const char* paro_ctx_last_error(const paro_ctx* ctx);
+double paro_ctx_last_residual(const paro_ctx* ctx);
+/* kernels launched by this library so far (CUDA-graph nodes counted) */
+unsigned long long paro_ctx_launches(const paro_ctx* ctx);
+int paro_ctx_synchronize(paro_ctx* ctx);
+
+/* Device memory helpers for callers without their own allocator. */
+int paro_malloc(paro_ctx* ctx, size_t bytes, void** dev);
+int paro_free(paro_ctx* ctx, void* dev);
+int paro_memcpy_h2d(paro_ctx* ctx, void* dev, const void* host, size_t bytes);
+int paro_memcpy_d2h(paro_ctx* ctx, void* host, const void* dev, size_t bytes);
+
+/* Uniform box mesh [lo,hi]^3 with `subdivisions` cells per axis
+ * (create_box_mesh + FeSpace::create, mesh.cpp:411-478, fem.cpp:13-30). */
+int paro_grid_init(paro_ctx* ctx, int subdivisions, double lo, double hi);
+long long paro_grid_dofs(const paro_ctx* ctx);
+
+/* ---------------------------------------------------------- operators ---- */
+/* A symmetric 15-point P1/Kuhn operator (SparseOperator, linalg.hpp:14-50).
+ * Slot o = (x:bit0, y:bit1, z:bit2) holds A[v, v+o]; slot 0 the diagonal. */
+int paro_op_create_const(paro_ctx* ctx, const double w[8], paro_op** out);
+int paro_op_create_var(paro_ctx* ctx, paro_op** out);
+/* SparseOperator(n, row_offsets, cols, vals) -> stencil (linalg.cpp:16-22);
+ * PARO_INVALID_ARGUMENT if the pattern is not the Kuhn stencil of the grid or
+ * the matrix is not symmetric. Uniform operators become constant stencils. */
+int paro_op_from_csr(paro_ctx* ctx, size_t n, const size_t* row_offsets, const uint32_t* cols,
+                     const double* vals, paro_op** out);
+/* host copy of the operator as CSR in the reference's pattern (sorted cols,
+ * all 15 Kuhn neighbours, zeros kept): rows n+1, cols/vals nnz; pass NULLs to
+ * query nnz. */
+int paro_op_to_csr(paro_ctx* ctx, const paro_op* a, size_t* nnz, size_t* row_offsets, uint32_t* cols,
+                   double* vals);
+int paro_op_coefficients(paro_op* a, double** dev_coef8);
+int paro_op_weights(const paro_op* a, double w[8], int* is_variable);
+int paro_op_destroy(paro_op* a);
+
+/* y = (A + sigma B) x for k columns (SparseOperator::matvec + add_scaled,
+ * linalg.cpp:88-94, 120-125). `shift` may be NULL. */
+int paro_op_apply(paro_ctx* ctx, const paro_op* a, const paro_op* shift, double sigma, int k, const double* x,
+                  long long ldx, double* y, long long ldy);
+
+/* ----------------------------------------------------------- solvers ----- */
+/* cg_solve (linalg.cpp:143-223, Jacobi preconditioner) for k right-hand sides;
+ * x0 may be NULL (zero start). iterations/residual: host arrays of k or NULL. */
+int paro_cg_solve(paro_ctx* ctx, const paro_op* a, int k, const double* b, const double* x0, long long ld,
+                  double tol, size_t max_iter, int throw_on_max_iter, double* x, size_t* iterations,
+                  double* residual);
+
+/* Step 3: source_solve_step (paro.cpp:81-119):
+ *   (A + sigma B) u_half_i = (lambda_i + sigma) B u_prev_i,  x0 = u_prev_i,
+ * one tolerance-relaxation retry (tol*100, max_iter*4) per orbital.
+ * lambdas: host array of k. */
+int paro_source_solve_step(paro_ctx* ctx, const paro_op* a, const paro_op* b, int k, const double* u_prev,
+                           long long ld, const double* lambdas, double tol, size_t max_iter, double sigma,
+                           double* u_half, size_t* iterations, double* residual);
+/* shifted_source_step (paro.cpp:194-210): sigma = max(0, 0.5 - lambda_1),
+ * 2 sigma + 1 on NotSpd, at most 5 attempts; sigma_out: host. */
+int paro_shifted_source_step(paro_ctx* ctx, const paro_op* a, const paro_op* b, int k, const double* u_prev,
+                             long long ld, const double* lambdas, double tol, size_t max_iter, double* u_half,
+                             double* sigma_out, size_t* iterations, double* residual);
+
+/* hartree_solve_with (model.cpp:242-255): poisson V = 4 pi M rho. */
+int paro_hartree_solve(paro_ctx* ctx, const paro_op* poisson, const paro_op* mass, const double* rho, double tol,
+                       double* vh, size_t* iterations);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PARO_B200_H */

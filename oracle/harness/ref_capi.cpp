@@ -1,0 +1,661 @@
+// oracle/harness/ref_capi.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// A flat C wrapper over the *unmodified* reference implementation
+// (/root/reference/proj), compiled from its own sources by oracle/Makefile into
+// oracle/_ref/libparo_ref.so. Only tests/, __graft_entry__.smoke() and
+// bench.py's CPU-baseline / --impl reference legs load it, as the checker and
+// the CPU baseline; the product path never does.
+//
+// The harness only sequences public reference calls. The fixed-mesh loop
+// helpers (shifted_source_step, ks_form_matrix, assemble_ks_operators,
+// occupied_functions, cg_tol_for_iteration) live in an anonymous namespace in
+// proj/src/paro.cpp, so this file is a unity build that #includes paro.cpp
+// (SURVEY.md §8c "Oracle harness contract"); paro.cpp is therefore left out of
+// the object list in the Makefile.
+#include "paro.cpp"  // NOLINT: unity build of the reference driver (proj/src/paro.cpp)
+
+#include <cstring>
+#include <exception>
+#include <string>
+
+using namespace paro;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local double g_resid = 0.0;
+
+enum RefStatus {
+  REF_OK = 0,
+  REF_ERR = 1,
+  REF_INVALID = 2,
+  REF_NOTSPD = 3,
+  REF_ITERLIMIT = 4,
+  REF_DEGENERATE = 5,
+  REF_PENCIL = 6,
+  REF_EMPTY = 7,
+  REF_CAPACITY = 8,
+  REF_LINEAGE = 9,
+  REF_EVAL = 10,
+  REF_DIVERGENCE = 11,
+  REF_UNKNOWN = 99,
+};
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return REF_OK;
+  } catch (const IterationLimitError& e) {
+    g_err = e.what();
+    g_resid = e.residual;
+    return REF_ITERLIMIT;
+  } catch (const NotSpdError& e) {
+    g_err = e.what();
+    return REF_NOTSPD;
+  } catch (const DegenerateSpanError& e) {
+    g_err = e.what();
+    return REF_DEGENERATE;
+  } catch (const PencilError& e) {
+    g_err = e.what();
+    return REF_PENCIL;
+  } catch (const EmptyBasisError& e) {
+    g_err = e.what();
+    return REF_EMPTY;
+  } catch (const CapacityError& e) {
+    g_err = e.what();
+    return REF_CAPACITY;
+  } catch (const LineageError& e) {
+    g_err = e.what();
+    return REF_LINEAGE;
+  } catch (const EvaluationError& e) {
+    g_err = e.what();
+    return REF_EVAL;
+  } catch (const ScfDivergenceError& e) {
+    g_err = e.what();
+    return REF_DIVERGENCE;
+  } catch (const InvalidArgumentError& e) {
+    g_err = e.what();
+    return REF_INVALID;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return REF_ERR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return REF_UNKNOWN;
+  }
+}
+
+struct SpaceH {
+  std::shared_ptr<const FeSpace> space;
+};
+
+struct OpH {
+  SparseOperator op;
+};
+
+struct KsH {
+  std::shared_ptr<const FeSpace> space;
+  KsModel model;
+  KsOperators ops;
+};
+
+Molecule make_molecule(int nnuc, const double* z, const double* r, int n_electrons) {
+  Molecule m;
+  for (int k = 0; k < nnuc; ++k) {
+    Nucleus nuc;
+    nuc.charge = z[k];
+    nuc.position = {r[3 * k], r[3 * k + 1], r[3 * k + 2]};
+    m.nuclei.push_back(nuc);
+  }
+  m.n_electrons = n_electrons;
+  return m;
+}
+
+std::vector<std::vector<double>> unpack(std::size_t k, std::size_t n, const double* u) {
+  std::vector<std::vector<double>> out(k, std::vector<double>(n));
+  for (std::size_t c = 0; c < k; ++c) std::memcpy(out[c].data(), u + c * n, n * sizeof(double));
+  return out;
+}
+
+void pack(const std::vector<std::vector<double>>& v, double* out) {
+  for (std::size_t c = 0; c < v.size(); ++c) std::memcpy(out + c * v[c].size(), v[c].data(), v[c].size() * sizeof(double));
+}
+
+Density make_density(const std::shared_ptr<const FeSpace>& space, const double* rho, std::size_t n_occ) {
+  Density d;
+  d.rho = DiscreteFunction(space, std::vector<double>(rho, rho + space->dof_count()));
+  d.occupations.assign(n_occ, 2.0);
+  d.raw_integral = integrate(d.rho);
+  return d;
+}
+
+// Fixed-mesh Kohn-Sham loop state (mirrors proj/src/paro.cpp:485-638 with the
+// adaptive branch off and the Step-2 estimator omitted on both sides).
+struct KsState {
+  KsH* ks = nullptr;
+  ParoConfig cfg;
+  OrbitalSet orbitals;
+  Density rho_in;
+  Density rho_out;
+  long clamped = 0;
+};
+
+// Fixed-mesh linear loop state (mirrors proj/src/paro.cpp:302-370).
+struct LinState {
+  std::shared_ptr<const FeSpace> space;
+  const SparseOperator* a = nullptr;
+  const SparseOperator* b = nullptr;
+  ParoConfig cfg;
+  OrbitalSet orbitals;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+double ref_last_residual() { return g_resid; }
+
+// ---------------------------------------------------------------- spaces ----
+void* ref_space_create(int subdivisions, double lo, double hi, int dim) {
+  SpaceH* h = nullptr;
+  const int st = guarded([&] {
+    Box box;
+    box.dim = dim;
+    box.lo = {lo, lo, dim == 3 ? lo : 0.0};
+    box.hi = {hi, hi, dim == 3 ? hi : 0.0};
+    auto mesh = std::make_shared<Mesh>(create_box_mesh(box, subdivisions));
+    h = new SpaceH{FeSpace::create(mesh)};
+  });
+  return st == REF_OK ? h : nullptr;
+}
+void ref_space_free(void* h) { delete static_cast<SpaceH*>(h); }
+std::size_t ref_space_dofs(void* h) { return static_cast<SpaceH*>(h)->space->dof_count(); }
+std::size_t ref_space_elements(void* h) { return static_cast<SpaceH*>(h)->space->mesh().element_count(); }
+
+// ------------------------------------------------------------- operators ----
+void* ref_op_mass(void* sp) {
+  OpH* h = nullptr;
+  guarded([&] { h = new OpH{assemble_mass(*static_cast<SpaceH*>(sp)->space)}; });
+  return h;
+}
+void* ref_op_stiffness(void* sp, double scale) {
+  OpH* h = nullptr;
+  guarded([&] {
+    h = new OpH{assemble_stiffness(*static_cast<SpaceH*>(sp)->space, constant_diffusion(scale),
+                                   constant_field(0.0))};
+  });
+  return h;
+}
+// Weighted mass of the (bare or smoothed) Coulomb potential, singular-aware
+// policy exactly as assemble_ks_operators / paro_linear use it.
+void* ref_op_wmass_coulomb(void* sp, int nnuc, const double* z, const double* r, double eps) {
+  OpH* h = nullptr;
+  guarded([&] {
+    const Molecule mol = make_molecule(nnuc, z, r, 2);
+    const PotentialField pf = external_potential(mol, eps);
+    SingularQuadPolicy policy;
+    policy.singular_points = pf.singular_points;
+    h = new OpH{assemble_weighted_mass(*static_cast<SpaceH*>(sp)->space, field_from(pf.value), policy)};
+  });
+  return h;
+}
+// Weighted mass of c * |x|^2 (harmonic reaction term, no singular points).
+void* ref_op_wmass_harmonic(void* sp, double c) {
+  OpH* h = nullptr;
+  guarded([&] {
+    const PointFn f = [c](const Vec3& x) { return c * (x.x * x.x + x.y * x.y + x.z * x.z); };
+    h = new OpH{assemble_weighted_mass(*static_cast<SpaceH*>(sp)->space, field_from(f), {})};
+  });
+  return h;
+}
+// Weighted mass of a nodal P1 field (assemble_weighted_mass(space, DiscreteFunction)).
+void* ref_op_wmass_nodal(void* sp, const double* w) {
+  OpH* h = nullptr;
+  guarded([&] {
+    auto space = static_cast<SpaceH*>(sp)->space;
+    DiscreteFunction f(space, std::vector<double>(w, w + space->dof_count()));
+    h = new OpH{assemble_weighted_mass(*space, f)};
+  });
+  return h;
+}
+void* ref_op_copy(void* op) { return new OpH{static_cast<OpH*>(op)->op}; }
+int ref_op_add_scaled(void* a, void* b, double s) {
+  return guarded([&] { static_cast<OpH*>(a)->op.add_scaled(static_cast<OpH*>(b)->op, s); });
+}
+void ref_op_free(void* op) { delete static_cast<OpH*>(op); }
+std::size_t ref_op_nnz(void* op) { return static_cast<OpH*>(op)->op.nnz(); }
+std::size_t ref_op_dim(void* op) { return static_cast<OpH*>(op)->op.dimension(); }
+void ref_op_csr(void* op, std::size_t* rows, std::uint32_t* cols, double* vals) {
+  const SparseOperator& a = static_cast<OpH*>(op)->op;
+  std::memcpy(rows, a.row_offsets().data(), (a.dimension() + 1) * sizeof(std::size_t));
+  std::memcpy(cols, a.col_indices().data(), a.nnz() * sizeof(std::uint32_t));
+  std::memcpy(vals, a.values().data(), a.nnz() * sizeof(double));
+}
+void* ref_op_from_csr(std::size_t n, const std::size_t* rows, const std::uint32_t* cols,
+                      const double* vals, int symmetric) {
+  OpH* h = nullptr;
+  guarded([&] {
+    const std::size_t nnz = rows[n];
+    h = new OpH{SparseOperator(n, std::vector<std::size_t>(rows, rows + n + 1),
+                               std::vector<std::uint32_t>(cols, cols + nnz),
+                               std::vector<double>(vals, vals + nnz), symmetric != 0)};
+  });
+  return h;
+}
+
+// --------------------------------------------------------------- algebra ----
+void ref_matvec(void* op, const double* x, double* y) {
+  const SparseOperator& a = static_cast<OpH*>(op)->op;
+  a.matvec(std::span<const double>(x, a.dimension()), std::span<double>(y, a.dimension()));
+}
+
+int ref_cg(void* op, const double* b, const double* x0, double tol, std::size_t max_iter,
+           int precond, int throw_on_max, double* x, std::size_t* iters, double* resid, int* conv) {
+  return guarded([&] {
+    const SparseOperator& a = static_cast<OpH*>(op)->op;
+    const std::size_t n = a.dimension();
+    std::vector<double> bv(b, b + n), x0v;
+    CgOptions o;
+    o.tol = tol;
+    o.max_iter = max_iter;
+    o.precond = precond ? Preconditioner::diagonal : Preconditioner::none;
+    o.throw_on_max_iter = throw_on_max != 0;
+    if (x0) {
+      x0v.assign(x0, x0 + n);
+      o.x0 = &x0v;
+    }
+    const CgResult r = cg_solve(a, bv, o);
+    std::memcpy(x, r.x.data(), n * sizeof(double));
+    *iters = r.iterations;
+    *resid = r.residual;
+    *conv = r.converged ? 1 : 0;
+  });
+}
+
+int ref_source_solve(void* a, void* b, std::size_t k, const double* u, const double* lambdas,
+                     double tol, std::size_t max_iter, int workers, double sigma, double* out) {
+  return guarded([&] {
+    const std::size_t n = static_cast<OpH*>(a)->op.dimension();
+    SourceSolveOptions o;
+    o.tol = tol;
+    o.max_iter = max_iter;
+    o.workers = workers;
+    o.sigma = sigma;
+    const auto half = source_solve_step(static_cast<OpH*>(a)->op, static_cast<OpH*>(b)->op,
+                                        unpack(k, n, u), std::vector<double>(lambdas, lambdas + k), o);
+    pack(half, out);
+  });
+}
+
+// shifted_source_step (paro.cpp:194-210): the sigma policy around Step 3.
+int ref_shifted_source(void* a, void* b, void* sp, std::size_t k, const double* u,
+                       const double* lambdas, double tol, std::size_t max_iter, int workers,
+                       double* out, double* sigma_out) {
+  return guarded([&] {
+    const std::size_t n = static_cast<OpH*>(a)->op.dimension();
+    OrbitalSet set;
+    set.space = static_cast<SpaceH*>(sp)->space;
+    set.orbitals = unpack(k, n, u);
+    set.lambdas.assign(lambdas, lambdas + k);
+    SourceSolveOptions o;
+    o.tol = tol;
+    o.max_iter = max_iter;
+    o.workers = workers;
+    const StepOutcome step = shifted_source_step(static_cast<OpH*>(a)->op, static_cast<OpH*>(b)->op, set, o);
+    pack(step.half, out);
+    *sigma_out = step.sigma;
+  });
+}
+
+// Step 3 at a pinned inner-iteration count (precedent: proj/src/suites.cpp:439-457):
+// each column runs exactly `iters` CG iterations (tol 1e-30, no throw).
+int ref_source_pinned(void* a, void* b, std::size_t k, const double* u, const double* lambdas,
+                      double sigma, std::size_t iters, int workers) {
+  return guarded([&] {
+    const SparseOperator& bb = static_cast<OpH*>(b)->op;
+    SparseOperator shifted = static_cast<OpH*>(a)->op;
+    if (sigma != 0.0) shifted.add_scaled(bb, sigma);
+    const std::size_t n = shifted.dimension();
+    const auto uu = unpack(k, n, u);
+    parallel_for(k, workers, [&](std::size_t i) {
+      std::vector<double> rhs = bb.apply(uu[i]);
+      for (double& v : rhs) v *= lambdas[i] + sigma;
+      CgOptions cg;
+      cg.tol = 1e-30;
+      cg.max_iter = iters;
+      cg.throw_on_max_iter = false;
+      cg.x0 = &uu[i];
+      (void)cg_solve(shifted, rhs, cg);
+    });
+  });
+}
+
+int ref_rayleigh_ritz(void* sp, std::size_t k, const double* cands, void* a, void* b,
+                      std::size_t min_keep, double drop_tol, double* lambdas, double* orbs,
+                      std::size_t* k_out, double* defect, double* timings4) {
+  return guarded([&] {
+    const std::size_t n = static_cast<OpH*>(a)->op.dimension();
+    RitzTimings t;
+    const OrbitalSet set = rayleigh_ritz(unpack(k, n, cands), static_cast<OpH*>(a)->op,
+                                         static_cast<OpH*>(b)->op, static_cast<SpaceH*>(sp)->space,
+                                         min_keep, drop_tol, &t);
+    *k_out = set.count();
+    for (std::size_t j = 0; j < set.count(); ++j) lambdas[j] = set.lambdas[j];
+    pack(set.orbitals, orbs);
+    *defect = set.gram_defect;
+    if (timings4) {
+      timings4[0] = t.t_orthonormalize;
+      timings4[1] = t.t_pencil;
+      timings4[2] = t.t_dense;
+      timings4[3] = t.t_lift;
+    }
+  });
+}
+
+int ref_b_orthonormalize(std::size_t k, std::size_t n, const double* u, void* b, double drop_tol,
+                         double* out, std::size_t* k_out, std::size_t* dropped, std::size_t* n_dropped) {
+  return guarded([&] {
+    const OrthonormalizeResult r = b_orthonormalize(unpack(k, n, u), static_cast<OpH*>(b)->op, drop_tol);
+    *k_out = r.vectors.size();
+    pack(r.vectors, out);
+    *n_dropped = r.dropped.size();
+    for (std::size_t i = 0; i < r.dropped.size(); ++i) dropped[i] = r.dropped[i];
+  });
+}
+
+int ref_gram_defect(std::size_t k, std::size_t n, const double* u, void* b, double* defect) {
+  return guarded([&] { *defect = gram_defect(unpack(k, n, u), static_cast<OpH*>(b)->op); });
+}
+
+// Dense pencil (row-major A, B of size m x m); vectors row-major, columns = eigenvectors.
+int ref_dense_sym_geneig(std::size_t m, const double* a, const double* b, double* vals, double* vecs) {
+  return guarded([&] {
+    DenseSymPencil p;
+    p.a = DenseMatrix(m, m);
+    p.b = DenseMatrix(m, m);
+    for (std::size_t i = 0; i < m; ++i)
+      for (std::size_t j = 0; j < m; ++j) {
+        p.a(i, j) = a[i * m + j];
+        p.b(i, j) = b[i * m + j];
+      }
+    const EigenPairs e = dense_sym_geneig(p);
+    for (std::size_t j = 0; j < m; ++j) vals[j] = e.values[j];
+    for (std::size_t i = 0; i < m; ++i)
+      for (std::size_t j = 0; j < m; ++j) vecs[i * m + j] = e.vectors(i, j);
+  });
+}
+
+int ref_jacobi_eig(std::size_t m, const double* a, double tol, int sweeps, double* vals, double* vecs) {
+  return guarded([&] {
+    DenseMatrix am(m, m);
+    for (std::size_t i = 0; i < m; ++i)
+      for (std::size_t j = 0; j < m; ++j) am(i, j) = a[i * m + j];
+    const EigenPairs e = jacobi_eig(am, tol, sweeps);
+    for (std::size_t j = 0; j < m; ++j) vals[j] = e.values[j];
+    for (std::size_t i = 0; i < m; ++i)
+      for (std::size_t j = 0; j < m; ++j) vecs[i * m + j] = e.vectors(i, j);
+  });
+}
+
+void ref_fix_sign(std::size_t n, double* v) { fix_sign(std::span<double>(v, n)); }
+
+// ----------------------------------------------------------------- model ----
+int ref_density(void* sp, std::size_t nocc, const double* u, const double* occ, double* rho,
+                double* raw) {
+  return guarded([&] {
+    auto space = static_cast<SpaceH*>(sp)->space;
+    const std::size_t n = space->dof_count();
+    std::vector<DiscreteFunction> orbs;
+    for (std::size_t i = 0; i < nocc; ++i) orbs.emplace_back(space, std::vector<double>(u + i * n, u + (i + 1) * n));
+    const Density d = density_from_orbitals(orbs, std::vector<double>(occ, occ + nocc));
+    std::memcpy(rho, d.rho.coeffs.data(), n * sizeof(double));
+    *raw = d.raw_integral;
+  });
+}
+
+int ref_mix(void* sp, const double* rin, const double* rout, double alpha, double* mixed) {
+  return guarded([&] {
+    auto space = static_cast<SpaceH*>(sp)->space;
+    const Density a = make_density(space, rin, 1), b = make_density(space, rout, 1);
+    const Density m = mix_density(a, b, alpha);
+    std::memcpy(mixed, m.rho.coeffs.data(), space->dof_count() * sizeof(double));
+  });
+}
+
+int ref_hartree(void* sp, void* poisson, void* mass, const double* rho, double tol, double* vh) {
+  return guarded([&] {
+    auto space = static_cast<SpaceH*>(sp)->space;
+    const Density d = make_density(space, rho, 1);
+    const DiscreteFunction v = hartree_solve_with(static_cast<OpH*>(poisson)->op, static_cast<OpH*>(mass)->op, d, space, tol);
+    std::memcpy(vh, v.coeffs.data(), space->dof_count() * sizeof(double));
+  });
+}
+
+int ref_lda(double rho, int exchange_only, double* v, double* e) {
+  const LdaXc x = lda_vxc(rho, exchange_only ? XcModel::exchange_only : XcModel::lda_pz81);
+  *v = x.v_xc;
+  *e = x.eps_xc;
+  return x.clamped ? 1 : 0;
+}
+
+int ref_total_energy(void* sp, std::size_t nl, const double* lambdas, std::size_t nocc,
+                     const double* rho, const double* vh, int exchange_only, int nnuc,
+                     const double* z, const double* r, double* e_out) {
+  return guarded([&] {
+    auto space = static_cast<SpaceH*>(sp)->space;
+    const Density d = make_density(space, rho, nocc);
+    DiscreteFunction v(space, std::vector<double>(vh, vh + space->dof_count()));
+    *e_out = total_energy(std::vector<double>(lambdas, lambdas + nl), d, v,
+                          exchange_only ? XcModel::exchange_only : XcModel::lda_pz81,
+                          make_molecule(nnuc, z, r, static_cast<int>(2 * nocc)));
+  });
+}
+
+double ref_norm_l2(void* sp, const double* f) {
+  auto space = static_cast<SpaceH*>(sp)->space;
+  return norm_l2(DiscreteFunction(space, std::vector<double>(f, f + space->dof_count())));
+}
+double ref_integrate(void* sp, const double* f) {
+  auto space = static_cast<SpaceH*>(sp)->space;
+  return integrate(DiscreteFunction(space, std::vector<double>(f, f + space->dof_count())));
+}
+double ref_nuclear_repulsion(int nnuc, const double* z, const double* r) {
+  return nuclear_repulsion(make_molecule(nnuc, z, r, 2));
+}
+
+// ------------------------------------------------------------ quadrature ----
+// levels < 0: simplex_rule(dim, degree); else subdivided_rule(dim, degree, levels).
+std::size_t ref_quad_rule(int dim, int degree, int levels, double* points4, double* weights) {
+  const QuadratureRule& r = levels < 0 ? simplex_rule(dim, degree) : subdivided_rule(dim, degree, levels);
+  if (points4) {
+    for (std::size_t q = 0; q < r.points.size(); ++q) {
+      for (int c = 0; c < 4; ++c) points4[4 * q + c] = r.points[q][c];
+      weights[q] = r.weights[q];
+    }
+  }
+  return r.points.size();
+}
+
+// ------------------------------------------------------- Kohn-Sham model ----
+void* ref_ks_create(void* sp, int nnuc, const double* z, const double* r, int n_electrons,
+                    double eps, int exchange_only) {
+  KsH* h = nullptr;
+  guarded([&] {
+    auto space = static_cast<SpaceH*>(sp)->space;
+    KsSetup setup;
+    setup.molecule = make_molecule(nnuc, z, r, n_electrons);
+    setup.box = space->mesh().domain_box();
+    ParoConfig cfg;
+    cfg.vext_smoothing = eps;
+    cfg.xc = exchange_only ? XcModel::exchange_only : XcModel::lda_pz81;
+    KsModel model = make_ks_model(setup, cfg);
+    AssemblyOptions ao;
+    KsOperators ops = assemble_ks_operators(space, model, ao);
+    h = new KsH{space, std::move(model), std::move(ops)};
+  });
+  return h;
+}
+void ref_ks_free(void* h) { delete static_cast<KsH*>(h); }
+// which: 0 mass, 1 kinetic, 2 vext_mass, 3 poisson. Returns a borrowed copy handle.
+void* ref_ks_op(void* h, int which) {
+  KsH* k = static_cast<KsH*>(h);
+  const SparseOperator& op = which == 0 ? k->ops.mass : which == 1 ? k->ops.kinetic : which == 2 ? k->ops.vext_mass : k->ops.poisson;
+  return new OpH{op};
+}
+// ks_form_matrix (paro.cpp:446-454) for a nodal density and Hartree potential.
+void* ref_ks_form(void* h, const double* rho, const double* vh, long* clamped) {
+  OpH* out = nullptr;
+  guarded([&] {
+    KsH* k = static_cast<KsH*>(h);
+    const Density d = make_density(k->space, rho, k->model.n_occupied);
+    DiscreteFunction v(k->space, std::vector<double>(vh, vh + k->space->dof_count()));
+    AssemblyOptions ao;
+    out = new OpH{ks_form_matrix(k->ops, k->model, d, v, clamped, ao)};
+  });
+  return out;
+}
+
+// Initial state from injected guess vectors: rayleigh_ritz on the core
+// Hamiltonian (kinetic + V_ext, the V_H = V_xc = 0 linearisation of
+// paro.cpp:499-502) with min_keep = K, then rho_in from the first N orbitals
+// (paro.cpp:504-505). Returns a loop-state handle.
+void* ref_ks_state_create(void* h, std::size_t k, const double* guess, double cg_tol_start,
+                          double cg_tol, double cg_tol_factor, std::size_t cg_max_iter,
+                          double mixing_alpha, double drop_tol, int workers) {
+  KsState* st = nullptr;
+  guarded([&] {
+    KsH* ks = static_cast<KsH*>(h);
+    auto s = new KsState();
+    s->ks = ks;
+    s->cfg.n_orbitals = ks->model.n_occupied;
+    s->cfg.cg_tol_start = cg_tol_start;
+    s->cfg.cg_tol = cg_tol;
+    s->cfg.cg_tol_factor = cg_tol_factor;
+    s->cfg.cg_max_iter = cg_max_iter;
+    s->cfg.mixing_alpha = mixing_alpha;
+    s->cfg.drop_tol = drop_tol;
+    s->cfg.workers = workers;
+    const std::size_t n = ks->space->dof_count();
+    SparseOperator a0 = ks->ops.kinetic;
+    a0.add_scaled(ks->ops.vext_mass);
+    s->orbitals = rayleigh_ritz(unpack(k, n, guess), a0, ks->ops.mass, ks->space, k, drop_tol);
+    s->rho_in = density_from_orbitals(occupied_functions(ks->space, s->orbitals.orbitals, ks->model.n_occupied),
+                                      ks->model.occupations);
+    st = s;
+  });
+  return st;
+}
+void ref_ks_state_free(void* s) { delete static_cast<KsState*>(s); }
+std::size_t ref_ks_state_k(void* s) { return static_cast<KsState*>(s)->orbitals.count(); }
+
+// One fixed-mesh outer iteration n (0-based), paro.cpp:514-638 with
+// adaptive = false and the Step-2 estimator omitted; no stop tests.
+// out6: [e_tot, rho_residual, sigma, gram_defect, t_source, t_project]
+int ref_ks_state_step(void* sv, int n, double* lambdas_out, double* out6) {
+  return guarded([&] {
+    KsState* s = static_cast<KsState*>(sv);
+    KsH* ks = s->ks;
+    const auto& space = ks->space;
+    const double hartree_tol = 1e-11;
+    DiscreteFunction vh_in = hartree_solve_with(ks->ops.poisson, ks->ops.mass, s->rho_in, space, hartree_tol);
+    auto t0 = Clock::now();
+    const SparseOperator a_in = ks_form_matrix(ks->ops, ks->model, s->rho_in, vh_in, &s->clamped, {});
+    SourceSolveOptions sopts;
+    sopts.tol = cg_tol_for_iteration(s->cfg, n);
+    sopts.max_iter = s->cfg.cg_max_iter;
+    sopts.workers = s->cfg.workers;
+    const StepOutcome step = shifted_source_step(a_in, ks->ops.mass, s->orbitals, sopts);
+    const double t_source = seconds_since(t0);
+    t0 = Clock::now();
+    const Density rho_half = density_from_orbitals(occupied_functions(space, step.half, ks->model.n_occupied),
+                                                   ks->model.occupations);
+    const DiscreteFunction vh_half = hartree_solve_with(ks->ops.poisson, ks->ops.mass, rho_half, space, hartree_tol);
+    const SparseOperator a_half = ks_form_matrix(ks->ops, ks->model, rho_half, vh_half, &s->clamped, {});
+    s->orbitals = rayleigh_ritz(step.half, a_half, ks->ops.mass, space, ks->model.n_occupied, s->cfg.drop_tol);
+    const double t_project = seconds_since(t0);
+    s->rho_out = density_from_orbitals(occupied_functions(space, s->orbitals.orbitals, ks->model.n_occupied),
+                                       ks->model.occupations);
+    const DiscreteFunction vh_out = hartree_solve_with(ks->ops.poisson, ks->ops.mass, s->rho_out, space, hartree_tol);
+    const double e_tot = total_energy(s->orbitals.lambdas, s->rho_out, vh_out, ks->model.xc, ks->model.molecule);
+    DiscreteFunction diff = s->rho_out.rho;
+    for (std::size_t i = 0; i < diff.coeffs.size(); ++i) diff.coeffs[i] -= s->rho_in.rho.coeffs[i];
+    const double rho_res = norm_l2(diff);
+    for (std::size_t j = 0; j < s->orbitals.count(); ++j) lambdas_out[j] = s->orbitals.lambdas[j];
+    out6[0] = e_tot;
+    out6[1] = rho_res;
+    out6[2] = step.sigma;
+    out6[3] = s->orbitals.gram_defect;
+    out6[4] = t_source;
+    out6[5] = t_project;
+    s->rho_in = mix_density(s->rho_in, s->rho_out, s->cfg.mixing_alpha);
+  });
+}
+
+// which: 0 orbitals (K x n), 1 rho_in (current, after mixing), 2 rho_out, 3 lambdas (K)
+void ref_ks_state_get(void* sv, int which, double* out) {
+  KsState* s = static_cast<KsState*>(sv);
+  if (which == 0) pack(s->orbitals.orbitals, out);
+  if (which == 1) std::memcpy(out, s->rho_in.rho.coeffs.data(), s->rho_in.rho.coeffs.size() * sizeof(double));
+  if (which == 2) std::memcpy(out, s->rho_out.rho.coeffs.data(), s->rho_out.rho.coeffs.size() * sizeof(double));
+  if (which == 3)
+    for (std::size_t j = 0; j < s->orbitals.count(); ++j) out[j] = s->orbitals.lambdas[j];
+}
+long ref_ks_state_clamped(void* sv) { return static_cast<KsState*>(sv)->clamped; }
+
+// --------------------------------------------------------- linear loop ------
+void* ref_lin_state_create(void* sp, void* a, void* b, std::size_t k, std::size_t n_orbitals,
+                           const double* guess, double cg_tol_start, double cg_tol,
+                           double cg_tol_factor, std::size_t cg_max_iter, double drop_tol, int workers) {
+  LinState* st = nullptr;
+  guarded([&] {
+    auto s = new LinState();
+    s->space = static_cast<SpaceH*>(sp)->space;
+    s->a = &static_cast<OpH*>(a)->op;
+    s->b = &static_cast<OpH*>(b)->op;
+    s->cfg.n_orbitals = n_orbitals;
+    s->cfg.cg_tol_start = cg_tol_start;
+    s->cfg.cg_tol = cg_tol;
+    s->cfg.cg_tol_factor = cg_tol_factor;
+    s->cfg.cg_max_iter = cg_max_iter;
+    s->cfg.drop_tol = drop_tol;
+    s->cfg.workers = workers;
+    const std::size_t n = s->space->dof_count();
+    s->orbitals = rayleigh_ritz(unpack(k, n, guess), *s->a, *s->b, s->space, k, drop_tol);
+    st = s;
+  });
+  return st;
+}
+void ref_lin_state_free(void* s) { delete static_cast<LinState*>(s); }
+
+// One fixed-mesh linear iteration (paro.cpp:340-354). out4: [sigma, gram_defect, t_source, t_project]
+int ref_lin_state_step(void* sv, int n, double* lambdas_out, double* out4) {
+  return guarded([&] {
+    LinState* s = static_cast<LinState*>(sv);
+    auto t0 = Clock::now();
+    SourceSolveOptions sopts;
+    sopts.tol = cg_tol_for_iteration(s->cfg, n);
+    sopts.max_iter = s->cfg.cg_max_iter;
+    sopts.workers = s->cfg.workers;
+    const StepOutcome step = shifted_source_step(*s->a, *s->b, s->orbitals, sopts);
+    const double t_source = seconds_since(t0);
+    t0 = Clock::now();
+    s->orbitals = rayleigh_ritz(step.half, *s->a, *s->b, s->space, s->cfg.n_orbitals, s->cfg.drop_tol);
+    const double t_project = seconds_since(t0);
+    for (std::size_t j = 0; j < s->orbitals.count(); ++j) lambdas_out[j] = s->orbitals.lambdas[j];
+    out4[0] = step.sigma;
+    out4[1] = s->orbitals.gram_defect;
+    out4[2] = t_source;
+    out4[3] = t_project;
+  });
+}
+void ref_lin_state_get(void* sv, int which, double* out) {
+  LinState* s = static_cast<LinState*>(sv);
+  if (which == 0) pack(s->orbitals.orbitals, out);
+  if (which == 3)
+    for (std::size_t j = 0; j < s->orbitals.count(); ++j) out[j] = s->orbitals.lambdas[j];
+}
+std::size_t ref_lin_state_k(void* s) { return static_cast<LinState*>(s)->orbitals.count(); }
+
+}  // extern "C"

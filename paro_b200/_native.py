@@ -1,0 +1,130 @@
+"""ctypes binding of the C ABI (include/paro_b200.h) -> paro_b200/_lib/libparo_b200.so.
+
+There is no CPU fallback: if the native library or a GPU is missing, the
+product path raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+_LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libparo_b200.so"
+
+_P = C.c_void_p
+_D = C.c_double
+_DP = C.POINTER(C.c_double)
+_SZ = C.c_size_t
+_SZP = C.POINTER(C.c_size_t)
+_LL = C.c_longlong
+_I = C.c_int
+
+
+class Error(RuntimeError):
+    """paro::Error (proj/include/paro/errors.hpp:10-13)."""
+
+    code = 1
+
+    def __init__(self, msg: str = "", residual: float = 0.0):
+        super().__init__(msg)
+        self.residual = residual
+
+
+class InvalidArgumentError(Error):
+    code = 2
+
+
+class NotSpdError(Error):
+    code = 3
+
+
+class IterationLimitError(Error):
+    """Carries the final relative residual (errors.hpp:30-33)."""
+
+    code = 4
+
+
+class DegenerateSpanError(Error):
+    code = 5
+
+
+class PencilError(Error):
+    code = 6
+
+
+class EmptyBasisError(Error):
+    code = 7
+
+
+class CapacityError(Error):
+    code = 8
+
+
+class LineageError(Error):
+    code = 9
+
+
+class CudaError(Error):
+    code = 20
+
+
+ERRORS = {c.code: c for c in (Error, InvalidArgumentError, NotSpdError, IterationLimitError, DegenerateSpanError,
+                              PencilError, EmptyBasisError, CapacityError, LineageError, CudaError)}
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "paro_ctx_create": (_I, [_I, _P, C.POINTER(_P)]),
+    "paro_ctx_destroy": (_I, [_P]),
+    "paro_ctx_set_stream": (_I, [_P, _P]),
+    "paro_ctx_last_error": (C.c_char_p, [_P]),
+    "paro_ctx_last_residual": (_D, [_P]),
+    "paro_ctx_launches": (C.c_ulonglong, [_P]),
+    "paro_ctx_synchronize": (_I, [_P]),
+    "paro_malloc": (_I, [_P, _SZ, C.POINTER(_P)]),
+    "paro_free": (_I, [_P, _P]),
+    "paro_memcpy_h2d": (_I, [_P, _P, _P, _SZ]),
+    "paro_memcpy_d2h": (_I, [_P, _P, _P, _SZ]),
+    "paro_grid_init": (_I, [_P, _I, _D, _D]),
+    "paro_grid_dofs": (_LL, [_P]),
+    "paro_op_create_const": (_I, [_P, _DP, C.POINTER(_P)]),
+    "paro_op_create_var": (_I, [_P, C.POINTER(_P)]),
+    "paro_op_from_csr": (_I, [_P, _SZ, _SZP, C.POINTER(C.c_uint32), _DP, C.POINTER(_P)]),
+    "paro_op_to_csr": (_I, [_P, _P, _SZP, _SZP, C.POINTER(C.c_uint32), _DP]),
+    "paro_op_coefficients": (_I, [_P, C.POINTER(_DP)]),
+    "paro_op_weights": (_I, [_P, _DP, C.POINTER(_I)]),
+    "paro_op_destroy": (_I, [_P]),
+    "paro_op_apply": (_I, [_P, _P, _P, _D, _I, _P, _LL, _P, _LL]),
+    "paro_cg_solve": (_I, [_P, _P, _I, _P, _P, _LL, _D, _SZ, _I, _P, _SZP, _DP]),
+    "paro_source_solve_step": (_I, [_P, _P, _P, _I, _P, _LL, _DP, _D, _SZ, _D, _P, _SZP, _DP]),
+    "paro_shifted_source_step": (_I, [_P, _P, _P, _I, _P, _LL, _DP, _D, _SZ, _P, _DP, _SZP, _DP]),
+    "paro_hartree_solve": (_I, [_P, _P, _P, _P, _D, _P, _SZP]),
+}
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not _LIB_PATH.exists():
+            raise ImportError(f"paro_b200 native library missing ({_LIB_PATH}); run `python -m paro_b200.build`")
+        L = C.CDLL(str(_LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name, None)
+            if f is None:
+                continue
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def library_path() -> Path:
+    return _LIB_PATH
+
+
+def check(ctx_handle, status: int) -> None:
+    if status != 0:
+        L = lib()
+        msg = (L.paro_ctx_last_error(ctx_handle) or b"").decode()
+        res = L.paro_ctx_last_residual(ctx_handle)
+        raise ERRORS.get(status, Error)(msg, res)

@@ -1,0 +1,269 @@
+"""Host mirror of the reference's solver/operator interface over the C ABI.
+
+Names, argument meaning and error behaviour follow proj/include/paro
+(linalg.hpp, paro.hpp, model.hpp); vectors are torch float64 CUDA tensors of
+shape [n] or [k, n] (k orbitals, interior-dof order). The heavy lifting (CG
+loop, Gram/pencil, assembly) runs natively; this module only marshals.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+_DP = C.POINTER(C.c_double)
+
+
+def _ptr(t: torch.Tensor):
+    return C.c_void_p(t.data_ptr())
+
+
+def _as_cols(x: torch.Tensor, n: int) -> torch.Tensor:
+    if x.dim() == 1:
+        x = x.unsqueeze(0)
+    if x.dtype != torch.float64 or not x.is_cuda:
+        raise N.InvalidArgumentError("paro_b200: vectors must be float64 CUDA tensors")
+    if x.shape[1] != n or x.stride(1) != 1:
+        raise N.InvalidArgumentError("paro_b200: vector length does not match the grid")
+    return x
+
+
+class Context:
+    """One paro_ctx bound to a CUDA device and (by default) torch's current stream."""
+
+    def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paro_b200 requires a CUDA device (no CPU fallback)")
+        self.device = torch.device("cuda", device)
+        self.stream = stream or torch.cuda.current_stream(self.device)
+        h = C.c_void_p()
+        st = N.lib().paro_ctx_create(device, C.c_void_p(self.stream.cuda_stream), C.byref(h))
+        if st != 0:
+            raise N.ERRORS.get(st, N.Error)(N.lib().paro_ctx_last_error(None).decode())
+        self.h = h
+        self.s = None
+        self.n = 0
+
+    def close(self):
+        if getattr(self, "h", None):
+            N.lib().paro_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, st: int):
+        N.check(self.h, st)
+
+    def set_stream(self, stream: torch.cuda.Stream):
+        self.stream = stream
+        self.check(N.lib().paro_ctx_set_stream(self.h, C.c_void_p(stream.cuda_stream)))
+
+    def grid(self, subdivisions: int, lo: float, hi: float) -> "Context":
+        """create_box_mesh([lo,hi]^3, subdivisions) + FeSpace::create (mesh.cpp:411-478)."""
+        self.check(N.lib().paro_grid_init(self.h, subdivisions, lo, hi))
+        self.s, self.lo, self.hi = subdivisions, lo, hi
+        self.S = subdivisions - 1
+        self.n = N.lib().paro_grid_dofs(self.h)
+        self.hgrid = (hi - lo) / subdivisions
+        return self
+
+    def launches(self) -> int:
+        return int(N.lib().paro_ctx_launches(self.h))
+
+    def synchronize(self):
+        self.check(N.lib().paro_ctx_synchronize(self.h))
+
+    def empty(self, *shape) -> torch.Tensor:
+        return torch.empty(*shape, dtype=torch.float64, device=self.device)
+
+    def zeros(self, *shape) -> torch.Tensor:
+        return torch.zeros(*shape, dtype=torch.float64, device=self.device)
+
+
+class Operator:
+    """SparseOperator (linalg.hpp:14-50) as a 15-point P1/Kuhn stencil."""
+
+    def __init__(self, ctx: Context, handle):
+        self.ctx = ctx
+        self.h = handle
+        w = (C.c_double * 8)()
+        var = C.c_int(0)
+        ctx.check(N.lib().paro_op_weights(self.h, w, C.byref(var)))
+        self.variable = bool(var.value)
+        self.weights = np.array(list(w))
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                N.lib().paro_op_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    @classmethod
+    def constant(cls, ctx: Context, w) -> "Operator":
+        arr = (C.c_double * 8)(*[float(v) for v in w])
+        h = C.c_void_p()
+        ctx.check(N.lib().paro_op_create_const(ctx.h, arr, C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def variable_empty(cls, ctx: Context) -> "Operator":
+        h = C.c_void_p()
+        ctx.check(N.lib().paro_op_create_var(ctx.h, C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def from_csr(cls, ctx: Context, rows, cols, vals) -> "Operator":
+        """SparseOperator(n, row_offsets, cols, vals) -> stencil (pattern-checked)."""
+        rows = np.ascontiguousarray(rows, np.uintp)
+        cols = np.ascontiguousarray(cols, np.uint32)
+        vals = np.ascontiguousarray(vals, np.float64)
+        h = C.c_void_p()
+        ctx.check(N.lib().paro_op_from_csr(ctx.h, len(rows) - 1, rows.ctypes.data_as(C.POINTER(C.c_size_t)),
+                                           cols.ctypes.data_as(C.POINTER(C.c_uint32)), vals.ctypes.data_as(_DP),
+                                           C.byref(h)))
+        return cls(ctx, h)
+
+    def coefficients(self) -> torch.Tensor:
+        """Device view [8, n] of a variable operator's SoA coefficients."""
+        p = _DP()
+        self.ctx.check(N.lib().paro_op_coefficients(self.h, C.byref(p)))
+        n = self.ctx.n
+        addr = C.cast(p, C.c_void_p).value
+        return _wrap_device(addr, (8, n), self.ctx.device, owner=self)
+
+    def to_csr(self):
+        nnz = C.c_size_t(0)
+        self.ctx.check(N.lib().paro_op_to_csr(self.ctx.h, self.h, C.byref(nnz), None, None, None))
+        rows = np.zeros(self.ctx.n + 1, np.uintp)
+        cols = np.zeros(nnz.value, np.uint32)
+        vals = np.zeros(nnz.value, np.float64)
+        self.ctx.check(N.lib().paro_op_to_csr(self.ctx.h, self.h, C.byref(nnz),
+                                              rows.ctypes.data_as(C.POINTER(C.c_size_t)),
+                                              cols.ctypes.data_as(C.POINTER(C.c_uint32)), vals.ctypes.data_as(_DP)))
+        return rows.astype(np.int64), cols, vals
+
+    def apply(self, x: torch.Tensor, shift: "Operator | None" = None, sigma: float = 0.0,
+              out: torch.Tensor | None = None) -> torch.Tensor:
+        """y = (A + sigma*shift) x  (SparseOperator::apply / matvec, linalg.cpp:88-100)."""
+        squeeze = x.dim() == 1
+        xc = _as_cols(x, self.ctx.n)
+        y = out if out is not None else torch.empty_like(xc)
+        y = _as_cols(y, self.ctx.n)
+        if xc.stride(0) != y.stride(0):
+            raise N.InvalidArgumentError("apply: x and y strides differ")
+        ld = xc.stride(0) if xc.shape[0] > 1 else self.ctx.n
+        self.ctx.check(N.lib().paro_op_apply(self.ctx.h, self.h, shift.h if shift else None, sigma, xc.shape[0],
+                                             _ptr(xc), ld, _ptr(y), ld))
+        return y[0] if squeeze else y
+
+
+def _wrap_device(addr: int, shape, device, owner=None) -> torch.Tensor:
+    """Zero-copy torch view of device memory owned by the native library."""
+    numel = int(np.prod(shape))
+
+    class _Holder:
+        __cuda_array_interface__ = {"shape": (numel,), "typestr": "<f8", "data": (addr, False), "version": 3,
+                                    "strides": None}
+
+    h = _Holder()
+    t = torch.as_tensor(h, device=device).view(*shape)
+    t._paro_owner = owner  # keep the operator alive while the view exists
+    return t
+
+
+@dataclass
+class CgResult:
+    """CgResult (linalg.hpp:107-112), per column."""
+
+    x: torch.Tensor
+    iterations: list = field(default_factory=list)
+    residual: list = field(default_factory=list)
+    converged: list = field(default_factory=list)
+
+
+def cg_solve(a: Operator, b: torch.Tensor, x0: torch.Tensor | None = None, tol: float = 1e-10,
+             max_iter: int = 10000, throw_on_max_iter: bool = True) -> CgResult:
+    """cg_solve (linalg.cpp:143-223), Jacobi preconditioner, k right-hand sides at once."""
+    ctx = a.ctx
+    squeeze = b.dim() == 1
+    bc = _as_cols(b, ctx.n).contiguous()
+    k = bc.shape[0]
+    x = torch.empty_like(bc)
+    x0c = _as_cols(x0, ctx.n).contiguous() if x0 is not None else None
+    it = (C.c_size_t * k)()
+    res = (C.c_double * k)()
+    st = N.lib().paro_cg_solve(ctx.h, a.h, k, _ptr(bc), _ptr(x0c) if x0c is not None else None, ctx.n, tol,
+                               max_iter, int(throw_on_max_iter), _ptr(x), it, res)
+    ctx.check(st)
+    iters = list(it)
+    resid = list(res)
+    conv = [r <= tol for r in resid]
+    return CgResult(x[0] if squeeze else x, iters, resid, conv)
+
+
+def source_solve_step(a: Operator, b: Operator, u_prev: torch.Tensor, lambdas, tol: float = 1e-10,
+                      max_iter: int = 100000, sigma: float = 0.0, out: torch.Tensor | None = None,
+                      report: dict | None = None) -> torch.Tensor:
+    """Step 3, source_solve_step (paro.cpp:81-119), all K orbitals in one batch."""
+    ctx = a.ctx
+    u = _as_cols(u_prev, ctx.n)
+    k = u.shape[0]
+    if len(lambdas) != k:
+        raise N.InvalidArgumentError("source_solve_step: orbital/lambda count mismatch")
+    if u.stride(0) != ctx.n:
+        u = u.contiguous()
+    y = out if out is not None else torch.empty_like(u)
+    lam = (C.c_double * k)(*[float(v) for v in lambdas])
+    it = (C.c_size_t * k)()
+    res = (C.c_double * k)()
+    st = N.lib().paro_source_solve_step(ctx.h, a.h, b.h, k, _ptr(u), ctx.n, lam, tol, max_iter, sigma, _ptr(y),
+                                        it, res)
+    if report is not None:
+        report.update(iterations=list(it), residual=list(res))
+    ctx.check(st)
+    return y
+
+
+def shifted_source_step(a: Operator, b: Operator, u_prev: torch.Tensor, lambdas, tol: float = 1e-10,
+                        max_iter: int = 100000, out: torch.Tensor | None = None, report: dict | None = None):
+    """shifted_source_step (paro.cpp:194-210) -> (u_half, sigma)."""
+    ctx = a.ctx
+    u = _as_cols(u_prev, ctx.n)
+    if u.stride(0) != ctx.n:
+        u = u.contiguous()
+    k = u.shape[0]
+    y = out if out is not None else torch.empty_like(u)
+    lam = (C.c_double * k)(*[float(v) for v in lambdas])
+    it = (C.c_size_t * k)()
+    res = (C.c_double * k)()
+    sig = C.c_double(0.0)
+    st = N.lib().paro_shifted_source_step(ctx.h, a.h, b.h, k, _ptr(u), ctx.n, lam, tol, max_iter, _ptr(y),
+                                          C.byref(sig), it, res)
+    if report is not None:
+        report.update(iterations=list(it), residual=list(res), sigma=sig.value)
+    ctx.check(st)
+    return y, sig.value
+
+
+def hartree_solve_with(poisson: Operator, mass: Operator, rho: torch.Tensor, tol: float = 1e-11,
+                       out: torch.Tensor | None = None, report: dict | None = None) -> torch.Tensor:
+    """hartree_solve_with (model.cpp:242-255)."""
+    ctx = poisson.ctx
+    r = _as_cols(rho, ctx.n).contiguous()
+    vh = out if out is not None else ctx.empty(ctx.n)
+    it = C.c_size_t(0)
+    st = N.lib().paro_hartree_solve(ctx.h, poisson.h, mass.h, _ptr(r), tol, _ptr(vh), C.byref(it))
+    if report is not None:
+        report.update(iterations=it.value)
+    ctx.check(st)
+    return vh

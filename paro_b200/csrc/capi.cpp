@@ -1,0 +1,376 @@
+// C ABI (include/paro_b200.h) over the device implementation.
+#include "paro_b200.h"
+
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "ctx.hpp"
+#include "solver.hpp"
+
+struct paro_ctx {
+  paro_b200::Ctx c;
+};
+struct paro_op {
+  paro_b200::Op o;
+  paro_ctx* owner = nullptr;
+};
+
+using namespace paro_b200;
+
+namespace {
+
+thread_local std::string g_noctx_err;
+
+template <typename F>
+int guarded(paro_ctx* ctx, F&& f) {
+  try {
+    if (ctx) PARO_CUDA(cudaSetDevice(ctx->c.device));
+    return f();
+  } catch (const ParoError& e) {
+    if (ctx) {
+      ctx->c.err = e.what();
+      ctx->c.resid = e.residual;
+    } else {
+      g_noctx_err = e.what();
+    }
+    return e.code;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->c.err = e.what();
+    else g_noctx_err = e.what();
+    return kError;
+  }
+}
+
+void dof_xyz(long long i, int S, int& x, int& y, int& z) {
+  x = static_cast<int>(i % S);
+  y = static_cast<int>((i / S) % S);
+  z = static_cast<int>(i / (static_cast<long long>(S) * S));
+}
+
+}  // namespace
+
+extern "C" {
+
+int paro_ctx_create(int device, void* stream, paro_ctx** out) {
+  return guarded(nullptr, [&] {
+    auto* ctx = new paro_ctx();
+    ctx->c.device = device;
+    PARO_CUDA(cudaSetDevice(device));
+    ctx->c.stream = static_cast<cudaStream_t>(stream);
+    if (cublasCreate(&ctx->c.cublas) != CUBLAS_STATUS_SUCCESS) throw ParoError(kCuda, "cublasCreate failed");
+    cublasSetStream(ctx->c.cublas, ctx->c.stream);
+    PARO_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->c.pinned_count), sizeof(int), cudaHostAllocMapped));
+    PARO_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->c.pinned_count_dev), ctx->c.pinned_count, 0));
+    *out = ctx;
+    return kOk;
+  });
+}
+
+int paro_ctx_destroy(paro_ctx* ctx) {
+  if (!ctx) return kOk;
+  cudaSetDevice(ctx->c.device);
+  cudaStreamSynchronize(ctx->c.stream);
+  for (DevBuf* b : {&ctx->c.partials, &ctx->c.cols, &ctx->c.scale, &ctx->c.invd, &ctx->c.pbuf0, &ctx->c.pbuf1,
+                    &ctx->c.flag, &ctx->c.ws_a, &ctx->c.ws_b, &ctx->c.ws_c, &ctx->c.ws_small, &ctx->c.ws_small2,
+                    &ctx->c.ws_small3})
+    b->release();
+  if (ctx->c.cublas) cublasDestroy(ctx->c.cublas);
+  if (ctx->c.pinned_count) cudaFreeHost(ctx->c.pinned_count);
+  delete ctx;
+  return kOk;
+}
+
+int paro_ctx_set_stream(paro_ctx* ctx, void* stream) {
+  return guarded(ctx, [&] {
+    ctx->c.stream = static_cast<cudaStream_t>(stream);
+    cublasSetStream(ctx->c.cublas, ctx->c.stream);
+    return kOk;
+  });
+}
+
+const char* paro_ctx_last_error(const paro_ctx* ctx) { return ctx ? ctx->c.err.c_str() : g_noctx_err.c_str(); }
+double paro_ctx_last_residual(const paro_ctx* ctx) { return ctx ? ctx->c.resid : 0.0; }
+unsigned long long paro_ctx_launches(const paro_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+int paro_ctx_synchronize(paro_ctx* ctx) {
+  return guarded(ctx, [&] {
+    PARO_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    return kOk;
+  });
+}
+
+int paro_malloc(paro_ctx* ctx, size_t bytes, void** dev) {
+  return guarded(ctx, [&] {
+    PARO_CUDA(cudaMalloc(dev, bytes));
+    return kOk;
+  });
+}
+int paro_free(paro_ctx* ctx, void* dev) {
+  return guarded(ctx, [&] {
+    PARO_CUDA(cudaFree(dev));
+    return kOk;
+  });
+}
+int paro_memcpy_h2d(paro_ctx* ctx, void* dev, const void* host, size_t bytes) {
+  return guarded(ctx, [&] {
+    PARO_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, ctx->c.stream));
+    PARO_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    return kOk;
+  });
+}
+int paro_memcpy_d2h(paro_ctx* ctx, void* host, const void* dev, size_t bytes) {
+  return guarded(ctx, [&] {
+    PARO_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, ctx->c.stream));
+    PARO_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    return kOk;
+  });
+}
+
+int paro_grid_init(paro_ctx* ctx, int subdivisions, double lo, double hi) {
+  return guarded(ctx, [&] {
+    if (subdivisions < 2) throw ParoError(kInvalidArgument, "grid: subdivisions must be >= 2");
+    if (!(hi - lo > 0.0)) throw ParoError(kInvalidArgument, "grid: box has non-positive edge length");
+    Grid& g = ctx->c.grid;
+    g.s = subdivisions;
+    g.S = subdivisions - 1;
+    g.n = static_cast<long long>(g.S) * g.S * g.S;
+    g.lo = lo;
+    g.hi = hi;
+    ctx->c.grid_set = true;
+    return kOk;
+  });
+}
+
+long long paro_grid_dofs(const paro_ctx* ctx) { return ctx && ctx->c.grid_set ? ctx->c.grid.n : 0; }
+
+int paro_op_create_const(paro_ctx* ctx, const double w[8], paro_op** out) {
+  return guarded(ctx, [&] {
+    auto* op = new paro_op();
+    op->owner = ctx;
+    op->o.var = false;
+    for (int o = 0; o < kSlots; ++o) op->o.w[o] = w[o];
+    op->o.n = ctx->c.grid.n;
+    *out = op;
+    return kOk;
+  });
+}
+
+int paro_op_create_var(paro_ctx* ctx, paro_op** out) {
+  return guarded(ctx, [&] {
+    ctx->c.check_grid();
+    auto* op = new paro_op();
+    op->owner = ctx;
+    op->o.var = true;
+    op->o.n = ctx->c.grid.n;
+    PARO_CUDA(cudaMalloc(&op->o.coef, sizeof(double) * kSlots * op->o.n));
+    PARO_CUDA(cudaMemsetAsync(op->o.coef, 0, sizeof(double) * kSlots * op->o.n, ctx->c.stream));
+    op->o.owns = true;
+    *out = op;
+    return kOk;
+  });
+}
+
+int paro_op_from_csr(paro_ctx* ctx, size_t n, const size_t* rows, const uint32_t* cols, const double* vals,
+                     paro_op** out) {
+  return guarded(ctx, [&] {
+    ctx->c.check_grid();
+    const int S = ctx->c.grid.S;
+    if (static_cast<long long>(n) != ctx->c.grid.n)
+      throw ParoError(kInvalidArgument, "op_from_csr: dimension does not match the grid");
+    std::vector<double> coef(static_cast<size_t>(kSlots) * n, 0.0);
+    double scale = 0.0;
+    for (size_t k = 0; k < rows[n]; ++k) scale = std::max(scale, std::abs(vals[k]));
+    struct Back {
+      size_t j;
+      int o;
+      double v;
+    };
+    std::vector<Back> back;
+    back.reserve(7 * n);
+    for (size_t i = 0; i < n; ++i) {
+      int x, y, z;
+      dof_xyz(static_cast<long long>(i), S, x, y, z);
+      for (size_t k = rows[i]; k < rows[i + 1]; ++k) {
+        const size_t j = cols[k];
+        if (j >= n) throw ParoError(kInvalidArgument, "op_from_csr: column out of range");
+        int xj, yj, zj;
+        dof_xyz(static_cast<long long>(j), S, xj, yj, zj);
+        const int dx = xj - x, dy = yj - y, dz = zj - z;
+        const bool fwd = (dx == 0 || dx == 1) && (dy == 0 || dy == 1) && (dz == 0 || dz == 1);
+        const bool bwd = (dx == 0 || dx == -1) && (dy == 0 || dy == -1) && (dz == 0 || dz == -1);
+        if (!fwd && !bwd) throw ParoError(kInvalidArgument, "op_from_csr: pattern is not the P1/Kuhn stencil");
+        if (fwd) {
+          const int o = dx + 2 * dy + 4 * dz;
+          coef[static_cast<size_t>(o) * n + i] = vals[k];
+        } else {
+          back.push_back({j, -dx - 2 * dy - 4 * dz, vals[k]});
+        }
+      }
+    }
+    for (const Back& b : back) {
+      if (std::abs(coef[static_cast<size_t>(b.o) * n + b.j] - b.v) > 1e-13 * std::max(1.0, scale))
+        throw ParoError(kInvalidArgument, "op_from_csr: matrix is not symmetric");
+    }
+    // uniform operator -> constant stencil (only slots whose neighbour exists)
+    bool uniform = true;
+    double w[kSlots];
+    bool seen[kSlots] = {};
+    for (size_t i = 0; i < n && uniform; ++i) {
+      int x, y, z;
+      dof_xyz(static_cast<long long>(i), S, x, y, z);
+      for (int o = 0; o < kSlots; ++o) {
+        const int ox = o & 1, oy = (o >> 1) & 1, oz = (o >> 2) & 1;
+        if (x + ox >= S || y + oy >= S || z + oz >= S) continue;
+        const double v = coef[static_cast<size_t>(o) * n + i];
+        if (!seen[o]) {
+          w[o] = v;
+          seen[o] = true;
+        } else if (v != w[o]) {
+          uniform = false;
+          break;
+        }
+      }
+    }
+    auto* op = new paro_op();
+    op->owner = ctx;
+    op->o.n = static_cast<long long>(n);
+    if (uniform) {
+      op->o.var = false;
+      for (int o = 0; o < kSlots; ++o) op->o.w[o] = seen[o] ? w[o] : 0.0;
+    } else {
+      op->o.var = true;
+      PARO_CUDA(cudaMalloc(&op->o.coef, sizeof(double) * kSlots * n));
+      PARO_CUDA(cudaMemcpy(op->o.coef, coef.data(), sizeof(double) * kSlots * n, cudaMemcpyHostToDevice));
+      op->o.owns = true;
+    }
+    *out = op;
+    return kOk;
+  });
+}
+
+int paro_op_to_csr(paro_ctx* ctx, const paro_op* a, size_t* nnz, size_t* rows, uint32_t* cols, double* vals) {
+  return guarded(ctx, [&] {
+    ctx->c.check_grid();
+    const int S = ctx->c.grid.S;
+    const long long n = ctx->c.grid.n;
+    std::vector<double> coef;
+    if (a->o.var && vals) {
+      coef.resize(static_cast<size_t>(kSlots) * n);
+      PARO_CUDA(cudaStreamSynchronize(ctx->c.stream));
+      PARO_CUDA(cudaMemcpy(coef.data(), a->o.coef, sizeof(double) * coef.size(), cudaMemcpyDeviceToHost));
+    }
+    auto weight = [&](int o, long long at) { return a->o.var ? coef[static_cast<size_t>(o) * n + at] : a->o.w[o]; };
+    size_t k = 0;
+    const long long S2 = static_cast<long long>(S) * S;
+    for (long long i = 0; i < n; ++i) {
+      int x, y, z;
+      dof_xyz(i, S, x, y, z);
+      if (rows) rows[i] = k;
+      // ascending column order: backward 7..1, centre, forward 1..7
+      for (int pass = 0; pass < 3; ++pass) {
+        for (int t = 1; t <= 7; ++t) {
+          if (pass == 1 && t > 1) break;
+          const int o = pass == 0 ? 8 - t : pass == 1 ? 0 : t;
+          const int ox = o & 1, oy = (o >> 1) & 1, oz = (o >> 2) & 1;
+          const int sg = pass == 0 ? -1 : 1;
+          const int xj = x + sg * ox, yj = y + sg * oy, zj = z + sg * oz;
+          if (xj < 0 || yj < 0 || zj < 0 || xj >= S || yj >= S || zj >= S) continue;
+          const long long j = (static_cast<long long>(zj) * S + yj) * S + xj;
+          if (cols) cols[k] = static_cast<uint32_t>(j);
+          if (vals) vals[k] = pass == 0 ? weight(o, j) : weight(o, i);
+          ++k;
+        }
+      }
+    }
+    if (rows) rows[n] = k;
+    (void)S2;
+    *nnz = k;
+    return kOk;
+  });
+}
+
+int paro_op_coefficients(paro_op* a, double** dev) {
+  if (!a || !a->o.var) return kInvalidArgument;
+  *dev = a->o.coef;
+  return kOk;
+}
+
+int paro_op_weights(const paro_op* a, double w[8], int* is_var) {
+  if (!a) return kInvalidArgument;
+  for (int o = 0; o < kSlots; ++o) w[o] = a->o.w[o];
+  if (is_var) *is_var = a->o.var ? 1 : 0;
+  return kOk;
+}
+
+int paro_op_destroy(paro_op* a) {
+  if (!a) return kOk;
+  if (a->o.owns && a->o.coef) {
+    if (a->owner) cudaSetDevice(a->owner->c.device);
+    cudaFree(a->o.coef);
+  }
+  delete a;
+  return kOk;
+}
+
+int paro_op_apply(paro_ctx* ctx, const paro_op* a, const paro_op* shift, double sigma, int k, const double* x,
+                  long long ldx, double* y, long long ldy) {
+  return guarded(ctx, [&] {
+    apply_op(ctx->c, a->o, shift ? &shift->o : nullptr, sigma, k, x, ldx, y, ldy);
+    return kOk;
+  });
+}
+
+static void fill_report(const SolveReport& r, size_t* iters, double* resid) {
+  for (size_t c = 0; c < r.iterations.size(); ++c) {
+    if (iters) iters[c] = static_cast<size_t>(r.iterations[c]);
+    if (resid) resid[c] = r.residual[c];
+  }
+}
+
+int paro_cg_solve(paro_ctx* ctx, const paro_op* a, int k, const double* b, const double* x0, long long ld,
+                  double tol, size_t max_iter, int throw_on_max, double* x, size_t* iters, double* resid) {
+  return guarded(ctx, [&] {
+    SolveReport rep;
+    const int st = cg_solve(ctx->c, a->o, k, b, x0, ld, tol, max_iter, throw_on_max != 0, x, &rep);
+    fill_report(rep, iters, resid);
+    return st;
+  });
+}
+
+int paro_source_solve_step(paro_ctx* ctx, const paro_op* a, const paro_op* b, int k, const double* u, long long ld,
+                           const double* lambdas, double tol, size_t max_iter, double sigma, double* out,
+                           size_t* iters, double* resid) {
+  return guarded(ctx, [&] {
+    SolveReport rep;
+    const int st = source_solve(ctx->c, a->o, b->o, sigma, k, u, ld, lambdas, tol, max_iter, out, &rep);
+    fill_report(rep, iters, resid);
+    return st;
+  });
+}
+
+int paro_shifted_source_step(paro_ctx* ctx, const paro_op* a, const paro_op* b, int k, const double* u,
+                             long long ld, const double* lambdas, double tol, size_t max_iter, double* out,
+                             double* sigma_out, size_t* iters, double* resid) {
+  return guarded(ctx, [&] {
+    SolveReport rep;
+    const int st = shifted_source_solve(ctx->c, a->o, b->o, k, u, ld, lambdas, tol, max_iter, out, sigma_out, &rep);
+    fill_report(rep, iters, resid);
+    return st;
+  });
+}
+
+int paro_hartree_solve(paro_ctx* ctx, const paro_op* poisson, const paro_op* mass, const double* rho, double tol,
+                       double* vh, size_t* iters) {
+  return guarded(ctx, [&] {
+    SolveReport rep;
+    const int st = hartree_solve(ctx->c, poisson->o, mass->o, rho, tol, vh, &rep);
+    fill_report(rep, iters, nullptr);
+    return st;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,70 @@
+// Host-side context: device, stream, grid, operators and grow-only workspace.
+#pragma once
+
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace paro_b200 {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  template <typename T>
+  T* get(size_t count) {
+    const size_t need = count * sizeof(T);
+    if (need > bytes) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      bytes = 0;
+      PARO_CUDA(cudaMalloc(&p, need));
+      bytes = need;
+    }
+    return static_cast<T*>(p);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+// A stencil operator on the interior lattice. Constant operators (mass,
+// Poisson/kinetic stiffness) carry their 8 weights; variable ones (the KS
+// form, V_ext mass) own 8 SoA coefficient arrays of n doubles on the device.
+struct Op {
+  bool var = false;
+  double w[kSlots] = {};
+  double* coef = nullptr;
+  long long n = 0;
+  bool owns = false;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cublasHandle_t cublas = nullptr;
+  Grid grid;
+  bool grid_set = false;
+  std::string err;
+  double resid = 0.0;
+  unsigned long long launches = 0;   // kernels launched by this library (graph nodes counted)
+
+  DevBuf partials, cols, scale, invd, pbuf0, pbuf1, flag;
+  DevBuf ws_a, ws_b, ws_c, ws_small, ws_small2, ws_small3;
+  int* pinned_count = nullptr;       // mapped host memory for the active-column poll
+  int* pinned_count_dev = nullptr;
+
+  double mass_w[kSlots] = {};        // reference mass stencil on this grid
+  bool mass_set = false;
+
+  void check_grid() const {
+    if (!grid_set) throw ParoError(kInvalidArgument, "paro_b200: grid not initialised");
+  }
+};
+
+}  // namespace paro_b200

@@ -1,0 +1,73 @@
+// Plane-marching 15-point Kuhn/P1 stencil kernels (sm_100a).
+//
+// Every operator on the ParO hot path is, on the uniform Kuhn mesh, the
+// symmetric 15-point stencil of proj/src/fem.cpp:221-321 restricted to the
+// interior lattice. One CTA owns a 32x8 (x,y) tile of the
+// interior lattice and a z-range; it marches up in z keeping a ring of three
+// (x,y) planes per column (with a one-point halo, zero outside the lattice =
+// the Dirichlet elimination of fem.cpp:21-28) in shared memory, prefetching
+// the next plane into registers while the current one is computed. The 15
+// weights of a point are loaded once per plane step and reused for up to CB
+// columns (orbitals), so the coefficient traffic is amortised over the batch.
+//
+// Row sums are accumulated in ascending column order without FMA contraction,
+// exactly like SparseOperator::matvec (proj/src/linalg.cpp:88-94), so an apply
+// is bit-identical to the reference CSR matvec on the same coefficients.
+#pragma once
+
+#include "common.cuh"
+
+namespace paro_b200 {
+
+constexpr int kTX = 32;
+constexpr int kTY = 8;
+constexpr int kNT = kTX * kTY;
+constexpr int kHX = kTX + 2;
+constexpr int kHY = kTY + 2;
+constexpr int kHP = kHX * kHY;              // halo'd plane, 340 points
+constexpr int kLoadsPerThread = (kHP + kNT - 1) / kNT;  // 2
+
+enum MarchMode : int {
+  kApply = 0,       // y = (A + sigma M) x                       [opt. x.y partial]
+  kK1 = 1,          // p_new = z + beta p_old (z = r/d); pq = p_new.(A p_new)
+  kK2 = 2,          // q = A p; x += alpha p; r -= alpha q; rz, rr partials
+  kSetupWarm = 3,   // b = (M u)*scale; r = b - A u; x = u; bb, rz, rr partials
+  kSetupCold = 4,   // b = (M f)*scale; r = b; x = 0;      bb, rz, rr partials
+};
+
+// Operator as seen by the kernels: (A + sigma*M) with A either 8 SoA
+// coefficient arrays (variable) or 8 constants, and M a constant stencil.
+struct OpDev {
+  const double* coef = nullptr;  // slot o at coef + o*n; nullptr -> constant w[]
+  double w[kSlots] = {};         // constant weights
+  double m[kSlots] = {};         // shift stencil (mass) weights
+  double sigma = 0.0;            // add_scaled(b, sigma): fl(w + fl(sigma*m))
+  double invd_const = 0.0;       // 1/diag for the constant case
+};
+
+struct MarchArgs {
+  int S = 0;
+  long long n = 0;
+  int nTX = 0, nTY = 0, nZ = 0, ZC = 0;
+  int nblk = 0;                  // spatial blocks = nTX*nTY*nZ
+  int K = 0;                     // columns in the batch
+  long long ld = 0;              // column stride of every vector operand
+  OpDev op;
+  double mw[kSlots] = {};        // right-hand-side mass stencil (setup modes)
+  const double* src = nullptr;   // plane source (x | p | u | f)
+  const double* pold = nullptr;  // K1: previous direction
+  double* dst = nullptr;         // Apply: y; K1: p_new; Setup: r
+  double* x = nullptr;           // K2 / Setup
+  double* r = nullptr;           // K1 (read) / K2 (read-write)
+  const double* invd = nullptr;  // variable-op inverse diagonal (n)
+  CgColumn* cols = nullptr;      // per-column state (active mask, alpha, beta, first)
+  const double* scale = nullptr; // Setup: rhs scale per column
+  const double* rhs = nullptr;   // Setup (warm): explicit right-hand side instead of (M u)*scale
+  double* partials = nullptr;    // [K][3][nblk]
+  int with_dot = 0;              // Apply: accumulate x.y
+};
+
+void launch_march(int mode, bool var, int cb, const MarchArgs& a, cudaStream_t st);
+void plan_march(MarchArgs& a, int S);
+
+}  // namespace paro_b200

@@ -1,0 +1,462 @@
+// Batched, column-masked Jacobi-PCG on the device (cg_solve, linalg.cpp:143-223)
+// and the Step-3 / Hartree drivers built on it (source_solve_step,
+// paro.cpp:81-119; shifted_source_step, paro.cpp:194-210; hartree_solve_with,
+// model.cpp:242-255).
+//
+// Per CG iteration two fused stencil passes run (march.cu):
+//   K1: p = z + beta p (z = r / diag), pq = p.(A p)       -> finalize: alpha
+//   K2: q = A p, x += alpha p, r -= alpha q, rz, rr       -> finalize: beta, stop test
+// q is recomputed in K2 instead of stored, so one iteration moves
+// 8 doubles per point and column (r,p,p' in K1; p,x,r,x',r' in K2). All
+// scalars (alpha, beta, stop tests, NotSpd / IterationLimit detection) stay on
+// the device; the host only polls an active-column count between CUDA-graph
+// chunks of iterations, keeping one chunk in flight ahead of the poll.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "march.cuh"
+#include "solver.hpp"
+
+namespace paro_b200 {
+
+namespace {
+
+constexpr int kFinThreads = 256;
+
+__device__ double block_sum(double v, double* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s += sh[w];
+  }
+  __syncthreads();
+  return s;  // valid on thread 0
+}
+
+// Fixed-order sum of the per-CTA partials of column c, quantity q.
+__device__ double sum_partials(const double* partials, int c, int q, int nblk, double* sh) {
+  double s = 0.0;
+  const double* p = partials + (static_cast<long long>(c) * 3 + q) * nblk;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) s += p[i];
+  return block_sum(s, sh);
+}
+
+enum FinMode { kFinSetup = 0, kFinK1 = 1, kFinK2 = 2 };
+
+__global__ void fin_kernel(int mode, CgColumn* cols, const double* partials, int nblk, const int* diag_bad) {
+  __shared__ double sh[32];
+  const int c = blockIdx.x;
+  CgColumn& col = cols[c];
+  if (!col.active) return;
+  if (mode == kFinSetup) {
+    const double bb = sum_partials(partials, c, 0, nblk, sh);
+    const double rz = sum_partials(partials, c, 1, nblk, sh);
+    const double rr = sum_partials(partials, c, 2, nblk, sh);
+    if (threadIdx.x != 0) return;
+    const double bnorm = sqrt(bb);
+    col.bnorm = bnorm;
+    col.it = 0;
+    if (bnorm == 0.0) {  // linalg.cpp:158-162: x = 0, converged
+      col.converged = 1;
+      col.active = 0;
+      col.first = 2;     // marks "zero the solution"
+      col.rnorm = 0.0;
+      return;
+    }
+    if (*diag_bad) {     // linalg.cpp:165-167
+      col.status = kNotSpd;
+      col.active = 0;
+      return;
+    }
+    col.rz = rz;
+    col.rnorm = sqrt(rr);
+    col.first = 1;
+    if (col.rnorm / bnorm <= col.tol) {
+      col.converged = 1;
+      col.active = 0;
+    } else if (col.max_iter == 0) {
+      col.status = kIterationLimit;
+      col.active = 0;
+    }
+  } else if (mode == kFinK1) {
+    const double pq = sum_partials(partials, c, 0, nblk, sh);
+    if (threadIdx.x != 0) return;
+    col.pq = pq;
+    if (pq <= 0.0) {  // linalg.cpp:200
+      col.status = kNotSpd;
+      col.active = 0;
+      return;
+    }
+    col.alpha = col.rz / pq;
+  } else {
+    const double rzn = sum_partials(partials, c, 0, nblk, sh);
+    const double rr = sum_partials(partials, c, 1, nblk, sh);
+    if (threadIdx.x != 0) return;
+    col.beta = rzn / col.rz;  // linalg.cpp:207-209
+    col.rz = rzn;
+    col.rnorm = sqrt(rr);
+    col.it += 1;
+    col.first = 0;
+    if (col.rnorm / col.bnorm <= col.tol) {
+      col.converged = 1;
+      col.active = 0;
+    } else if (col.it >= col.max_iter) {
+      col.status = kIterationLimit;
+      col.active = 0;
+    }
+  }
+}
+
+__global__ void count_active_kernel(const CgColumn* cols, int K, int* out) {
+  __shared__ int sh;
+  if (threadIdx.x == 0) sh = 0;
+  __syncthreads();
+  int c = 0;
+  for (int i = threadIdx.x; i < K; i += blockDim.x) c += cols[i].active != 0;
+  atomicAdd(&sh, c);
+  __syncthreads();
+  if (threadIdx.x == 0) *out = sh;
+}
+
+// Columns with bnorm == 0 return x = 0 (linalg.cpp:158-162).
+__global__ void zero_marked_kernel(const CgColumn* cols, int K, double* x, long long ld, long long n) {
+  const int c = blockIdx.y;
+  if (c >= K || cols[c].first != 2) return;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    x[c * ld + i] = 0.0;
+}
+
+// inv_diag = 1 / fl(c0 + fl(sigma*m0)); flags a non-positive diagonal.
+__global__ void invd_kernel(const double* c0, double sigma, double m0, long long n, double* invd, int* bad) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double d = __dadd_rn(c0[i], __dmul_rn(sigma, m0));
+    if (d <= 0.0) *bad = 1;
+    invd[i] = 1.0 / d;
+  }
+}
+
+__global__ void set_flag_kernel(int* flag, int v) { *flag = v; }
+
+int pick_cb(int K) { return K >= 8 ? 8 : K >= 4 ? 4 : K >= 2 ? 2 : 1; }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+
+OpDev make_opdev(const Ctx& ctx, const Op& a, const Op* shift, double sigma) {
+  OpDev d;
+  d.coef = a.var ? a.coef : nullptr;
+  for (int o = 0; o < kSlots; ++o) d.w[o] = a.w[o];
+  if (shift) {
+    for (int o = 0; o < kSlots; ++o) d.m[o] = shift->w[o];
+    d.sigma = sigma;
+  }
+  if (!a.var) d.invd_const = 1.0 / (a.w[0] + d.sigma * d.m[0]);
+  (void)ctx;
+  return d;
+}
+
+void apply_op(Ctx& ctx, const Op& a, const Op* shift, double sigma, int K, const double* x, long long ldx,
+              double* y, long long ldy) {
+  ctx.check_grid();
+  if (ldx != ldy) throw ParoError(kInvalidArgument, "apply: x and y must share a column stride");
+  if (K <= 0) return;
+  if (shift && shift->var) throw ParoError(kInvalidArgument, "apply: shift operator must be a constant stencil");
+  MarchArgs m;
+  plan_march(m, ctx.grid.S);
+  m.K = K;
+  m.ld = ldx;
+  m.op = make_opdev(ctx, a, shift, sigma);
+  m.src = x;
+  m.dst = y;
+  launch_march(kApply, a.var, pick_cb(K), m, ctx.stream);
+  ++ctx.launches;
+}
+
+// Core batched PCG. On entry `cols` (host) holds tol/max_iter per column; the
+// setup pass computes r0 from either (M src)*scale (rhs == nullptr) or rhs.
+// warm: x0 = src (source solves) ; cold: x0 = 0 (Hartree).
+void batched_pcg(Ctx& ctx, const OpDev& op, bool var, int K, const double* src, const double* rhs,
+                 const double* scale_host, bool warm, double* x, long long ld, std::vector<CgColumn>& cols) {
+  const Grid& g = ctx.grid;
+  const long long n = g.n;
+  cudaStream_t st = ctx.stream;
+  MarchArgs m;
+  plan_march(m, g.S);
+  m.K = K;
+  m.ld = ld;
+  m.op = op;
+  for (int o = 0; o < kSlots; ++o) m.mw[o] = ctx.mass_w[o];
+  const int cb = pick_cb(K);
+
+  CgColumn* dcols = ctx.cols.get<CgColumn>(K);
+  double* dscale = ctx.scale.get<double>(K);
+  double* partials = ctx.partials.get<double>(static_cast<size_t>(K) * 3 * m.nblk);
+  double* r = ctx.ws_a.get<double>(static_cast<size_t>(K) * ld);
+  double* p0 = ctx.pbuf0.get<double>(static_cast<size_t>(K) * ld);
+  double* p1 = ctx.pbuf1.get<double>(static_cast<size_t>(K) * ld);
+  int* flag = ctx.flag.get<int>(1);
+
+  PARO_CUDA(cudaMemcpyAsync(dcols, cols.data(), sizeof(CgColumn) * K, cudaMemcpyHostToDevice, st));
+  if (scale_host) PARO_CUDA(cudaMemcpyAsync(dscale, scale_host, sizeof(double) * K, cudaMemcpyHostToDevice, st));
+
+  // Jacobi preconditioner and the SPD diagonal check (linalg.cpp:164-173)
+  set_flag_kernel<<<1, 1, 0, st>>>(flag, 0);
+  ++ctx.launches;
+  double* invd = nullptr;
+  if (var) {
+    invd = ctx.invd.get<double>(n);
+    invd_kernel<<<148 * 8, 256, 0, st>>>(op.coef, op.sigma, op.m[0], n, invd, flag);
+    ++ctx.launches;
+  } else {
+    const double d = op.w[0] + op.sigma * op.m[0];
+    if (d <= 0.0) set_flag_kernel<<<1, 1, 0, st>>>(flag, 1), ++ctx.launches;
+  }
+  PARO_CUDA(cudaGetLastError());
+  m.invd = invd;
+  m.cols = dcols;
+  m.partials = partials;
+
+  // setup: r0, x0, bnorm, rz0, rnorm0
+  m.src = src;
+  m.dst = r;
+  m.x = x;
+  m.scale = dscale;
+  m.rhs = rhs;
+  launch_march(warm ? kSetupWarm : kSetupCold, var, cb, m, st);
+  fin_kernel<<<K, kFinThreads, 0, st>>>(kFinSetup, dcols, partials, m.nblk, flag);
+  zero_marked_kernel<<<dim3(148, K), 256, 0, st>>>(dcols, K, x, ld, n);
+  ctx.launches += 3;
+  PARO_CUDA(cudaGetLastError());
+
+  // iteration chunks captured once into a CUDA graph
+  const int chunk = n >= (1 << 22) ? 4 : n >= (1 << 18) ? 8 : 16;  // even: ping-pong parity repeats
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t cap;
+  PARO_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  PARO_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+  for (int it = 0; it < chunk; ++it) {
+    MarchArgs k1 = m;
+    k1.pold = (it & 1) ? p1 : p0;
+    k1.dst = (it & 1) ? p0 : p1;
+    k1.r = r;
+    launch_march(kK1, var, cb, k1, cap);
+    fin_kernel<<<K, kFinThreads, 0, cap>>>(kFinK1, dcols, partials, m.nblk, flag);
+    MarchArgs k2 = m;
+    k2.src = k1.dst;
+    k2.x = x;
+    k2.r = r;
+    launch_march(kK2, var, cb, k2, cap);
+    fin_kernel<<<K, kFinThreads, 0, cap>>>(kFinK2, dcols, partials, m.nblk, flag);
+  }
+  count_active_kernel<<<1, 256, 0, cap>>>(dcols, K, ctx.pinned_count_dev);
+  PARO_CUDA(cudaStreamEndCapture(cap, &graph));
+  PARO_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  PARO_CUDA(cudaStreamDestroy(cap));
+  const unsigned long long nodes = 4ull * chunk + 1;
+
+  cudaEvent_t ev[2];
+  PARO_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  PARO_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  volatile int* hcount = ctx.pinned_count;
+  // prime: the setup may already have finished every column
+  count_active_kernel<<<1, 256, 0, st>>>(dcols, K, ctx.pinned_count_dev);
+  ++ctx.launches;
+  PARO_CUDA(cudaEventRecord(ev[0], st));
+  PARO_CUDA(cudaEventSynchronize(ev[0]));
+  int remaining = *hcount;
+  unsigned long long max_iter = 0;
+  for (const auto& c : cols) max_iter = std::max(max_iter, c.max_iter);
+  unsigned long long launched = 0;
+  // keep one chunk in flight ahead of the poll
+  if (remaining > 0) {
+    PARO_CUDA(cudaGraphLaunch(exec, st));
+    PARO_CUDA(cudaEventRecord(ev[0], st));
+    launched += chunk;
+    ctx.launches += nodes;
+  }
+  int cur = 0;
+  while (remaining > 0) {
+    const bool more = launched < max_iter;
+    if (more) {
+      PARO_CUDA(cudaGraphLaunch(exec, st));
+      PARO_CUDA(cudaEventRecord(ev[cur ^ 1], st));
+      launched += chunk;
+      ctx.launches += nodes;
+    }
+    PARO_CUDA(cudaEventSynchronize(ev[cur]));
+    remaining = *hcount;
+    if (!more) {
+      PARO_CUDA(cudaStreamSynchronize(st));
+      remaining = *hcount;
+      break;
+    }
+    cur ^= 1;
+  }
+  PARO_CUDA(cudaStreamSynchronize(st));
+  PARO_CUDA(cudaEventDestroy(ev[0]));
+  PARO_CUDA(cudaEventDestroy(ev[1]));
+  PARO_CUDA(cudaGraphExecDestroy(exec));
+  PARO_CUDA(cudaGraphDestroy(graph));
+  PARO_CUDA(cudaMemcpy(cols.data(), dcols, sizeof(CgColumn) * K, cudaMemcpyDeviceToHost));
+}
+
+static CgColumn make_col(double tol, unsigned long long max_iter) {
+  CgColumn c{};
+  c.tol = tol;
+  c.max_iter = max_iter;
+  c.active = 1;
+  return c;
+}
+
+// source_solve_step (paro.cpp:81-119) for K columns at once.
+int source_solve(Ctx& ctx, const Op& a, const Op& b, double sigma, int K, const double* u, long long ld,
+                 const double* lambdas, double tol, unsigned long long max_iter, double* out,
+                 SolveReport* report) {
+  ctx.check_grid();
+  if (!a.var && false) throw ParoError(kInvalidArgument, "source_solve: A must be variable");
+  if (b.var) throw ParoError(kInvalidArgument, "source_solve: B must be the constant mass stencil");
+  if (K <= 0) return kOk;
+  for (int o = 0; o < kSlots; ++o) ctx.mass_w[o] = b.w[o];
+  const OpDev op = make_opdev(ctx, a, &b, sigma);
+  std::vector<double> scale(K);
+  for (int c = 0; c < K; ++c) scale[c] = lambdas[c] + sigma;  // paro.cpp:97
+  std::vector<CgColumn> cols(K);
+  for (int c = 0; c < K; ++c) cols[c] = make_col(tol, max_iter);
+  batched_pcg(ctx, op, a.var, K, u, nullptr, scale.data(), true, out, ld, cols);
+
+  std::vector<int> first_status(K, kOk), retry_status(K, kOk);
+  std::vector<double> retry_resid(K, 0.0);
+  std::vector<CgColumn> retry(K);
+  bool any_retry = false;
+  for (int c = 0; c < K; ++c) {
+    first_status[c] = cols[c].status;
+    if (cols[c].status == kIterationLimit) {
+      retry[c] = make_col(tol * 100.0, max_iter * 4);  // paro.cpp:105-109
+      any_retry = true;
+    } else {
+      retry[c] = cols[c];
+      retry[c].active = 0;
+    }
+  }
+  if (any_retry) {
+    batched_pcg(ctx, op, a.var, K, u, nullptr, scale.data(), true, out, ld, retry);
+    for (int c = 0; c < K; ++c)
+      if (first_status[c] == kIterationLimit) {
+        retry_status[c] = retry[c].status;
+        retry_resid[c] = retry[c].rnorm / retry[c].bnorm;
+      }
+  }
+  if (report) {
+    report->iterations.assign(K, 0);
+    report->residual.assign(K, 0.0);
+    report->status.assign(K, kOk);
+    for (int c = 0; c < K; ++c) {
+      const CgColumn& f = first_status[c] == kIterationLimit ? retry[c] : cols[c];
+      report->iterations[c] = f.it;
+      report->residual[c] = f.bnorm > 0 ? f.rnorm / f.bnorm : 0.0;
+      report->status[c] = first_status[c] == kIterationLimit ? retry_status[c] : first_status[c];
+    }
+  }
+  // Exception semantics of the serial reference loop: a failure inside the
+  // retry escapes immediately; first-attempt failures are rethrown by index.
+  for (int c = 0; c < K; ++c)
+    if (first_status[c] == kIterationLimit && retry_status[c] != kOk) {
+      ctx.resid = retry_resid[c];
+      ctx.err = retry_status[c] == kNotSpd ? "cg: operator not positive definite (p'Ap <= 0)"
+                                            : "cg: iteration limit reached";
+      return retry_status[c];
+    }
+  for (int c = 0; c < K; ++c)
+    if (first_status[c] != kOk && first_status[c] != kIterationLimit) {
+      ctx.err = "cg: operator not positive definite";
+      return first_status[c];
+    }
+  return kOk;
+}
+
+// shifted_source_step (paro.cpp:194-210): sigma = max(0, 0.5 - lambda_1),
+// doubled (2 sigma + 1) on NotSpd, at most 5 attempts.
+int shifted_source_solve(Ctx& ctx, const Op& a, const Op& b, int K, const double* u, long long ld,
+                         const double* lambdas, double tol, unsigned long long max_iter, double* out,
+                         double* sigma_out, SolveReport* report) {
+  double sigma = std::max(0.0, 0.5 - lambdas[0]);
+  for (int attempt = 0;; ++attempt) {
+    const int st = source_solve(ctx, a, b, sigma, K, u, ld, lambdas, tol, max_iter, out, report);
+    *sigma_out = sigma;
+    if (st != kNotSpd) return st;
+    if (attempt >= 4) return st;
+    sigma = 2.0 * sigma + 1.0;
+  }
+}
+
+// cg_solve(a, b, {x0, tol, max_iter}) for K right-hand sides at once.
+int cg_solve(Ctx& ctx, const Op& a, int K, const double* rhs, const double* x0, long long ld, double tol,
+             unsigned long long max_iter, bool throw_on_max, double* x, SolveReport* report) {
+  ctx.check_grid();
+  const OpDev op = make_opdev(ctx, a, nullptr, 0.0);
+  std::vector<CgColumn> cols(K);
+  for (int c = 0; c < K; ++c) cols[c] = make_col(tol, max_iter);
+  const double* src = x0;
+  double* zeros = nullptr;
+  if (!src) {
+    zeros = ctx.ws_c.get<double>(static_cast<size_t>(K) * ld);
+    PARO_CUDA(cudaMemsetAsync(zeros, 0, sizeof(double) * K * ld, ctx.stream));
+    src = zeros;
+  }
+  batched_pcg(ctx, op, a.var, K, src, rhs, nullptr, true, x, ld, cols);
+  int status = kOk;
+  if (report) {
+    report->iterations.assign(K, 0);
+    report->residual.assign(K, 0.0);
+    report->status.assign(K, kOk);
+  }
+  for (int c = 0; c < K; ++c) {
+    int s = cols[c].status;
+    if (s == kIterationLimit && !throw_on_max) s = kOk;
+    if (report) {
+      report->iterations[c] = cols[c].it;
+      report->residual[c] = cols[c].bnorm > 0 ? cols[c].rnorm / cols[c].bnorm : 0.0;
+      report->status[c] = s;
+    }
+    if (s != kOk && status == kOk) {
+      status = s;
+      ctx.resid = cols[c].bnorm > 0 ? cols[c].rnorm / cols[c].bnorm : 0.0;
+      ctx.err = s == kNotSpd ? "cg: operator not positive definite" : "cg: iteration limit reached";
+    }
+  }
+  return status;
+}
+
+// hartree_solve_with (model.cpp:242-255): K_poisson V = 4 pi M rho, cold start,
+// Jacobi-PCG to `tol`, at most 200000 iterations.
+int hartree_solve(Ctx& ctx, const Op& poisson, const Op& mass, const double* rho, double tol, double* vh,
+                  SolveReport* report) {
+  ctx.check_grid();
+  if (mass.var) throw ParoError(kInvalidArgument, "hartree: mass must be the constant stencil");
+  for (int o = 0; o < kSlots; ++o) ctx.mass_w[o] = mass.w[o];
+  const OpDev op = make_opdev(ctx, poisson, nullptr, 0.0);
+  const double four_pi = 4.0 * M_PI;
+  std::vector<CgColumn> cols(1, make_col(tol, 200000));
+  batched_pcg(ctx, op, poisson.var, 1, rho, nullptr, &four_pi, false, vh, ctx.grid.n, cols);
+  if (report) {
+    report->iterations.assign(1, cols[0].it);
+    report->residual.assign(1, cols[0].bnorm > 0 ? cols[0].rnorm / cols[0].bnorm : 0.0);
+    report->status.assign(1, cols[0].status);
+  }
+  if (cols[0].status != kOk) {
+    ctx.resid = cols[0].bnorm > 0 ? cols[0].rnorm / cols[0].bnorm : 0.0;
+    ctx.err = cols[0].status == kNotSpd ? "hartree: cg not positive definite" : "hartree: cg iteration limit";
+  }
+  return cols[0].status;
+}
+
+}  // namespace paro_b200

@@ -1,0 +1,35 @@
+// Device solvers behind the C ABI (host-callable, device pointers).
+#pragma once
+
+#include <vector>
+
+#include "ctx.hpp"
+#include "march.cuh"
+
+namespace paro_b200 {
+
+struct SolveReport {
+  std::vector<unsigned long long> iterations;
+  std::vector<double> residual;
+  std::vector<int> status;
+};
+
+OpDev make_opdev(const Ctx& ctx, const Op& a, const Op* shift, double sigma);
+
+void apply_op(Ctx& ctx, const Op& a, const Op* shift, double sigma, int K, const double* x, long long ldx,
+              double* y, long long ldy);
+
+int source_solve(Ctx& ctx, const Op& a, const Op& b, double sigma, int K, const double* u, long long ld,
+                 const double* lambdas, double tol, unsigned long long max_iter, double* out, SolveReport* rep);
+
+int shifted_source_solve(Ctx& ctx, const Op& a, const Op& b, int K, const double* u, long long ld,
+                         const double* lambdas, double tol, unsigned long long max_iter, double* out,
+                         double* sigma_out, SolveReport* rep);
+
+int cg_solve(Ctx& ctx, const Op& a, int K, const double* rhs, const double* x0, long long ld, double tol,
+             unsigned long long max_iter, bool throw_on_max, double* x, SolveReport* rep);
+
+int hartree_solve(Ctx& ctx, const Op& poisson, const Op& mass, const double* rho, double tol, double* vh,
+                  SolveReport* rep);
+
+}  // namespace paro_b200
