@@ -114,6 +114,20 @@ int paro_shifted_source_step(paro_ctx* ctx, const paro_op* a, const paro_op* b, 
 int paro_hartree_solve(paro_ctx* ctx, const paro_op* poisson, const paro_op* mass, const double* rho, double tol,
                        double* vh, size_t* iterations);
 
+/* ------------------------------------------------------------ Step 4 ----- */
+/* rayleigh_ritz (paro.cpp:121-177): B-orthonormalise the k candidates with the
+ * drop rule of b_orthonormalize (linalg.cpp:409-439), solve the projected
+ * pencil (dense_sym_geneig, linalg.cpp:341-393), lift, fix_sign and check the
+ * Gram certificate (<= 1e-8, paro.cpp:170-174). cands/orbitals: device,
+ * ld == n; lambdas: host array of k (ascending); k_out, defect: host. */
+int paro_rayleigh_ritz(paro_ctx* ctx, const paro_op* a_form, const paro_op* b, int k, const double* cands,
+                       long long ld, size_t min_keep, double drop_tol, double* lambdas, double* orbitals,
+                       long long ldo, int* k_out, double* gram_defect);
+/* dense_sym_geneig on one warp of the device, host row-major m x m in/out. */
+int paro_dense_sym_geneig(paro_ctx* ctx, int m, const double* a, const double* b, double* values, double* vectors);
+/* fix_sign (linalg.cpp:229-241) on k device columns. */
+int paro_fix_sign(paro_ctx* ctx, int k, double* v, long long ld);
+
 #ifdef __cplusplus
 }
 #endif

@@ -97,6 +97,9 @@ SIGNATURES = {
     "paro_source_solve_step": (_I, [_P, _P, _P, _I, _P, _LL, _DP, _D, _SZ, _D, _P, _SZP, _DP]),
     "paro_shifted_source_step": (_I, [_P, _P, _P, _I, _P, _LL, _DP, _D, _SZ, _P, _DP, _SZP, _DP]),
     "paro_hartree_solve": (_I, [_P, _P, _P, _P, _D, _P, _SZP]),
+    "paro_rayleigh_ritz": (_I, [_P, _P, _P, _I, _P, _LL, _SZ, _D, _DP, _P, _LL, C.POINTER(_I), _DP]),
+    "paro_dense_sym_geneig": (_I, [_P, _I, _DP, _DP, _DP, _DP]),
+    "paro_fix_sign": (_I, [_P, _I, _P, _LL]),
 }
 
 _lib = None

@@ -18,6 +18,8 @@ OUT = PKG / "_lib"
 LIB = OUT / "libparo_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# files whose arithmetic must match the reference operation-for-operation (no FMA contraction)
+NO_FMA = {"dense.cu"}
 CFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{ROOT / 'include'}", f"-I{CSRC}",
           "--expt-relaxed-constexpr"]
 
@@ -38,6 +40,8 @@ def _compile(src: Path, hdr_mtime: float, verbose: bool) -> Path:
     cmd = [NVCC, *ARCH, *CFLAGS, "-c", str(src), "-o", str(obj)]
     if src.suffix == ".cu":
         cmd.insert(1, "-Xptxas=-warn-spills")
+    if src.name in NO_FMA:
+        cmd.insert(1, "-fmad=false")
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -267,3 +267,51 @@ def hartree_solve_with(poisson: Operator, mass: Operator, rho: torch.Tensor, tol
         report.update(iterations=it.value)
     ctx.check(st)
     return vh
+
+
+@dataclass
+class OrbitalSet:
+    """OrbitalSet (paro.hpp:16-23): B-orthonormal orbitals [k, n] + ascending lambdas."""
+
+    orbitals: torch.Tensor
+    lambdas: list
+    gram_defect: float = 0.0
+
+    def count(self) -> int:
+        return len(self.lambdas)
+
+
+def rayleigh_ritz(candidates: torch.Tensor, a_form: Operator, b: Operator, min_keep: int, drop_tol: float = 1e-8,
+                  out: torch.Tensor | None = None) -> OrbitalSet:
+    """Step 4, rayleigh_ritz (paro.cpp:121-177)."""
+    ctx = a_form.ctx
+    U = _as_cols(candidates, ctx.n).contiguous()
+    k = U.shape[0]
+    V = out if out is not None else torch.empty_like(U)
+    lam = (C.c_double * k)()
+    kout = C.c_int(0)
+    defect = C.c_double(0.0)
+    st = N.lib().paro_rayleigh_ritz(ctx.h, a_form.h, b.h, k, _ptr(U), ctx.n, min_keep, drop_tol, lam, _ptr(V), ctx.n,
+                                    C.byref(kout), C.byref(defect))
+    ctx.check(st)
+    kk = kout.value
+    return OrbitalSet(V[:kk], list(lam)[:kk], defect.value)
+
+
+def dense_sym_geneig(ctx: Context, A, B):
+    """dense_sym_geneig (linalg.cpp:341-393) on the device; host row-major in/out."""
+    A = np.ascontiguousarray(A, np.float64)
+    B = np.ascontiguousarray(B, np.float64)
+    m = A.shape[0]
+    vals = np.zeros(m)
+    vecs = np.zeros((m, m))
+    ctx.check(N.lib().paro_dense_sym_geneig(ctx.h, m, A.ctypes.data_as(_DP), B.ctypes.data_as(_DP),
+                                            vals.ctypes.data_as(_DP), vecs.ctypes.data_as(_DP)))
+    return vals, vecs
+
+
+def fix_sign(ctx: Context, v: torch.Tensor) -> torch.Tensor:
+    """fix_sign (linalg.cpp:229-241) in place on [k, n] device columns."""
+    vc = _as_cols(v, ctx.n)
+    ctx.check(N.lib().paro_fix_sign(ctx.h, vc.shape[0], _ptr(vc), vc.stride(0)))
+    return v

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "ctx.hpp"
+#include "ritz.hpp"
 #include "solver.hpp"
 
 struct paro_ctx {
@@ -370,6 +371,27 @@ int paro_hartree_solve(paro_ctx* ctx, const paro_op* poisson, const paro_op* mas
     const int st = hartree_solve(ctx->c, poisson->o, mass->o, rho, tol, vh, &rep);
     fill_report(rep, iters, nullptr);
     return st;
+  });
+}
+
+int paro_rayleigh_ritz(paro_ctx* ctx, const paro_op* a, const paro_op* b, int k, const double* cands, long long ld,
+                       size_t min_keep, double drop_tol, double* lambdas, double* orbs, long long ldo, int* k_out,
+                       double* defect) {
+  return guarded(ctx, [&] {
+    RitzInfo info;
+    return rayleigh_ritz(ctx->c, a->o, b->o, k, cands, ld, min_keep, drop_tol, lambdas, orbs, ldo, k_out, defect,
+                         &info);
+  });
+}
+
+int paro_dense_sym_geneig(paro_ctx* ctx, int m, const double* a, const double* b, double* vals, double* vecs) {
+  return guarded(ctx, [&] { return dense_sym_geneig(ctx->c, m, a, b, vals, vecs); });
+}
+
+int paro_fix_sign(paro_ctx* ctx, int k, double* v, long long ld) {
+  return guarded(ctx, [&] {
+    fix_sign_columns(ctx->c, v, ld, k);
+    return kOk;
   });
 }
 

@@ -1,0 +1,289 @@
+// Step 4 on the device: rayleigh_ritz (proj/src/paro.cpp:121-177).
+//
+//   W = B U, G1 = U^T W            -> ordered Cholesky with the MGS drop rule
+//   Q1 = U C1                       (C1 = L1^{-T} on the accepted candidates)
+//   W = B Q1, G2 = Q1^T W           -> C2 = L2^{-T}, Bt = L2^{-1} G2 L2^{-T}
+//   W = A Q1, GA = Q1^T W           -> At = C2^T GA C2, dense_sym_geneig(At, Bt)
+//   V = Q1 (C2 X), fix_sign, certificate max|V^T B V - I| <= 1e-8
+//
+// i.e. CholQR2 in place of two-pass MGS (identical in exact arithmetic,
+// SURVEY.md §8a), with the stencil applies on the plane-marching kernels, the
+// tall-skinny Grams / rotations as FP64 DGEMMs and the K x K work in
+// single-warp kernels (dense.cu).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "dense.hpp"
+#include "ritz.hpp"
+#include "solver.hpp"
+
+namespace paro_b200 {
+
+namespace {
+
+void cublas_check(cublasStatus_t s, const char* what) {
+  if (s != CUBLAS_STATUS_SUCCESS) throw ParoError(kCuda, std::string("cuBLAS failure in ") + what);
+}
+
+// G (k1 x k2, column-major) = X^T Y, X: n x k1 (ldx), Y: n x k2 (ldy)
+void gram(Ctx& ctx, int k1, int k2, const double* X, long long ldx, const double* Y, long long ldy, double* G) {
+  const double one = 1.0, zero = 0.0;
+  cublas_check(cublasDgemm(ctx.cublas, CUBLAS_OP_T, CUBLAS_OP_N, k1, k2, static_cast<int>(ctx.grid.n), &one, X,
+                           static_cast<int>(ldx), Y, static_cast<int>(ldy), &zero, G, k1),
+               "gram");
+  ++ctx.launches;
+}
+
+// Z (n x k2) = X (n x k1) C (k1 x k2, column-major, ldc)
+void rotate(Ctx& ctx, int k1, int k2, const double* X, long long ldx, const double* Cm, int ldc, double* Z,
+            long long ldz) {
+  const double one = 1.0, zero = 0.0;
+  cublas_check(cublasDgemm(ctx.cublas, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(ctx.grid.n), k2, k1, &one, X,
+                           static_cast<int>(ldx), Cm, ldc, &zero, Z, static_cast<int>(ldz)),
+               "rotate");
+  ++ctx.launches;
+}
+
+__device__ __forceinline__ double block_max(double v, double* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) v = fmax(v, sh[w]);
+  __syncthreads();
+  return v;
+}
+
+// fix_sign (linalg.cpp:229-241) on device columns: max |v|, first index with
+// |v_i| > 1e-12 max, negate the column if that entry is negative.
+__global__ void colmax_kernel(const double* V, long long ld, long long n, unsigned long long* amax) {
+  __shared__ double sh[32];
+  const int c = blockIdx.y;
+  double m = 0.0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    m = fmax(m, fabs(V[c * ld + i]));
+  m = block_max(m, sh);
+  if (threadIdx.x == 0 && m > 0.0) atomicMax(amax + c, static_cast<unsigned long long>(__double_as_longlong(m)));
+}
+
+__global__ void firstidx_kernel(const double* V, long long ld, long long n, const unsigned long long* amax,
+                                unsigned long long* first) {
+  const int c = blockIdx.y;
+  const double thr = 1e-12 * __longlong_as_double(static_cast<long long>(amax[c]));
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (static_cast<unsigned long long>(i) >= first[c]) return;
+    if (fabs(V[c * ld + i]) > thr) {
+      atomicMin(first + c, static_cast<unsigned long long>(i));
+      return;
+    }
+  }
+}
+
+__global__ void negate_kernel(double* V, long long ld, long long n, const unsigned long long* amax,
+                              const unsigned long long* first) {
+  const int c = blockIdx.y;
+  if (amax[c] == 0ull || first[c] >= static_cast<unsigned long long>(n)) return;
+  if (!(V[c * ld + static_cast<long long>(first[c])] < 0.0)) return;
+  __syncthreads();
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    V[c * ld + i] = -V[c * ld + i];
+}
+
+__global__ void init_sign_kernel(int k, unsigned long long* amax, unsigned long long* first) {
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    amax[i] = 0ull;
+    first[i] = ~0ull;
+  }
+}
+
+// gram_defect (paro.cpp:50-61): max over j <= i of |v_i^T B v_j - delta_ij|.
+__global__ void defect_kernel(int k, const double* G, double* out) {
+  __shared__ double sh[32];
+  double m = 0.0;
+  for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) {
+    const int i = idx % k, j = idx / k;
+    if (j <= i) m = fmax(m, fabs(G[i + j * k] - (i == j ? 1.0 : 0.0)));
+  }
+  m = block_max(m, sh);
+  if (threadIdx.x == 0) *out = m;
+}
+
+}  // namespace
+
+void fix_sign_columns(Ctx& ctx, double* V, long long ld, int k) {
+  if (k <= 0) return;
+  const long long n = ctx.grid.n;
+  auto* amax = ctx.ws_small3.get<unsigned long long>(2 * static_cast<size_t>(k));
+  unsigned long long* first = amax + k;
+  cudaStream_t st = ctx.stream;
+  init_sign_kernel<<<1, 256, 0, st>>>(k, amax, first);
+  const int bx = static_cast<int>(std::min<long long>(148 * 4, (n + 255) / 256));
+  colmax_kernel<<<dim3(bx, k), 256, 0, st>>>(V, ld, n, amax);
+  firstidx_kernel<<<dim3(bx, k), 256, 0, st>>>(V, ld, n, amax, first);
+  negate_kernel<<<dim3(bx, k), 256, 0, st>>>(V, ld, n, amax, first);
+  ctx.launches += 4;
+  PARO_CUDA(cudaGetLastError());
+}
+
+namespace {
+
+struct Small {
+  double *G, *C1, *G2, *C2, *Bt, *GA, *vals, *Y, *At, *X, *G3, *rmin, *defect;
+  int *acc, *kout, *status;
+  DenseScratch w;
+};
+
+Small small_buffers(Ctx& ctx, int K) {
+  const size_t kk = static_cast<size_t>(K) * K;
+  double* base = ctx.ws_small.get<double>(16 * kk + 4 * K + 64);
+  Small s{};
+  double* p = base;
+  auto take = [&](size_t cnt) {
+    double* r = p;
+    p += cnt;
+    return r;
+  };
+  s.G = take(kk);
+  s.C1 = take(kk);
+  s.G2 = take(kk);
+  s.C2 = take(kk);
+  s.Bt = take(kk);
+  s.GA = take(kk);
+  s.Y = take(kk);
+  s.At = take(kk);
+  s.X = take(kk);
+  s.G3 = take(kk);
+  s.w.a = take(kk);
+  s.w.v = take(kk);
+  s.w.l = take(kk);
+  s.w.w = take(kk);
+  s.w.c = take(kk);
+  s.vals = take(K);
+  s.rmin = take(1);
+  s.defect = take(1);
+  int* ib = ctx.ws_small2.get<int>(3 * static_cast<size_t>(K) + 8);
+  s.acc = ib;
+  s.w.order = ib + K;
+  s.kout = ib + 2 * K;
+  s.status = ib + 2 * K + 1;
+  return s;
+}
+
+int read_int(Ctx& ctx, const int* d) {
+  int v = 0;
+  PARO_CUDA(cudaMemcpyAsync(&v, d, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  PARO_CUDA(cudaStreamSynchronize(ctx.stream));
+  return v;
+}
+
+double read_double(Ctx& ctx, const double* d) {
+  double v = 0;
+  PARO_CUDA(cudaMemcpyAsync(&v, d, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+  PARO_CUDA(cudaStreamSynchronize(ctx.stream));
+  return v;
+}
+
+}  // namespace
+
+int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, long long ld, size_t min_keep,
+                  double drop_tol, double* lambdas, double* V, long long ldv, int* k_out, double* defect,
+                  RitzInfo* info) {
+  ctx.check_grid();
+  if (B.var) throw ParoError(kInvalidArgument, "rayleigh_ritz: B must be the constant mass stencil");
+  if (K <= 0) throw ParoError(kEmptyBasis, "b_orthonormalize: all vectors dropped");
+  const long long n = ctx.grid.n;
+  cudaStream_t st = ctx.stream;
+  cublasSetStream(ctx.cublas, st);
+  double* W = ctx.ws_b.get<double>(static_cast<size_t>(K) * n);
+  double* Q1 = ctx.ws_c.get<double>(static_cast<size_t>(K) * n);
+  Small s = small_buffers(ctx, K);
+
+  // pass 1: Gram of the candidates, ordered Cholesky with drops
+  if (ld != n || ldv != n) throw ParoError(kInvalidArgument, "rayleigh_ritz: vectors must be contiguous (ld == n)");
+  apply_op(ctx, B, nullptr, 0.0, K, U, ld, W, n);
+  gram(ctx, K, K, U, ld, W, n, s.G);
+  ortho_from_gram_kernel<<<1, 32, 0, st>>>(K, s.G, drop_tol, 1, s.C1, s.acc, s.kout, s.rmin, s.w, s.status);
+  ++ctx.launches;
+  PARO_CUDA(cudaGetLastError());
+  const int k = read_int(ctx, s.kout);
+  const double rmin = read_double(ctx, s.rmin);
+  if (info) {
+    info->min_ratio = rmin;
+    info->k = k;
+  }
+  if (k == 0) {
+    ctx.err = "b_orthonormalize: all vectors dropped";
+    return kEmptyBasis;
+  }
+  if (static_cast<size_t>(k) < min_keep) {
+    ctx.err = "rayleigh_ritz: candidate span collapsed to " + std::to_string(k) + " < " + std::to_string(min_keep);
+    return kDegenerateSpan;
+  }
+  rotate(ctx, K, k, U, ld, s.C1, K, Q1, n);
+
+  // pass 2
+  apply_op(ctx, B, nullptr, 0.0, k, Q1, n, W, n);
+  gram(ctx, k, k, Q1, n, W, n, s.G2);
+  second_pass_kernel<<<1, 32, 0, st>>>(k, s.G2, s.C2, s.Bt, s.w, s.status);
+  ++ctx.launches;
+  if (read_int(ctx, s.status) != kOk) {
+    ctx.err = "rayleigh_ritz: second orthonormalisation pass lost positive definiteness";
+    return kPencil;
+  }
+
+  // projected pencil
+  apply_op(ctx, A, nullptr, 0.0, k, Q1, n, W, n);
+  gram(ctx, k, k, Q1, n, W, n, s.GA);
+  pencil_kernel<<<1, 32, 0, st>>>(k, s.GA, s.C2, s.Bt, s.vals, s.Y, s.At, s.X, s.w, s.status);
+  ++ctx.launches;
+  if (read_int(ctx, s.status) != kOk) {
+    ctx.err = "pencil: B is not positive definite";
+    return kPencil;
+  }
+
+  // lift, sign convention, certificate
+  rotate(ctx, k, k, Q1, n, s.Y, k, V, ldv);
+  fix_sign_columns(ctx, V, ldv, k);
+  apply_op(ctx, B, nullptr, 0.0, k, V, ldv, W, n);
+  gram(ctx, k, k, V, ldv, W, n, s.G3);
+  defect_kernel<<<1, 256, 0, st>>>(k, s.G3, s.defect);
+  ++ctx.launches;
+  PARO_CUDA(cudaMemcpyAsync(lambdas, s.vals, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+  const double d = read_double(ctx, s.defect);
+  *k_out = k;
+  *defect = d;
+  if (d > 1e-8) {
+    ctx.err = "rayleigh_ritz: orthonormality certificate violated (defect " + std::to_string(d) + ")";
+    return kError;
+  }
+  return kOk;
+}
+
+int dense_sym_geneig(Ctx& ctx, int m, const double* A_host, const double* B_host, double* vals_host,
+                     double* vecs_host) {
+  Small s = small_buffers(ctx, m);
+  cudaStream_t st = ctx.stream;
+  const size_t bytes = sizeof(double) * m * m;
+  PARO_CUDA(cudaMemcpyAsync(s.At, A_host, bytes, cudaMemcpyHostToDevice, st));
+  PARO_CUDA(cudaMemcpyAsync(s.Bt, B_host, bytes, cudaMemcpyHostToDevice, st));
+  geneig_kernel<<<1, 32, 0, st>>>(m, s.At, s.Bt, s.vals, s.X, s.w, s.status);
+  ++ctx.launches;
+  PARO_CUDA(cudaGetLastError());
+  const int status = read_int(ctx, s.status);
+  if (status != kOk) {
+    ctx.err = "pencil: B is not positive definite or the pencil is not symmetric";
+    return status;
+  }
+  PARO_CUDA(cudaMemcpyAsync(vals_host, s.vals, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
+  PARO_CUDA(cudaMemcpyAsync(vecs_host, s.X, bytes, cudaMemcpyDeviceToHost, st));
+  PARO_CUDA(cudaStreamSynchronize(st));
+  return kOk;
+}
+
+}  // namespace paro_b200

@@ -1,0 +1,22 @@
+// Step 4 (rayleigh_ritz) and the dense pencil solve behind the C ABI.
+#pragma once
+
+#include "ctx.hpp"
+
+namespace paro_b200 {
+
+struct RitzInfo {
+  double min_ratio = 0.0;  // smallest projected/original B-norm ratio of the candidates
+  int k = 0;
+};
+
+int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, long long ld, size_t min_keep,
+                  double drop_tol, double* lambdas_host, double* V, long long ldv, int* k_out, double* defect,
+                  RitzInfo* info);
+
+int dense_sym_geneig(Ctx& ctx, int m, const double* A_host, const double* B_host, double* vals_host,
+                     double* vecs_host);
+
+void fix_sign_columns(Ctx& ctx, double* V, long long ld, int k);
+
+}  // namespace paro_b200
