@@ -128,6 +128,48 @@ int paro_dense_sym_geneig(paro_ctx* ctx, int m, const double* a, const double* b
 /* fix_sign (linalg.cpp:229-241) on k device columns. */
 int paro_fix_sign(paro_ctx* ctx, int k, double* v, long long ld);
 
+/* ------------------------------------------------- operator assembly ----- */
+/* On the device, element by element in the reference's element order, so the
+ * coefficients equal the reference CSR values. Uniform results become
+ * constant stencils. */
+/* assemble_mass (fem.cpp:253-268) */
+int paro_assemble_mass(paro_ctx* ctx, paro_op** out);
+/* assemble_stiffness(scale * I, 0) (fem.cpp:221-251): kinetic (0.5), Poisson (1) */
+int paro_assemble_stiffness(paro_ctx* ctx, double scale, paro_op** out);
+/* assemble_weighted_mass of external_potential(molecule, eps)
+ * (model.cpp:146-175, fem.cpp:272-321): eps == 0 -> bare Coulomb with the
+ * singular-quadrature policy (degree-5 Duffy rule, 2-level subdivided rule
+ * near a nucleus); eps > 0 -> -Z/sqrt(r^2 + eps^2), 4-point rule.
+ * positions: 3*nnuc host doubles. */
+int paro_assemble_vext(paro_ctx* ctx, int nnuc, const double* charges, const double* positions, double eps,
+                       paro_op** out);
+/* weighted mass of c*|x|^2 (4-point rule), the harmonic-oscillator reaction */
+int paro_assemble_harmonic(paro_ctx* ctx, double c, paro_op** out);
+/* a += s * b (SparseOperator::add_scaled, linalg.cpp:120-125) */
+int paro_op_add_scaled(paro_ctx* ctx, paro_op* a, const paro_op* b, double s);
+/* ks_form_matrix (paro.cpp:446-454): out = kinetic + vext + M[V_H + v_xc(rho)];
+ * out: variable operator (paro_op_create_var); clamped: host, may be NULL. */
+int paro_ks_form(paro_ctx* ctx, const paro_op* kinetic, const paro_op* vext_mass, const double* rho,
+                 const double* vh, int exchange_only, paro_op* out, long long* clamped);
+
+/* ---------------------------------------------------------- fields ------- */
+/* density_from_orbitals (model.cpp:192-223): rho = sum_i occ_i u_i^2
+ * normalised to sum occ; occ: host array of nocc; raw_integral: host. */
+int paro_density(paro_ctx* ctx, int nocc, const double* u, long long ld, const double* occ, double* rho,
+                 double* raw_integral);
+/* mix_density (model.cpp:225-236) */
+int paro_mix_density(paro_ctx* ctx, const double* rho_in, const double* rho_out, double alpha, double* out);
+/* integrate / norm_l2 (fem.cpp:419-448), integrate_product (model.cpp:306-327); results: host */
+int paro_integrate(paro_ctx* ctx, const double* f, double* out);
+int paro_norm_l2(paro_ctx* ctx, const double* f, double* out);
+int paro_integrate_product(paro_ctx* ctx, const double* u, const double* v, double* out);
+/* ||rho_out - rho_in||_L2 (paro.cpp:608-612); scratch: n device doubles */
+int paro_rho_residual(paro_ctx* ctx, const double* rho_out, const double* rho_in, double* scratch, double* out);
+/* total_energy (model.cpp:329-360); lambdas, occ, charges, positions: host */
+int paro_total_energy(paro_ctx* ctx, int n_lambdas, const double* lambdas, int nocc, const double* occ,
+                      const double* rho, const double* vh, int exchange_only, int nnuc, const double* charges,
+                      const double* positions, double* e_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -100,6 +100,19 @@ SIGNATURES = {
     "paro_rayleigh_ritz": (_I, [_P, _P, _P, _I, _P, _LL, _SZ, _D, _DP, _P, _LL, C.POINTER(_I), _DP]),
     "paro_dense_sym_geneig": (_I, [_P, _I, _DP, _DP, _DP, _DP]),
     "paro_fix_sign": (_I, [_P, _I, _P, _LL]),
+    "paro_assemble_mass": (_I, [_P, C.POINTER(_P)]),
+    "paro_assemble_stiffness": (_I, [_P, _D, C.POINTER(_P)]),
+    "paro_assemble_vext": (_I, [_P, _I, _DP, _DP, _D, C.POINTER(_P)]),
+    "paro_assemble_harmonic": (_I, [_P, _D, C.POINTER(_P)]),
+    "paro_op_add_scaled": (_I, [_P, _P, _P, _D]),
+    "paro_ks_form": (_I, [_P, _P, _P, _P, _P, _I, _P, C.POINTER(_LL)]),
+    "paro_density": (_I, [_P, _I, _P, _LL, _DP, _P, _DP]),
+    "paro_mix_density": (_I, [_P, _P, _P, _D, _P]),
+    "paro_integrate": (_I, [_P, _P, _DP]),
+    "paro_norm_l2": (_I, [_P, _P, _DP]),
+    "paro_integrate_product": (_I, [_P, _P, _P, _DP]),
+    "paro_rho_residual": (_I, [_P, _P, _P, _P, _DP]),
+    "paro_total_energy": (_I, [_P, _I, _DP, _I, _DP, _P, _P, _I, _I, _DP, _DP, _DP]),
 }
 
 _lib = None

@@ -19,7 +19,7 @@ LIB = OUT / "libparo_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # files whose arithmetic must match the reference operation-for-operation (no FMA contraction)
-NO_FMA = {"dense.cu"}
+NO_FMA = {"dense.cu", "assemble.cu", "fields.cu"}
 CFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{ROOT / 'include'}", f"-I{CSRC}",
           "--expt-relaxed-constexpr"]
 
@@ -35,19 +35,23 @@ def _headers_mtime() -> float:
 
 def _compile(src: Path, hdr_mtime: float, verbose: bool) -> Path:
     obj = OUT / "obj" / (src.name + ".o")
-    if obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, hdr_mtime):
-        return obj
     cmd = [NVCC, *ARCH, *CFLAGS, "-c", str(src), "-o", str(obj)]
     if src.suffix == ".cu":
         cmd.insert(1, "-Xptxas=-warn-spills")
     if src.name in NO_FMA:
         cmd.insert(1, "-fmad=false")
+    stamp = obj.with_suffix(".cmd")
+    fresh = (obj.exists() and stamp.exists() and stamp.read_text() == " ".join(cmd)
+             and obj.stat().st_mtime >= max(src.stat().st_mtime, hdr_mtime))
+    if fresh:
+        return obj
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError(f"nvcc failed on {src.name}")
+    stamp.write_text(" ".join(cmd))
     return obj
 
 

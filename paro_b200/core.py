@@ -315,3 +315,111 @@ def fix_sign(ctx: Context, v: torch.Tensor) -> torch.Tensor:
     vc = _as_cols(v, ctx.n)
     ctx.check(N.lib().paro_fix_sign(ctx.h, vc.shape[0], _ptr(vc), vc.stride(0)))
     return v
+
+
+# ---------------------------------------------------------------- assembly --
+
+def _new_op(ctx: Context, fn, *args) -> Operator:
+    h = C.c_void_p()
+    ctx.check(fn(ctx.h, *args, C.byref(h)))
+    return Operator(ctx, h)
+
+
+def assemble_mass(ctx: Context) -> Operator:
+    """assemble_mass (fem.cpp:253-268), on the device."""
+    return _new_op(ctx, N.lib().paro_assemble_mass)
+
+
+def assemble_stiffness(ctx: Context, scale: float) -> Operator:
+    """assemble_stiffness(constant_diffusion(scale), 0) (fem.cpp:221-251)."""
+    return _new_op(ctx, N.lib().paro_assemble_stiffness, float(scale))
+
+
+def assemble_vext(ctx: Context, charges, positions, eps: float = 0.0) -> Operator:
+    """Weighted mass of external_potential(molecule, eps) with the singular policy."""
+    Z = np.ascontiguousarray(charges, np.float64)
+    R = np.ascontiguousarray(positions, np.float64).reshape(-1)
+    return _new_op(ctx, N.lib().paro_assemble_vext, len(Z), Z.ctypes.data_as(_DP), R.ctypes.data_as(_DP), float(eps))
+
+
+def assemble_harmonic(ctx: Context, c: float) -> Operator:
+    """Weighted mass of c*|x|^2 (4-point rule)."""
+    return _new_op(ctx, N.lib().paro_assemble_harmonic, float(c))
+
+
+def add_scaled(a: Operator, b: Operator, s: float = 1.0) -> Operator:
+    """a += s*b (SparseOperator::add_scaled, linalg.cpp:120-125)."""
+    a.ctx.check(N.lib().paro_op_add_scaled(a.ctx.h, a.h, b.h, float(s)))
+    w = (C.c_double * 8)()
+    var = C.c_int(0)
+    a.ctx.check(N.lib().paro_op_weights(a.h, w, C.byref(var)))
+    a.variable, a.weights = bool(var.value), np.array(list(w))
+    return a
+
+
+def ks_form_matrix(kinetic: Operator, vext: Operator, rho: torch.Tensor, vh: torch.Tensor,
+                   exchange_only: bool = False, out: Operator | None = None):
+    """ks_form_matrix (paro.cpp:446-454) -> (operator, clamped density points)."""
+    ctx = kinetic.ctx
+    op = out if out is not None else Operator.variable_empty(ctx)
+    cl = C.c_longlong(0)
+    ctx.check(N.lib().paro_ks_form(ctx.h, kinetic.h, vext.h, _ptr(rho), _ptr(vh), int(exchange_only), op.h,
+                                   C.byref(cl)))
+    return op, cl.value
+
+
+# ------------------------------------------------------------------ fields --
+
+def density_from_orbitals(ctx: Context, orbitals: torch.Tensor, occupations, out: torch.Tensor | None = None):
+    """density_from_orbitals (model.cpp:192-223) -> (rho, raw_integral)."""
+    U = _as_cols(orbitals, ctx.n)
+    nocc = len(occupations)
+    if nocc == 0 or U.shape[0] < nocc:
+        raise N.InvalidArgumentError("density: orbital/occupation count mismatch")
+    rho = out if out is not None else ctx.empty(ctx.n)
+    occ = (C.c_double * nocc)(*[float(f) for f in occupations])
+    raw = C.c_double(0.0)
+    ld = U.stride(0) if U.shape[0] > 1 else ctx.n
+    ctx.check(N.lib().paro_density(ctx.h, nocc, _ptr(U), ld, occ, _ptr(rho), C.byref(raw)))
+    return rho, raw.value
+
+
+def mix_density(ctx: Context, rho_in: torch.Tensor, rho_out: torch.Tensor, alpha: float,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+    """mix_density (model.cpp:225-236)."""
+    o = out if out is not None else ctx.empty(ctx.n)
+    ctx.check(N.lib().paro_mix_density(ctx.h, _ptr(rho_in), _ptr(rho_out), float(alpha), _ptr(o)))
+    return o
+
+
+def _scalar(ctx: Context, fn, *args) -> float:
+    out = C.c_double(0.0)
+    ctx.check(fn(ctx.h, *args, C.byref(out)))
+    return out.value
+
+
+def integrate(ctx: Context, f: torch.Tensor) -> float:
+    return _scalar(ctx, N.lib().paro_integrate, _ptr(f))
+
+
+def norm_l2(ctx: Context, f: torch.Tensor) -> float:
+    return _scalar(ctx, N.lib().paro_norm_l2, _ptr(f))
+
+
+def integrate_product(ctx: Context, u: torch.Tensor, v: torch.Tensor) -> float:
+    return _scalar(ctx, N.lib().paro_integrate_product, _ptr(u), _ptr(v))
+
+
+def rho_residual(ctx: Context, rho_out: torch.Tensor, rho_in: torch.Tensor, scratch: torch.Tensor) -> float:
+    return _scalar(ctx, N.lib().paro_rho_residual, _ptr(rho_out), _ptr(rho_in), _ptr(scratch))
+
+
+def total_energy(ctx: Context, lambdas, occupations, rho: torch.Tensor, vh: torch.Tensor, charges, positions,
+                 exchange_only: bool = False) -> float:
+    """total_energy (model.cpp:329-360)."""
+    lam = (C.c_double * len(lambdas))(*[float(v) for v in lambdas])
+    occ = (C.c_double * len(occupations))(*[float(v) for v in occupations])
+    Z = np.ascontiguousarray(charges, np.float64)
+    R = np.ascontiguousarray(positions, np.float64).reshape(-1)
+    return _scalar(ctx, N.lib().paro_total_energy, len(lambdas), lam, len(occupations), occ, _ptr(rho), _ptr(vh),
+                   int(exchange_only), len(Z), Z.ctypes.data_as(_DP), R.ctypes.data_as(_DP))

@@ -1,0 +1,362 @@
+// Operator assembly on the device (compiled -fmad=false).
+//
+// One thread per interior dof v gathers the 8 stencil slots of its row
+// (diagonal + the 7 forward Kuhn edges) from the 24 incident tetrahedra,
+// visiting them in the reference's global element order (cells by (k,j,i),
+// then the 6 Kuhn permutations), so each slot is the same sum of element
+// contributions, in the same order, as the CSR entry produced by
+// assemble_matrix (fem.cpp:162-183). Element-local rows follow
+// assemble_mass (fem.cpp:253-268), assemble_stiffness (fem.cpp:221-251) and
+// assemble_weighted_mass with pick_weighted_rule (fem.cpp:272-321); the
+// Kohn-Sham form adds kinetic + V_ext + (V_H + v_xc) mass exactly like
+// ks_form_matrix (paro.cpp:433-454).
+#include <vector>
+
+#include "assemble.hpp"
+#include "fem.cuh"
+
+namespace paro_b200 {
+
+namespace {
+
+struct AsmArgs {
+  Box box;
+  long long n = 0;
+  int kind = 0;
+  double scale = 0.0;        // stiffness diffusion scale / harmonic coefficient
+  int nq = 0;                // main rule
+  const double* qp = nullptr;
+  const double* qw = nullptr;
+  int nqs = 0;               // subdivided rule for elements near a singular point
+  const double* qps = nullptr;
+  const double* qws = nullptr;
+  int nnuc = 0;
+  const double* nuc = nullptr;  // Z, x, y, z per nucleus
+  double eps2 = 0.0;
+  int singular = 0;          // singular-quadrature policy active (bare Coulomb)
+  const double* rho = nullptr;
+  const double* vh = nullptr;
+  int exchange_only = 0;
+  double cx = 0.0;
+  // KS form: out = (kinetic + vext) + scf
+  const double* kin_coef = nullptr;
+  double kin_w[kSlots] = {};
+  const double* vext_coef = nullptr;
+  double* out = nullptr;
+  int* flags = nullptr;      // bit0 singular point hit, bit1 non-finite weight
+};
+
+__device__ __forceinline__ double eval_in_element(const double* f, int s, const int (&vtx)[4][3],
+                                                  const double (&bary)[4]) {
+  double v = 0.0;
+  for (int i = 0; i < 4; ++i) {
+    const long long d = vertex_dof(s, vtx[i][0], vtx[i][1], vtx[i][2]);
+    if (d >= 0) v += bary[i] * f[d];
+  }
+  return v;
+}
+
+// weight function w(e, x) of the weighted-mass kinds
+__device__ double weight_at(const AsmArgs& a, const V3 (&P)[4], const int (&vtx)[4][3], V3 x) {
+  if (a.kind == kAsmCoulomb) {  // external_potential, eps = 0 (model.cpp:150-162)
+    double v = 0.0;
+    for (int k = 0; k < a.nnuc; ++k) {
+      const V3 R{a.nuc[4 * k + 1], a.nuc[4 * k + 2], a.nuc[4 * k + 3]};
+      const double r = v3dist(x, R);
+      if (r < 1e-14) atomicOr(a.flags, 1);
+      v -= a.nuc[4 * k] / r;
+    }
+    return v;
+  }
+  if (a.kind == kAsmSoftCoulomb) {  // external_potential, eps > 0 (model.cpp:163-173)
+    double v = 0.0;
+    for (int k = 0; k < a.nnuc; ++k) {
+      const V3 d = v3sub(x, V3{a.nuc[4 * k + 1], a.nuc[4 * k + 2], a.nuc[4 * k + 3]});
+      v -= a.nuc[4 * k] / sqrt(v3dot(d, d) + a.eps2);
+    }
+    return v;
+  }
+  if (a.kind == kAsmHarmonic) return a.scale * (x.x * x.x + x.y * x.y + x.z * x.z);
+  // kAsmScf: scf_potential_field (paro.cpp:433-444)
+  double bary[4];
+  barycentric(P, x, bary);
+  const double rho_q = eval_in_element(a.rho, a.box.s, vtx, bary);
+  const Lda l = lda_vxc(rho_q, a.exchange_only != 0, a.cx);
+  return eval_in_element(a.vh, a.box.s, vtx, bary) + l.v;
+}
+
+__global__ void __launch_bounds__(128) assemble_kernel(const AsmArgs a) {
+  const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (t >= a.n) return;
+  const int s = a.box.s;
+  const long long S = s - 1;
+  const int I = static_cast<int>(t % S) + 1;
+  const int J = static_cast<int>((t / S) % S) + 1;
+  const int K = static_cast<int>(t / (S * S)) + 1;
+
+  double acc[kSlots];
+#pragma unroll
+  for (int o = 0; o < kSlots; ++o) acc[o] = 0.0;
+
+  for (int dk = -1; dk <= 0; ++dk)
+    for (int dj = -1; dj <= 0; ++dj)
+      for (int di = -1; di <= 0; ++di) {
+        const int ci = I + di, cj = J + dj, ck = K + dk;
+        const int lv[3] = {I - ci, J - cj, K - ck};
+        for (int p = 0; p < 6; ++p) {
+          int tc[4][3];
+          tet_corners(p, tc);
+          int iv = -1;
+          for (int i = 0; i < 4; ++i)
+            if (tc[i][0] == lv[0] && tc[i][1] == lv[1] && tc[i][2] == lv[2]) iv = i;
+          if (iv < 0) continue;
+          int vtx[4][3];
+          V3 P[4];
+          for (int i = 0; i < 4; ++i) {
+            vtx[i][0] = ci + tc[i][0];
+            vtx[i][1] = cj + tc[i][1];
+            vtx[i][2] = ck + tc[i][2];
+            P[i] = V3{a.box.coord(vtx[i][0]), a.box.coord(vtx[i][1]), a.box.coord(vtx[i][2])};
+          }
+          const double vol = tet_volume(P);
+          double row[4] = {0.0, 0.0, 0.0, 0.0};  // local[max(iv,j)][min(iv,j)]
+          if (a.kind == kAsmMass) {
+            for (int j = 0; j < 4; ++j) row[j] = vol * (j == iv ? 2.0 : 1.0) / 20.0;
+          } else if (a.kind == kAsmStiffness) {
+            const V3 ea = v3sub(P[1], P[0]), eb = v3sub(P[2], P[0]), ec = v3sub(P[3], P[0]);
+            const double det = v3dot(ea, v3cross(eb, ec));
+            V3 g[4];
+            g[1] = v3scale(1.0 / det, v3cross(eb, ec));
+            g[2] = v3scale(1.0 / det, v3cross(ec, ea));
+            g[3] = v3scale(1.0 / det, v3cross(ea, eb));
+            V3 sum{0.0, 0.0, 0.0};
+            for (int i = 1; i <= 3; ++i) sum = v3add(sum, g[i]);
+            g[0] = V3{-sum.x, -sum.y, -sum.z};
+            const double m = a.scale;
+            for (int q = 0; q < a.nq; ++q) {
+              const double w = a.qw[q] * vol;
+              for (int j = 0; j < 4; ++j) {
+                const int hi = iv > j ? iv : j, lo = iv > j ? j : iv;
+                const V3 gi = g[hi];
+                // Mat3::identity(m).apply(gi) (geometry.hpp:43-47)
+                const V3 agi{m * gi.x + 0.0 * gi.y + 0.0 * gi.z, 0.0 * gi.x + m * gi.y + 0.0 * gi.z,
+                             0.0 * gi.x + 0.0 * gi.y + m * gi.z};
+                row[j] += w * (v3dot(agi, g[lo]) + 0.0 * a.qp[4 * q + hi] * a.qp[4 * q + lo]);
+              }
+            }
+          } else {
+            // pick_weighted_rule (fem.cpp:272-287)
+            int nq = a.nq;
+            const double* qp = a.qp;
+            const double* qw = a.qw;
+            if (a.singular) {
+              double h = 0.0;
+              for (int i = 0; i <= 3; ++i)
+                for (int j = i + 1; j <= 3; ++j) h = fmax(h, v3dist(P[i], P[j]));
+              V3 bc{0.0, 0.0, 0.0};
+              for (int i = 0; i <= 3; ++i) bc = v3add(bc, P[i]);
+              bc = v3scale(1.0 / 4, bc);
+              for (int k = 0; k < a.nnuc; ++k) {
+                const V3 R{a.nuc[4 * k + 1], a.nuc[4 * k + 2], a.nuc[4 * k + 3]};
+                if (v3dist(bc, R) < 1.5 * h) {
+                  double br[4];
+                  barycentric(P, R, br);
+                  bool near = true;
+                  for (int i = 0; i <= 3; ++i) near = near && br[i] > -0.25;
+                  if (near) {
+                    nq = a.nqs;
+                    qp = a.qps;
+                    qw = a.qws;
+                    break;
+                  }
+                }
+              }
+            }
+            for (int q = 0; q < nq; ++q) {
+              const V3 x = quad_point(P, qp + 4 * q);
+              const double wq = weight_at(a, P, vtx, x);
+              if (!isfinite(wq)) atomicOr(a.flags, 2);
+              const double ww = qw[q] * vol * wq;
+              for (int j = 0; j < 4; ++j) {
+                const int hi = iv > j ? iv : j, lo = iv > j ? j : iv;
+                row[j] += ww * qp[4 * q + hi] * qp[4 * q + lo];
+              }
+            }
+          }
+          for (int j = 0; j < 4; ++j) {
+            const int ox = tc[j][0] - tc[iv][0], oy = tc[j][1] - tc[iv][1], oz = tc[j][2] - tc[iv][2];
+            if (j == iv) acc[0] += row[j];
+            else if (ox >= 0 && oy >= 0 && oz >= 0) acc[ox + 2 * oy + 4 * oz] += row[j];
+          }
+        }
+      }
+#pragma unroll
+  for (int o = 0; o < kSlots; ++o) {
+    double v = acc[o];
+    if (a.kind == kAsmScf && a.vext_coef) {
+      // ks_form_matrix: a = kinetic; a += vext_mass; a += scf_mass
+      const double kin = a.kin_coef ? a.kin_coef[o * a.n + t] : a.kin_w[o];
+      v = (kin + a.vext_coef[o * a.n + t]) + v;
+    }
+    a.out[o * a.n + t] = v;
+  }
+}
+
+// Uniform-operator detection: compare every defined slot with dof 0's.
+__global__ void uniform_kernel(const double* coef, long long n, int S, int* mismatch) {
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int x = static_cast<int>(t % S), y = static_cast<int>((t / S) % S), z = static_cast<int>(t / (static_cast<long long>(S) * S));
+    for (int o = 0; o < kSlots; ++o) {
+      if (x + (o & 1) >= S || y + ((o >> 1) & 1) >= S || z + ((o >> 2) & 1) >= S) continue;
+      if (coef[o * n + t] != coef[o * n]) *mismatch = 1;
+    }
+  }
+}
+
+struct RuleDev {
+  double* p = nullptr;
+  double* w = nullptr;
+  int n = 0;
+};
+
+RuleDev upload_rule(DevBuf& buf, const Rule& r) {
+  const size_t m = r.points.size();
+  std::vector<double> host(5 * m);
+  for (size_t q = 0; q < m; ++q) {
+    for (int c = 0; c < 4; ++c) host[4 * q + c] = r.points[q][c];
+    host[4 * m + q] = r.weights[q];
+  }
+  double* d = buf.get<double>(host.size());
+  PARO_CUDA(cudaMemcpy(d, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice));
+  return {d, d + 4 * m, static_cast<int>(m)};
+}
+
+}  // namespace
+
+void assemble(Ctx& ctx, const AssembleSpec& spec, Op& out) {
+  ctx.check_grid();
+  const Grid& g = ctx.grid;
+  if (!out.var || !out.coef) throw ParoError(kInvalidArgument, "assemble: output must be a variable operator");
+  static thread_local DevBuf rule_main, rule_sub, nuc_buf, flag_buf;
+  AsmArgs a;
+  a.box = Box{g.s, g.lo, g.hi};
+  a.n = g.n;
+  a.kind = spec.kind;
+  a.scale = spec.scale;
+  a.out = out.coef;
+  int* flags = flag_buf.get<int>(1);
+  PARO_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), ctx.stream));
+  a.flags = flags;
+  const bool wmass = spec.kind != kAsmMass && spec.kind != kAsmStiffness;
+  const bool singular = spec.kind == kAsmCoulomb;
+  // stiffness and non-singular weighted masses use simplex_rule(3, 2);
+  // the singular policy uses degree 5 everywhere and the 2-level subdivided
+  // degree-5 rule near a nucleus (SingularQuadPolicy, fem.hpp:71-76)
+  const RuleDev main = upload_rule(rule_main, simplex_rule3(singular ? 5 : 2));
+  a.nq = main.n;
+  a.qp = main.p;
+  a.qw = main.w;
+  if (singular) {
+    const RuleDev sub = upload_rule(rule_sub, subdivided_rule3(5, 2));
+    a.nqs = sub.n;
+    a.qps = sub.p;
+    a.qws = sub.w;
+    a.singular = 1;
+  }
+  if (wmass && (spec.kind == kAsmCoulomb || spec.kind == kAsmSoftCoulomb)) {
+    const std::vector<double>& nuc = spec.nuclei;
+    if (nuc.empty() || nuc.size() % 4 != 0) throw ParoError(kInvalidArgument, "external_potential: no nuclei");
+    double* d = nuc_buf.get<double>(nuc.size() + 1);
+    PARO_CUDA(cudaMemcpy(d, nuc.data(), sizeof(double) * nuc.size(), cudaMemcpyHostToDevice));
+    a.nuc = d;
+    a.nnuc = static_cast<int>(nuc.size() / 4);
+    a.eps2 = spec.eps * spec.eps;
+  }
+  if (spec.kind == kAsmScf) {
+    a.rho = spec.rho;
+    a.vh = spec.vh;
+    a.exchange_only = spec.exchange_only;
+    a.cx = std::cbrt(3.0 / M_PI);
+    if (spec.kinetic) {
+      a.kin_coef = spec.kinetic->var ? spec.kinetic->coef : nullptr;
+      for (int o = 0; o < kSlots; ++o) a.kin_w[o] = spec.kinetic->w[o];
+    }
+    a.vext_coef = spec.vext ? spec.vext->coef : nullptr;
+    if (spec.vext && !spec.vext->var) throw ParoError(kInvalidArgument, "ks form: V_ext mass must be variable");
+  }
+  const long long blocks = (g.n + 127) / 128;
+  assemble_kernel<<<static_cast<unsigned>(blocks), 128, 0, ctx.stream>>>(a);
+  ++ctx.launches;
+  PARO_CUDA(cudaGetLastError());
+  int hflags = 0;
+  PARO_CUDA(cudaMemcpyAsync(&hflags, flags, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  PARO_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (hflags & 1) throw ParoError(kError, "external potential evaluated at a nucleus");
+  if (hflags & 2) throw ParoError(kError, "weighted mass: non-finite coefficient");
+}
+
+namespace {
+
+// this += s * other (SparseOperator::add_scaled, linalg.cpp:120-125)
+__global__ void add_scaled_kernel(double* a, const double* b, const double* bw, double s, long long n) {
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < 8 * n;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double bv = b ? b[t] : bw[t / n];
+    a[t] += s * bv;
+  }
+}
+
+}  // namespace
+
+void add_scaled(Ctx& ctx, Op& a, const Op& b, double s) {
+  if (!a.var && !b.var) {
+    for (int o = 0; o < kSlots; ++o) a.w[o] += s * b.w[o];
+    return;
+  }
+  const long long n = ctx.grid.n;
+  if (!a.var) {  // promote to a variable operator
+    double* coef = nullptr;
+    PARO_CUDA(cudaMalloc(&coef, sizeof(double) * kSlots * n));
+    std::vector<double> w(kSlots * 1);
+    for (int o = 0; o < kSlots; ++o) {
+      std::vector<double> col(n, a.w[o]);
+      PARO_CUDA(cudaMemcpy(coef + o * n, col.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+    }
+    a.coef = coef;
+    a.owns = true;
+    a.var = true;
+    a.n = n;
+  }
+  static thread_local DevBuf wbuf;
+  double* dw = wbuf.get<double>(kSlots);
+  PARO_CUDA(cudaMemcpyAsync(dw, b.w, sizeof(double) * kSlots, cudaMemcpyHostToDevice, ctx.stream));
+  add_scaled_kernel<<<148 * 8, 256, 0, ctx.stream>>>(a.coef, b.var ? b.coef : nullptr, dw, s, n);
+  ++ctx.launches;
+  PARO_CUDA(cudaGetLastError());
+  PARO_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+
+bool make_uniform_if_possible(Ctx& ctx, Op& op) {
+  if (!op.var) return true;
+  static thread_local DevBuf flag_buf;
+  int* d = flag_buf.get<int>(1);
+  PARO_CUDA(cudaMemsetAsync(d, 0, sizeof(int), ctx.stream));
+  uniform_kernel<<<148 * 8, 256, 0, ctx.stream>>>(op.coef, op.n, ctx.grid.S, d);
+  ++ctx.launches;
+  int h = 0;
+  PARO_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  PARO_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (h) return false;
+  double w[kSlots];
+  for (int o = 0; o < kSlots; ++o)
+    PARO_CUDA(cudaMemcpy(&w[o], op.coef + o * op.n, sizeof(double), cudaMemcpyDeviceToHost));
+  if (op.owns) cudaFree(op.coef);
+  op.coef = nullptr;
+  op.owns = false;
+  op.var = false;
+  for (int o = 0; o < kSlots; ++o) op.w[o] = w[o];
+  return true;
+}
+
+}  // namespace paro_b200

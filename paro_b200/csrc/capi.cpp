@@ -9,6 +9,8 @@
 #include <vector>
 
 #include "ctx.hpp"
+#include "assemble.hpp"
+#include "fields.hpp"
 #include "ritz.hpp"
 #include "solver.hpp"
 
@@ -386,6 +388,153 @@ int paro_rayleigh_ritz(paro_ctx* ctx, const paro_op* a, const paro_op* b, int k,
 
 int paro_dense_sym_geneig(paro_ctx* ctx, int m, const double* a, const double* b, double* vals, double* vecs) {
   return guarded(ctx, [&] { return dense_sym_geneig(ctx->c, m, a, b, vals, vecs); });
+}
+
+static paro_op* new_var_op(paro_ctx* ctx) {
+  auto* op = new paro_op();
+  op->owner = ctx;
+  op->o.var = true;
+  op->o.n = ctx->c.grid.n;
+  PARO_CUDA(cudaMalloc(&op->o.coef, sizeof(double) * kSlots * op->o.n));
+  op->o.owns = true;
+  return op;
+}
+
+static int assemble_new(paro_ctx* ctx, const AssembleSpec& spec, bool try_uniform, paro_op** out) {
+  ctx->c.check_grid();
+  paro_op* op = new_var_op(ctx);
+  try {
+    assemble(ctx->c, spec, op->o);
+    if (try_uniform) make_uniform_if_possible(ctx->c, op->o);
+  } catch (...) {
+    paro_op_destroy(op);
+    throw;
+  }
+  *out = op;
+  return kOk;
+}
+
+int paro_assemble_mass(paro_ctx* ctx, paro_op** out) {
+  return guarded(ctx, [&] {
+    AssembleSpec s;
+    s.kind = kAsmMass;
+    return assemble_new(ctx, s, true, out);
+  });
+}
+
+int paro_assemble_stiffness(paro_ctx* ctx, double scale, paro_op** out) {
+  return guarded(ctx, [&] {
+    AssembleSpec s;
+    s.kind = kAsmStiffness;
+    s.scale = scale;
+    return assemble_new(ctx, s, true, out);
+  });
+}
+
+int paro_assemble_vext(paro_ctx* ctx, int nnuc, const double* charges, const double* positions, double eps,
+                       paro_op** out) {
+  return guarded(ctx, [&] {
+    AssembleSpec s;
+    s.kind = eps == 0.0 ? kAsmCoulomb : kAsmSoftCoulomb;
+    s.eps = eps;
+    for (int k = 0; k < nnuc; ++k) {
+      s.nuclei.push_back(charges[k]);
+      for (int c = 0; c < 3; ++c) s.nuclei.push_back(positions[3 * k + c]);
+    }
+    return assemble_new(ctx, s, false, out);
+  });
+}
+
+int paro_assemble_harmonic(paro_ctx* ctx, double c, paro_op** out) {
+  return guarded(ctx, [&] {
+    AssembleSpec s;
+    s.kind = kAsmHarmonic;
+    s.scale = c;
+    return assemble_new(ctx, s, false, out);
+  });
+}
+
+int paro_op_add_scaled(paro_ctx* ctx, paro_op* a, const paro_op* b, double s) {
+  return guarded(ctx, [&] {
+    add_scaled(ctx->c, a->o, b->o, s);
+    return kOk;
+  });
+}
+
+int paro_ks_form(paro_ctx* ctx, const paro_op* kinetic, const paro_op* vext, const double* rho, const double* vh,
+                 int exchange_only, paro_op* out, long long* clamped) {
+  return guarded(ctx, [&] {
+    if (!out->o.var) throw ParoError(kInvalidArgument, "ks_form: output must be a variable operator");
+    AssembleSpec s;
+    s.kind = kAsmScf;
+    s.rho = rho;
+    s.vh = vh;
+    s.exchange_only = exchange_only;
+    s.kinetic = &kinetic->o;
+    s.vext = &vext->o;
+    assemble(ctx->c, s, out->o);
+    if (clamped) *clamped = static_cast<long long>(cell_reduce(ctx->c, kCellClamp, rho, nullptr, exchange_only));
+    return kOk;
+  });
+}
+
+int paro_density(paro_ctx* ctx, int nocc, const double* u, long long ld, const double* occ, double* rho,
+                 double* raw_integral) {
+  return guarded(ctx, [&] {
+    const double raw = density(ctx->c, nocc, u, ld, occ, rho);
+    if (raw_integral) *raw_integral = raw;
+    return kOk;
+  });
+}
+
+int paro_mix_density(paro_ctx* ctx, const double* rho_in, const double* rho_out, double alpha, double* out) {
+  return guarded(ctx, [&] {
+    mix(ctx->c, rho_in, rho_out, alpha, out);
+    return kOk;
+  });
+}
+
+int paro_integrate(paro_ctx* ctx, const double* f, double* out) {
+  return guarded(ctx, [&] {
+    *out = cell_reduce(ctx->c, kCellIntegrate, f, nullptr, 0);
+    return kOk;
+  });
+}
+
+int paro_norm_l2(paro_ctx* ctx, const double* f, double* out) {
+  return guarded(ctx, [&] {
+    *out = norm_l2(ctx->c, f);
+    return kOk;
+  });
+}
+
+int paro_integrate_product(paro_ctx* ctx, const double* u, const double* v, double* out) {
+  return guarded(ctx, [&] {
+    *out = cell_reduce(ctx->c, kCellProduct, u, v, 0);
+    return kOk;
+  });
+}
+
+int paro_rho_residual(paro_ctx* ctx, const double* rho_out, const double* rho_in, double* scratch, double* out) {
+  return guarded(ctx, [&] {
+    diff(ctx->c, rho_out, rho_in, scratch);
+    *out = norm_l2(ctx->c, scratch);
+    return kOk;
+  });
+}
+
+int paro_total_energy(paro_ctx* ctx, int n_lambdas, const double* lambdas, int nocc, const double* occ,
+                      const double* rho, const double* vh, int exchange_only, int nnuc, const double* charges,
+                      const double* positions, double* e_out) {
+  return guarded(ctx, [&] {
+    std::vector<double> nuc;
+    for (int k = 0; k < nnuc; ++k) {
+      nuc.push_back(charges[k]);
+      for (int c = 0; c < 3; ++c) nuc.push_back(positions[3 * k + c]);
+    }
+    *e_out = total_energy(ctx->c, n_lambdas, lambdas, nocc, occ, rho, vh, exchange_only, nnuc, nuc.data());
+    return kOk;
+  });
 }
 
 int paro_fix_sign(paro_ctx* ctx, int k, double* v, long long ld) {

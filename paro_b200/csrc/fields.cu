@@ -1,0 +1,247 @@
+// Nodal fields on the device (compiled -fmad=false): density, mixing and the
+// element reductions of the energy / norms.
+//   density_from_orbitals (model.cpp:192-223), mix_density (model.cpp:225-236),
+//   integrate (fem.cpp:419-430), norm_l2 (fem.cpp:432-448),
+//   integrate_product (model.cpp:306-327), total_energy (model.cpp:329-360).
+// Element sums run one cell (6 Kuhn tets) per thread with a fixed-order
+// block/partial reduction, so results are deterministic run to run.
+#include <cmath>
+#include <vector>
+
+#include "fem.cuh"
+#include "fields.hpp"
+#include "quad.hpp"
+
+namespace paro_b200 {
+
+namespace {
+
+constexpr int kRedThreads = 256;
+
+__global__ void density_kernel(int nocc, const double* U, long long ld, const double* occ, long long n,
+                               double* rho) {
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double r = 0.0;
+    for (int i = 0; i < nocc; ++i) {
+      const double u = U[i * ld + k];
+      r += occ[i] * u * u;
+    }
+    rho[k] = r;
+  }
+}
+
+__global__ void scale_kernel(double* f, long long n, double s) {
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<long long>(gridDim.x) * blockDim.x)
+    f[k] *= s;
+}
+
+__global__ void mix_kernel(const double* a, const double* b, double alpha, long long n, double* out) {
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<long long>(gridDim.x) * blockDim.x)
+    out[k] = (1.0 - alpha) * a[k] + alpha * b[k];
+}
+
+__global__ void diff_kernel(const double* a, const double* b, long long n, double* out) {
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<long long>(gridDim.x) * blockDim.x)
+    out[k] = a[k] - b[k];
+}
+
+struct CellArgs {
+  Box box;
+  int mode;
+  const double* f;
+  const double* g;
+  const double* qp;  // 4-point rule
+  const double* qw;
+  int exchange_only;
+  double cx;
+  double* partials;
+};
+
+__device__ __forceinline__ double vval(const double* f, int s, int vx, int vy, int vz) {
+  const long long d = vertex_dof(s, vx, vy, vz);
+  return d >= 0 ? f[d] : 0.0;
+}
+
+__global__ void __launch_bounds__(kRedThreads) cell_reduce_kernel(const CellArgs a) {
+  __shared__ double sh[kRedThreads / 32];
+  const int s = a.box.s;
+  const long long ncell = static_cast<long long>(s) * s * s;
+  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  double acc = 0.0;
+  if (c < ncell) {
+    const int ci = static_cast<int>(c % s), cj = static_cast<int>((c / s) % s), ck = static_cast<int>(c / (static_cast<long long>(s) * s));
+    for (int p = 0; p < 6; ++p) {
+      int tc[4][3];
+      tet_corners(p, tc);
+      int vtx[4][3];
+      V3 P[4];
+      double fv[4], gv[4];
+      for (int i = 0; i < 4; ++i) {
+        vtx[i][0] = ci + tc[i][0];
+        vtx[i][1] = cj + tc[i][1];
+        vtx[i][2] = ck + tc[i][2];
+        P[i] = V3{a.box.coord(vtx[i][0]), a.box.coord(vtx[i][1]), a.box.coord(vtx[i][2])};
+        fv[i] = vval(a.f, s, vtx[i][0], vtx[i][1], vtx[i][2]);
+        gv[i] = a.g ? vval(a.g, s, vtx[i][0], vtx[i][1], vtx[i][2]) : 0.0;
+      }
+      const double vol = tet_volume(P);
+      if (a.mode == kCellIntegrate) {
+        double sm = 0.0;
+        for (int i = 0; i < 4; ++i) sm += fv[i];
+        acc += vol * sm / 4;
+      } else if (a.mode == kCellNorm2) {
+        double sum = 0.0, sq = 0.0;
+        for (int i = 0; i < 4; ++i) {
+          sum += fv[i];
+          sq += fv[i] * fv[i];
+        }
+        acc += vol * (sq + sum * sum) / 20.0;
+      } else if (a.mode == kCellProduct) {
+        double su = 0, sv = 0, sp = 0;
+        for (int i = 0; i < 4; ++i) {
+          su += fv[i];
+          sv += gv[i];
+          sp += fv[i] * gv[i];
+        }
+        acc += vol * (sp + su * sv) / 20.0;
+      } else if (a.mode == kCellExc) {
+        for (int q = 0; q < 4; ++q) {
+          double r = 0.0;
+          for (int i = 0; i < 4; ++i)
+            if (vertex_dof(s, vtx[i][0], vtx[i][1], vtx[i][2]) >= 0) r += a.qp[4 * q + i] * fv[i];
+          const double rho_q = fmax(0.0, r);
+          const Lda x = lda_vxc(rho_q, a.exchange_only != 0, a.cx);
+          acc += a.qw[q] * vol * (x.e - x.v) * rho_q;
+        }
+      } else {  // kCellClamp: (element, point) pairs where the KS form clamps rho
+        for (int q = 0; q < 4; ++q) {
+          const V3 x = quad_point(P, a.qp + 4 * q);
+          double bary[4];
+          barycentric(P, x, bary);
+          double r = 0.0;
+          for (int i = 0; i < 4; ++i)
+            if (vertex_dof(s, vtx[i][0], vtx[i][1], vtx[i][2]) >= 0) r += bary[i] * fv[i];
+          if (r < 0.0) acc += 1.0;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kRedThreads / 32; ++w) t += sh[w];
+    a.partials[blockIdx.x] = t;
+  }
+}
+
+__global__ void sum_kernel(const double* p, long long m, double* out) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < m; i += blockDim.x) s += p[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += sh[w];
+    *out = t;
+  }
+}
+
+int grid1d(long long n) { return static_cast<int>(std::min<long long>(148 * 16, (n + 255) / 256)); }
+
+}  // namespace
+
+double cell_reduce(Ctx& ctx, int mode, const double* f, const double* g, int exchange_only) {
+  ctx.check_grid();
+  const Grid& gr = ctx.grid;
+  static thread_local DevBuf rule, part;
+  const Rule& r4 = simplex_rule3(2);
+  std::vector<double> host(20);
+  for (int q = 0; q < 4; ++q) {
+    for (int c = 0; c < 4; ++c) host[4 * q + c] = r4.points[q][c];
+    host[16 + q] = r4.weights[q];
+  }
+  double* drule = rule.get<double>(20);
+  PARO_CUDA(cudaMemcpyAsync(drule, host.data(), sizeof(double) * 20, cudaMemcpyHostToDevice, ctx.stream));
+  const long long ncell = static_cast<long long>(gr.s) * gr.s * gr.s;
+  const long long blocks = (ncell + kRedThreads - 1) / kRedThreads;
+  double* partials = part.get<double>(blocks + 1);
+  CellArgs a{Box{gr.s, gr.lo, gr.hi}, mode, f, g, drule, drule + 16, exchange_only, std::cbrt(3.0 / M_PI), partials};
+  cell_reduce_kernel<<<static_cast<unsigned>(blocks), kRedThreads, 0, ctx.stream>>>(a);
+  sum_kernel<<<1, 1024, 0, ctx.stream>>>(partials, blocks, partials + blocks);
+  ctx.launches += 2;
+  PARO_CUDA(cudaGetLastError());
+  double out = 0.0;
+  PARO_CUDA(cudaMemcpyAsync(&out, partials + blocks, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+  PARO_CUDA(cudaStreamSynchronize(ctx.stream));
+  host.clear();
+  return out;
+}
+
+double density(Ctx& ctx, int nocc, const double* U, long long ld, const double* occ_host, double* rho) {
+  ctx.check_grid();
+  if (nocc <= 0) throw ParoError(kInvalidArgument, "density: orbital/occupation count mismatch");
+  double total = 0.0;
+  for (int i = 0; i < nocc; ++i) {
+    if (occ_host[i] < 0.0) throw ParoError(kInvalidArgument, "density: negative occupation");
+    total += occ_host[i];
+  }
+  static thread_local DevBuf occ;
+  double* docc = occ.get<double>(nocc);
+  PARO_CUDA(cudaMemcpyAsync(docc, occ_host, sizeof(double) * nocc, cudaMemcpyHostToDevice, ctx.stream));
+  const long long n = ctx.grid.n;
+  density_kernel<<<grid1d(n), 256, 0, ctx.stream>>>(nocc, U, ld, docc, n, rho);
+  ++ctx.launches;
+  const double raw = cell_reduce(ctx, kCellIntegrate, rho, nullptr, 0);
+  if (total > 0.0 && raw > 0.0) {
+    scale_kernel<<<grid1d(n), 256, 0, ctx.stream>>>(rho, n, total / raw);
+    ++ctx.launches;
+  }
+  PARO_CUDA(cudaGetLastError());
+  return raw;
+}
+
+void mix(Ctx& ctx, const double* rin, const double* rout, double alpha, double* out) {
+  const long long n = ctx.grid.n;
+  mix_kernel<<<grid1d(n), 256, 0, ctx.stream>>>(rin, rout, alpha, n, out);
+  ++ctx.launches;
+  PARO_CUDA(cudaGetLastError());
+}
+
+void diff(Ctx& ctx, const double* a, const double* b, double* out) {
+  const long long n = ctx.grid.n;
+  diff_kernel<<<grid1d(n), 256, 0, ctx.stream>>>(a, b, n, out);
+  ++ctx.launches;
+  PARO_CUDA(cudaGetLastError());
+}
+
+double norm_l2(Ctx& ctx, const double* f) { return std::sqrt(std::max(0.0, cell_reduce(ctx, kCellNorm2, f, nullptr, 0))); }
+
+double total_energy(Ctx& ctx, int nl, const double* lambdas, int nocc, const double* occ, const double* rho,
+                    const double* vh, int exchange_only, int nnuc, const double* nuclei) {
+  if (nl < nocc) throw ParoError(kInvalidArgument, "total_energy: missing eigenvalue estimates");
+  double e_band = 0.0;
+  for (int i = 0; i < nocc; ++i) e_band += occ[i] * lambdas[i];
+  const double e_hartree = 0.5 * cell_reduce(ctx, kCellProduct, vh, rho, 0);
+  const double e_xc = cell_reduce(ctx, kCellExc, rho, nullptr, exchange_only);
+  // nuclear_repulsion (model.cpp:177-186)
+  double enn = 0.0;
+  for (int k = 0; k < nnuc; ++k)
+    for (int l = k + 1; l < nnuc; ++l) {
+      const double dx = nuclei[4 * k + 1] - nuclei[4 * l + 1], dy = nuclei[4 * k + 2] - nuclei[4 * l + 2],
+                   dz = nuclei[4 * k + 3] - nuclei[4 * l + 3];
+      enn += nuclei[4 * k] * nuclei[4 * l] / std::sqrt(dx * dx + dy * dy + dz * dz);
+    }
+  return e_band - e_hartree + e_xc + enn;
+}
+
+}  // namespace paro_b200

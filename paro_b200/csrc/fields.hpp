@@ -1,0 +1,19 @@
+// Nodal fields: density, mixing, norms, energy (see fields.cu).
+#pragma once
+
+#include "ctx.hpp"
+
+namespace paro_b200 {
+
+enum CellMode : int { kCellIntegrate = 0, kCellNorm2 = 1, kCellProduct = 2, kCellExc = 3, kCellClamp = 4 };
+
+double cell_reduce(Ctx& ctx, int mode, const double* f, const double* g, int exchange_only);
+// rho = sum_i occ_i u_i^2, normalised to sum occ; returns the raw integral
+double density(Ctx& ctx, int nocc, const double* U, long long ld, const double* occ_host, double* rho);
+void mix(Ctx& ctx, const double* rin, const double* rout, double alpha, double* out);
+void diff(Ctx& ctx, const double* a, const double* b, double* out);
+double norm_l2(Ctx& ctx, const double* f);
+double total_energy(Ctx& ctx, int nl, const double* lambdas, int nocc, const double* occ, const double* rho,
+                    const double* vh, int exchange_only, int nnuc, const double* nuclei);
+
+}  // namespace paro_b200
