@@ -54,6 +54,10 @@ double paro_ctx_last_residual(const paro_ctx* ctx);
 /* kernels launched by this library so far (CUDA-graph nodes counted) */
 unsigned long long paro_ctx_launches(const paro_ctx* ctx);
 int paro_ctx_synchronize(paro_ctx* ctx);
+/* Step-4 orthonormalisation: 0 = Cholesky-QR twice with an automatic
+ * Gram-Schmidt fallback for near-dependent candidates (default), 1 = always
+ * two-pass Gram-Schmidt (b_orthonormalize's algorithm, linalg.cpp:409-439). */
+int paro_ctx_set_ritz_mode(paro_ctx* ctx, int mode);
 
 /* Device memory helpers for callers without their own allocator. */
 int paro_malloc(paro_ctx* ctx, size_t bytes, void** dev);
@@ -104,6 +108,14 @@ int paro_cg_solve(paro_ctx* ctx, const paro_op* a, int k, const double* b, const
 int paro_source_solve_step(paro_ctx* ctx, const paro_op* a, const paro_op* b, int k, const double* u_prev,
                            long long ld, const double* lambdas, double tol, size_t max_iter, double sigma,
                            double* u_half, size_t* iterations, double* residual);
+/* The same batched solve reporting per-column outcomes instead of collapsing
+ * them into one exception (for callers that shard the orbitals over several
+ * GPUs and decide globally): first_status / final_status host arrays of k
+ * (PARO_OK, PARO_NOT_SPD, PARO_ITERATION_LIMIT), NULL to skip. */
+int paro_source_solve_columns(paro_ctx* ctx, const paro_op* a, const paro_op* b, int k, const double* u_prev,
+                              long long ld, const double* lambdas, double tol, size_t max_iter, double sigma,
+                              double* u_half, size_t* iterations, double* residual, int* first_status,
+                              int* final_status);
 /* shifted_source_step (paro.cpp:194-210): sigma = max(0, 0.5 - lambda_1),
  * 2 sigma + 1 on NotSpd, at most 5 attempts; sigma_out: host. */
 int paro_shifted_source_step(paro_ctx* ctx, const paro_op* a, const paro_op* b, int k, const double* u_prev,
@@ -123,6 +135,10 @@ int paro_hartree_solve(paro_ctx* ctx, const paro_op* poisson, const paro_op* mas
 int paro_rayleigh_ritz(paro_ctx* ctx, const paro_op* a_form, const paro_op* b, int k, const double* cands,
                        long long ld, size_t min_keep, double drop_tol, double* lambdas, double* orbitals,
                        long long ldo, int* k_out, double* gram_defect);
+/* b_orthonormalize (linalg.cpp:409-439): two-pass Gram-Schmidt in the B inner
+ * product with the relative drop rule; u, q: device (ld == n); k_out: host. */
+int paro_b_orthonormalize(paro_ctx* ctx, const paro_op* b, int k, const double* u, double drop_tol, double* q,
+                          int* k_out);
 /* dense_sym_geneig on one warp of the device, host row-major m x m in/out. */
 int paro_dense_sym_geneig(paro_ctx* ctx, int m, const double* a, const double* b, double* values, double* vectors);
 /* fix_sign (linalg.cpp:229-241) on k device columns. */

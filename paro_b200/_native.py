@@ -79,6 +79,7 @@ SIGNATURES = {
     "paro_ctx_last_residual": (_D, [_P]),
     "paro_ctx_launches": (C.c_ulonglong, [_P]),
     "paro_ctx_synchronize": (_I, [_P]),
+    "paro_ctx_set_ritz_mode": (_I, [_P, _I]),
     "paro_malloc": (_I, [_P, _SZ, C.POINTER(_P)]),
     "paro_free": (_I, [_P, _P]),
     "paro_memcpy_h2d": (_I, [_P, _P, _P, _SZ]),
@@ -95,10 +96,13 @@ SIGNATURES = {
     "paro_op_apply": (_I, [_P, _P, _P, _D, _I, _P, _LL, _P, _LL]),
     "paro_cg_solve": (_I, [_P, _P, _I, _P, _P, _LL, _D, _SZ, _I, _P, _SZP, _DP]),
     "paro_source_solve_step": (_I, [_P, _P, _P, _I, _P, _LL, _DP, _D, _SZ, _D, _P, _SZP, _DP]),
+    "paro_source_solve_columns": (_I, [_P, _P, _P, _I, _P, _LL, _DP, _D, _SZ, _D, _P, _SZP, _DP, C.POINTER(_I),
+                                       C.POINTER(_I)]),
     "paro_shifted_source_step": (_I, [_P, _P, _P, _I, _P, _LL, _DP, _D, _SZ, _P, _DP, _SZP, _DP]),
     "paro_hartree_solve": (_I, [_P, _P, _P, _P, _D, _P, _SZP]),
     "paro_rayleigh_ritz": (_I, [_P, _P, _P, _I, _P, _LL, _SZ, _D, _DP, _P, _LL, C.POINTER(_I), _DP]),
     "paro_dense_sym_geneig": (_I, [_P, _I, _DP, _DP, _DP, _DP]),
+    "paro_b_orthonormalize": (_I, [_P, _P, _I, _P, _D, _P, C.POINTER(_I)]),
     "paro_fix_sign": (_I, [_P, _I, _P, _LL]),
     "paro_assemble_mass": (_I, [_P, C.POINTER(_P)]),
     "paro_assemble_stiffness": (_I, [_P, _D, C.POINTER(_P)]),

@@ -234,6 +234,27 @@ def source_solve_step(a: Operator, b: Operator, u_prev: torch.Tensor, lambdas, t
     return y
 
 
+def source_solve_columns(a: Operator, b: Operator, u_prev: torch.Tensor, lambdas, tol: float, max_iter: int,
+                         sigma: float, out: torch.Tensor):
+    """Batched Step 3 with per-column outcomes (no exception collapsing).
+
+    Returns (first_status, final_status, iterations, residual) lists; the
+    caller applies source_solve_step's exception order (paro.cpp:110-117)."""
+    ctx = a.ctx
+    u = _as_cols(u_prev, ctx.n)
+    k = u.shape[0]
+    lam = (C.c_double * k)(*[float(v) for v in lambdas])
+    it = (C.c_size_t * k)()
+    res = (C.c_double * k)()
+    fs = (C.c_int * k)()
+    ls = (C.c_int * k)()
+    st = N.lib().paro_source_solve_columns(ctx.h, a.h, b.h, k, _ptr(u), u.stride(0) if k > 1 else ctx.n, lam, tol,
+                                           max_iter, sigma, _ptr(out), it, res, fs, ls)
+    if st not in (0, N.NotSpdError.code, N.IterationLimitError.code):
+        ctx.check(st)
+    return list(fs), list(ls), list(it), list(res)
+
+
 def shifted_source_step(a: Operator, b: Operator, u_prev: torch.Tensor, lambdas, tol: float = 1e-10,
                         max_iter: int = 100000, out: torch.Tensor | None = None, report: dict | None = None):
     """shifted_source_step (paro.cpp:194-210) -> (u_half, sigma)."""
@@ -296,6 +317,16 @@ def rayleigh_ritz(candidates: torch.Tensor, a_form: Operator, b: Operator, min_k
     ctx.check(st)
     kk = kout.value
     return OrbitalSet(V[:kk], list(lam)[:kk], defect.value)
+
+
+def b_orthonormalize(vectors: torch.Tensor, b: Operator, drop_tol: float) -> torch.Tensor:
+    """b_orthonormalize (linalg.cpp:409-439) -> accepted B-orthonormal vectors [k, n]."""
+    ctx = b.ctx
+    U = _as_cols(vectors, ctx.n).contiguous()
+    Q = torch.empty_like(U)
+    k = C.c_int(0)
+    ctx.check(N.lib().paro_b_orthonormalize(ctx.h, b.h, U.shape[0], _ptr(U), float(drop_tol), _ptr(Q), C.byref(k)))
+    return Q[: k.value]
 
 
 def dense_sym_geneig(ctx: Context, A, B):

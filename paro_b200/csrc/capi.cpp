@@ -78,7 +78,8 @@ int paro_ctx_destroy(paro_ctx* ctx) {
   cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
   for (DevBuf* b : {&ctx->c.partials, &ctx->c.cols, &ctx->c.scale, &ctx->c.invd, &ctx->c.pbuf0, &ctx->c.pbuf1,
-                    &ctx->c.flag, &ctx->c.ws_a, &ctx->c.ws_b, &ctx->c.ws_c, &ctx->c.ws_small, &ctx->c.ws_small2,
+                    &ctx->c.flag, &ctx->c.ws_a, &ctx->c.ws_b, &ctx->c.ws_c, &ctx->c.ws_d, &ctx->c.ws_e,
+                    &ctx->c.ws_small, &ctx->c.ws_small2,
                     &ctx->c.ws_small3})
     b->release();
   if (ctx->c.cublas) cublasDestroy(ctx->c.cublas);
@@ -98,6 +99,13 @@ int paro_ctx_set_stream(paro_ctx* ctx, void* stream) {
 const char* paro_ctx_last_error(const paro_ctx* ctx) { return ctx ? ctx->c.err.c_str() : g_noctx_err.c_str(); }
 double paro_ctx_last_residual(const paro_ctx* ctx) { return ctx ? ctx->c.resid : 0.0; }
 unsigned long long paro_ctx_launches(const paro_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+int paro_ctx_set_ritz_mode(paro_ctx* ctx, int mode) {
+  return guarded(ctx, [&] {
+    ctx->c.force_cgs2 = mode == 1;
+    return kOk;
+  });
+}
 
 int paro_ctx_synchronize(paro_ctx* ctx) {
   return guarded(ctx, [&] {
@@ -347,10 +355,21 @@ int paro_cg_solve(paro_ctx* ctx, const paro_op* a, int k, const double* b, const
 int paro_source_solve_step(paro_ctx* ctx, const paro_op* a, const paro_op* b, int k, const double* u, long long ld,
                            const double* lambdas, double tol, size_t max_iter, double sigma, double* out,
                            size_t* iters, double* resid) {
+  return paro_source_solve_columns(ctx, a, b, k, u, ld, lambdas, tol, max_iter, sigma, out, iters, resid, nullptr,
+                                   nullptr);
+}
+
+int paro_source_solve_columns(paro_ctx* ctx, const paro_op* a, const paro_op* b, int k, const double* u,
+                              long long ld, const double* lambdas, double tol, size_t max_iter, double sigma,
+                              double* out, size_t* iters, double* resid, int* first_status, int* final_status) {
   return guarded(ctx, [&] {
     SolveReport rep;
     const int st = source_solve(ctx->c, a->o, b->o, sigma, k, u, ld, lambdas, tol, max_iter, out, &rep);
     fill_report(rep, iters, resid);
+    for (int c = 0; c < k; ++c) {
+      if (first_status) first_status[c] = rep.first_status.empty() ? kOk : rep.first_status[c];
+      if (final_status) final_status[c] = rep.status.empty() ? kOk : rep.status[c];
+    }
     return st;
   });
 }
@@ -384,6 +403,11 @@ int paro_rayleigh_ritz(paro_ctx* ctx, const paro_op* a, const paro_op* b, int k,
     return rayleigh_ritz(ctx->c, a->o, b->o, k, cands, ld, min_keep, drop_tol, lambdas, orbs, ldo, k_out, defect,
                          &info);
   });
+}
+
+int paro_b_orthonormalize(paro_ctx* ctx, const paro_op* b, int k, const double* u, double drop_tol, double* q,
+                          int* k_out) {
+  return guarded(ctx, [&] { return b_orthonormalize(ctx->c, b->o, k, u, drop_tol, q, k_out); });
 }
 
 int paro_dense_sym_geneig(paro_ctx* ctx, int m, const double* a, const double* b, double* vals, double* vecs) {

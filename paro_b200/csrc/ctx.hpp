@@ -55,7 +55,8 @@ struct Ctx {
   unsigned long long launches = 0;   // kernels launched by this library (graph nodes counted)
 
   DevBuf partials, cols, scale, invd, pbuf0, pbuf1, flag;
-  DevBuf ws_a, ws_b, ws_c, ws_small, ws_small2, ws_small3;
+  DevBuf ws_a, ws_b, ws_c, ws_d, ws_e, ws_small, ws_small2, ws_small3;
+  bool force_cgs2 = false;           // Step 4: skip the Cholesky-QR path
   int* pinned_count = nullptr;       // mapped host memory for the active-column poll
   int* pinned_count_dev = nullptr;
 

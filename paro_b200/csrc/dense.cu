@@ -356,6 +356,30 @@ __global__ void second_pass_kernel(int k, const double* G2, double* C2, double* 
   if (lane == 0) *status = kOk;
 }
 
+// Pencil in an explicitly orthonormalised basis Q (paro.cpp:143-150):
+// At = sym(Q^T A Q), Bt = sym(Q^T B Q) (column-major inputs), then
+// dense_sym_geneig; Y (column-major k x k) = X.
+__global__ void pencil_direct_kernel(int k, const double* GA, const double* GB, double* vals, double* Y, double* At,
+                                     double* Bt, double* X, DenseScratch w, int* status) {
+  const int lane = threadIdx.x;
+  for (int idx = lane; idx < k * k; idx += 32) {
+    const int i = idx / k, j = idx % k;
+    At[i * k + j] = 0.5 * (GA[i + j * k] + GA[j + i * k]);
+    Bt[i * k + j] = 0.5 * (GB[i + j * k] + GB[j + i * k]);
+  }
+  __syncwarp();
+  const int st = dense_sym_geneig_warp(k, At, Bt, vals, X, w);
+  if (st != kOk) {
+    if (lane == 0) *status = st;
+    return;
+  }
+  for (int idx = lane; idx < k * k; idx += 32) {
+    const int i = idx % k, j = idx / k;
+    Y[i + j * k] = X[i * k + j];
+  }
+  if (lane == 0) *status = kOk;
+}
+
 // Projected pencil in the orthonormal basis Q = Q1 C2 and its solve:
 // At = C2^T sym(GA) C2 (GA = Q1^T A Q1, column-major), symmetrised like the
 // reference's pencil (paro.cpp:143-150); then dense_sym_geneig(At, Bt);

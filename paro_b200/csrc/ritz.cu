@@ -84,12 +84,20 @@ __global__ void firstidx_kernel(const double* V, long long ld, long long n, cons
   }
 }
 
-__global__ void negate_kernel(double* V, long long ld, long long n, const unsigned long long* amax,
-                              const unsigned long long* first) {
+// decide every column's sign before any block negates (the pivot entry is
+// itself negated by some block, so it cannot be re-read inside negate_kernel)
+__global__ void decide_sign_kernel(const double* V, long long ld, long long n, int k, const unsigned long long* amax,
+                                   unsigned long long* first) {
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    const bool flip = amax[c] != 0ull && first[c] < static_cast<unsigned long long>(n) &&
+                      V[c * ld + static_cast<long long>(first[c])] < 0.0;
+    first[c] = flip ? 1ull : 0ull;
+  }
+}
+
+__global__ void negate_kernel(double* V, long long ld, long long n, const unsigned long long* flip) {
   const int c = blockIdx.y;
-  if (amax[c] == 0ull || first[c] >= static_cast<unsigned long long>(n)) return;
-  if (!(V[c * ld + static_cast<long long>(first[c])] < 0.0)) return;
-  __syncthreads();
+  if (flip[c] == 0ull) return;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
     V[c * ld + i] = -V[c * ld + i];
@@ -126,8 +134,9 @@ void fix_sign_columns(Ctx& ctx, double* V, long long ld, int k) {
   const int bx = static_cast<int>(std::min<long long>(148 * 4, (n + 255) / 256));
   colmax_kernel<<<dim3(bx, k), 256, 0, st>>>(V, ld, n, amax);
   firstidx_kernel<<<dim3(bx, k), 256, 0, st>>>(V, ld, n, amax, first);
-  negate_kernel<<<dim3(bx, k), 256, 0, st>>>(V, ld, n, amax, first);
-  ctx.launches += 4;
+  decide_sign_kernel<<<1, 256, 0, st>>>(V, ld, n, k, amax, first);
+  negate_kernel<<<dim3(bx, k), 256, 0, st>>>(V, ld, n, first);
+  ctx.launches += 5;
   PARO_CUDA(cudaGetLastError());
 }
 
@@ -191,6 +200,61 @@ double read_double(Ctx& ctx, const double* d) {
 
 }  // namespace
 
+namespace {
+
+__global__ void div_kernel(double* dst, const double* src, double d, long long n) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    dst[i] = src[i] / d;  // x /= nb (linalg.cpp:431)
+}
+
+double ddot(Ctx& ctx, const double* x, const double* y) {
+  double r = 0.0;
+  cublas_check(cublasDdot(ctx.cublas, static_cast<int>(ctx.grid.n), x, 1, y, 1, &r), "ddot");
+  ++ctx.launches;
+  return r;
+}
+
+// b_orthonormalize (linalg.cpp:409-439) as two-pass classical Gram-Schmidt in
+// the B inner product, candidate by candidate with the same drop rule:
+// Q (k columns) B-orthonormal, BQ = B Q. Used when the candidates are too
+// ill-conditioned for the Cholesky-QR path (e.g. right after a noise start).
+int cgs2_orthonormalize(Ctx& ctx, const Op& B, int K, const double* U, double drop_tol, double* Q, double* BQ,
+                        int* kout) {
+  const long long n = ctx.grid.n;
+  cudaStream_t st = ctx.stream;
+  double* h = ctx.ws_e.get<double>(2 * static_cast<size_t>(n) + K);
+  double* Bh = h + n;
+  double* c = Bh + n;
+  const double one = 1.0, zero = 0.0, mone = -1.0;
+  const int blocks = static_cast<int>(std::min<long long>(148 * 8, (n + 255) / 256));
+  int k = 0;
+  for (int j = 0; j < K; ++j) {
+    PARO_CUDA(cudaMemcpyAsync(h, U + j * n, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    apply_op(ctx, B, nullptr, 0.0, 1, h, n, Bh, n);
+    const double orig = std::sqrt(std::max(0.0, ddot(ctx, h, Bh)));
+    if (!(orig > 0.0)) continue;
+    for (int pass = 0; pass < 2 && k > 0; ++pass) {
+      cublas_check(cublasDgemv(ctx.cublas, CUBLAS_OP_T, static_cast<int>(n), k, &one, BQ, static_cast<int>(n), h, 1,
+                               &zero, c, 1), "cgs proj");
+      cublas_check(cublasDgemv(ctx.cublas, CUBLAS_OP_N, static_cast<int>(n), k, &mone, Q, static_cast<int>(n), c, 1,
+                               &one, h, 1), "cgs update");
+      ctx.launches += 2;
+    }
+    apply_op(ctx, B, nullptr, 0.0, 1, h, n, Bh, n);
+    const double nb = std::sqrt(std::max(0.0, ddot(ctx, h, Bh)));
+    if (nb <= drop_tol * orig) continue;
+    div_kernel<<<blocks, 256, 0, st>>>(Q + k * n, h, nb, n);
+    ++ctx.launches;
+    apply_op(ctx, B, nullptr, 0.0, 1, Q + k * n, n, BQ + k * n, n);
+    ++k;
+  }
+  *kout = k;
+  return kOk;
+}
+
+}  // namespace
+
 int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, long long ld, size_t min_keep,
                   double drop_tol, double* lambdas, double* V, long long ldv, int* k_out, double* defect,
                   RitzInfo* info) {
@@ -198,69 +262,116 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
   if (B.var) throw ParoError(kInvalidArgument, "rayleigh_ritz: B must be the constant mass stencil");
   if (K <= 0) throw ParoError(kEmptyBasis, "b_orthonormalize: all vectors dropped");
   const long long n = ctx.grid.n;
+  if (ld != n || ldv != n) throw ParoError(kInvalidArgument, "rayleigh_ritz: vectors must be contiguous (ld == n)");
   cudaStream_t st = ctx.stream;
   cublasSetStream(ctx.cublas, st);
   double* W = ctx.ws_b.get<double>(static_cast<size_t>(K) * n);
   double* Q1 = ctx.ws_c.get<double>(static_cast<size_t>(K) * n);
   Small s = small_buffers(ctx, K);
+  int k = 0;
+  bool use_cgs = ctx.force_cgs2;
 
-  // pass 1: Gram of the candidates, ordered Cholesky with drops
-  if (ld != n || ldv != n) throw ParoError(kInvalidArgument, "rayleigh_ritz: vectors must be contiguous (ld == n)");
-  apply_op(ctx, B, nullptr, 0.0, K, U, ld, W, n);
-  gram(ctx, K, K, U, ld, W, n, s.G);
-  ortho_from_gram_kernel<<<1, 32, 0, st>>>(K, s.G, drop_tol, 1, s.C1, s.acc, s.kout, s.rmin, s.w, s.status);
-  ++ctx.launches;
-  PARO_CUDA(cudaGetLastError());
-  const int k = read_int(ctx, s.kout);
-  const double rmin = read_double(ctx, s.rmin);
-  if (info) {
-    info->min_ratio = rmin;
-    info->k = k;
-  }
-  if (k == 0) {
-    ctx.err = "b_orthonormalize: all vectors dropped";
-    return kEmptyBasis;
-  }
-  if (static_cast<size_t>(k) < min_keep) {
-    ctx.err = "rayleigh_ritz: candidate span collapsed to " + std::to_string(k) + " < " + std::to_string(min_keep);
-    return kDegenerateSpan;
-  }
-  rotate(ctx, K, k, U, ld, s.C1, K, Q1, n);
+  auto check_count = [&](int kk) -> int {
+    if (kk == 0) {
+      ctx.err = "b_orthonormalize: all vectors dropped";
+      return kEmptyBasis;
+    }
+    if (static_cast<size_t>(kk) < min_keep) {
+      ctx.err = "rayleigh_ritz: candidate span collapsed to " + std::to_string(kk) + " < " + std::to_string(min_keep);
+      return kDegenerateSpan;
+    }
+    return kOk;
+  };
+  auto finish = [&](const double* Qb, int kk) -> double {
+    // lift, sign convention, certificate (paro.cpp:157-174)
+    rotate(ctx, kk, kk, Qb, n, s.Y, kk, V, ldv);
+    fix_sign_columns(ctx, V, ldv, kk);
+    apply_op(ctx, B, nullptr, 0.0, kk, V, ldv, W, n);
+    gram(ctx, kk, kk, V, ldv, W, n, s.G3);
+    defect_kernel<<<1, 256, 0, st>>>(kk, s.G3, s.defect);
+    ++ctx.launches;
+    return read_double(ctx, s.defect);
+  };
 
-  // pass 2
-  apply_op(ctx, B, nullptr, 0.0, k, Q1, n, W, n);
-  gram(ctx, k, k, Q1, n, W, n, s.G2);
-  second_pass_kernel<<<1, 32, 0, st>>>(k, s.G2, s.C2, s.Bt, s.w, s.status);
-  ++ctx.launches;
-  if (read_int(ctx, s.status) != kOk) {
-    ctx.err = "rayleigh_ritz: second orthonormalisation pass lost positive definiteness";
-    return kPencil;
+  double d = 0.0;
+  if (!use_cgs) {
+    // CholQR pass 1: Gram of the candidates, ordered Cholesky with drops
+    apply_op(ctx, B, nullptr, 0.0, K, U, ld, W, n);
+    gram(ctx, K, K, U, ld, W, n, s.G);
+    ortho_from_gram_kernel<<<1, 32, 0, st>>>(K, s.G, drop_tol, 1, s.C1, s.acc, s.kout, s.rmin, s.w, s.status);
+    ++ctx.launches;
+    PARO_CUDA(cudaGetLastError());
+    k = read_int(ctx, s.kout);
+    const double rmin = read_double(ctx, s.rmin);
+    if (info) info->min_ratio = rmin;
+    // Cholesky pivots lose ~eps/ratio^2 relative accuracy: near-dependent
+    // candidates (and every drop decision) go through the CGS2 path instead
+    if (rmin < 1e-5) use_cgs = true;
   }
-
-  // projected pencil
-  apply_op(ctx, A, nullptr, 0.0, k, Q1, n, W, n);
-  gram(ctx, k, k, Q1, n, W, n, s.GA);
-  pencil_kernel<<<1, 32, 0, st>>>(k, s.GA, s.C2, s.Bt, s.vals, s.Y, s.At, s.X, s.w, s.status);
-  ++ctx.launches;
-  if (read_int(ctx, s.status) != kOk) {
-    ctx.err = "pencil: B is not positive definite";
-    return kPencil;
+  if (!use_cgs) {
+    const int cs = check_count(k);
+    if (cs != kOk) return cs;
+    rotate(ctx, K, k, U, ld, s.C1, K, Q1, n);
+    // pass 2
+    apply_op(ctx, B, nullptr, 0.0, k, Q1, n, W, n);
+    gram(ctx, k, k, Q1, n, W, n, s.G2);
+    second_pass_kernel<<<1, 32, 0, st>>>(k, s.G2, s.C2, s.Bt, s.w, s.status);
+    ++ctx.launches;
+    if (read_int(ctx, s.status) != kOk) {
+      use_cgs = true;
+    } else {
+      apply_op(ctx, A, nullptr, 0.0, k, Q1, n, W, n);
+      gram(ctx, k, k, Q1, n, W, n, s.GA);
+      pencil_kernel<<<1, 32, 0, st>>>(k, s.GA, s.C2, s.Bt, s.vals, s.Y, s.At, s.X, s.w, s.status);
+      ++ctx.launches;
+      if (read_int(ctx, s.status) != kOk) {
+        ctx.err = "pencil: B is not positive definite";
+        return kPencil;
+      }
+      d = finish(Q1, k);
+      if (d > 1e-8) use_cgs = true;  // retry with explicit Gram-Schmidt before failing the certificate
+    }
   }
-
-  // lift, sign convention, certificate
-  rotate(ctx, k, k, Q1, n, s.Y, k, V, ldv);
-  fix_sign_columns(ctx, V, ldv, k);
-  apply_op(ctx, B, nullptr, 0.0, k, V, ldv, W, n);
-  gram(ctx, k, k, V, ldv, W, n, s.G3);
-  defect_kernel<<<1, 256, 0, st>>>(k, s.G3, s.defect);
-  ++ctx.launches;
+  if (use_cgs) {
+    if (info) info->cgs2 = true;
+    double* BQ = W;
+    cgs2_orthonormalize(ctx, B, K, U, drop_tol, Q1, BQ, &k);
+    const int cs = check_count(k);
+    if (cs != kOk) return cs;
+    double* AQ = ctx.ws_d.get<double>(static_cast<size_t>(k) * n);
+    apply_op(ctx, A, nullptr, 0.0, k, Q1, n, AQ, n);
+    gram(ctx, k, k, Q1, n, AQ, n, s.GA);
+    gram(ctx, k, k, Q1, n, BQ, n, s.G2);
+    pencil_direct_kernel<<<1, 32, 0, st>>>(k, s.GA, s.G2, s.vals, s.Y, s.At, s.Bt, s.X, s.w, s.status);
+    ++ctx.launches;
+    if (read_int(ctx, s.status) != kOk) {
+      ctx.err = "pencil: B is not positive definite";
+      return kPencil;
+    }
+    d = finish(Q1, k);
+  }
+  if (info) info->k = k;
   PARO_CUDA(cudaMemcpyAsync(lambdas, s.vals, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
-  const double d = read_double(ctx, s.defect);
+  PARO_CUDA(cudaStreamSynchronize(st));
   *k_out = k;
   *defect = d;
   if (d > 1e-8) {
     ctx.err = "rayleigh_ritz: orthonormality certificate violated (defect " + std::to_string(d) + ")";
     return kError;
+  }
+  return kOk;
+}
+
+int b_orthonormalize(Ctx& ctx, const Op& B, int K, const double* U, double drop_tol, double* Q, int* k_out) {
+  ctx.check_grid();
+  const long long n = ctx.grid.n;
+  cublasSetStream(ctx.cublas, ctx.stream);
+  double* BQ = ctx.ws_b.get<double>(static_cast<size_t>(K) * n);
+  cgs2_orthonormalize(ctx, B, K, U, drop_tol, Q, BQ, k_out);
+  PARO_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (*k_out == 0 && K > 0) {
+    ctx.err = "b_orthonormalize: all vectors dropped";
+    return kEmptyBasis;
   }
   return kOk;
 }

@@ -8,6 +8,7 @@ namespace paro_b200 {
 struct RitzInfo {
   double min_ratio = 0.0;  // smallest projected/original B-norm ratio of the candidates
   int k = 0;
+  bool cgs2 = false;       // the explicit Gram-Schmidt path was used
 };
 
 int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, long long ld, size_t min_keep,
@@ -16,6 +17,8 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
 
 int dense_sym_geneig(Ctx& ctx, int m, const double* A_host, const double* B_host, double* vals_host,
                      double* vecs_host);
+
+int b_orthonormalize(Ctx& ctx, const Op& B, int K, const double* U, double drop_tol, double* Q, int* k_out);
 
 void fix_sign_columns(Ctx& ctx, double* V, long long ld, int k);
 

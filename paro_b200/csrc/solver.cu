@@ -359,6 +359,7 @@ int source_solve(Ctx& ctx, const Op& a, const Op& b, double sigma, int K, const 
     report->iterations.assign(K, 0);
     report->residual.assign(K, 0.0);
     report->status.assign(K, kOk);
+    report->first_status = first_status;
     for (int c = 0; c < K; ++c) {
       const CgColumn& f = first_status[c] == kIterationLimit ? retry[c] : cols[c];
       report->iterations[c] = f.it;

@@ -11,7 +11,8 @@ namespace paro_b200 {
 struct SolveReport {
   std::vector<unsigned long long> iterations;
   std::vector<double> residual;
-  std::vector<int> status;
+  std::vector<int> status;        // final per-column status (after the retry, if any)
+  std::vector<int> first_status;  // status of the first attempt
 };
 
 OpDev make_opdev(const Ctx& ctx, const Op& a, const Op* shift, double sigma);

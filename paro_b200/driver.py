@@ -1,0 +1,304 @@
+"""Fixed-mesh ParO outer iteration, orbitals sharded over ranks.
+
+Mirrors the loop bodies of the reference drivers with the adaptive branch off
+(SURVEY.md §8c "Oracle harness contract"):
+  Kohn-Sham  proj/src/paro.cpp:514-638   (Step 2 estimator omitted on both sides)
+  linear     proj/src/paro.cpp:340-354
+Multi-GPU: rank r owns a contiguous block of orbital columns
+and solves its Step-3 source problems with no communication; the half-step
+orbitals are all-gathered once per iteration and every rank then runs the
+(small, deterministic) Step 4 and potential rebuild on identical inputs, so
+all ranks hold bitwise-identical orbitals, densities and energies and the
+results do not depend on the GPU count. The compute is delegated to a
+backend (GpuBackend = the native sm_100a library); the orchestration is
+backend-agnostic so the N > 1 path is testable with gloo on CPU.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import torch
+
+from . import _native as N
+from .configs import Workload, guess_vectors
+
+OK, NOT_SPD, ITER_LIMIT = 0, 3, 4
+
+
+def step3_outcome(first, final):
+    """Exception order of source_solve_step (paro.cpp:95-117, serial worker):
+    a failure inside the per-orbital retry escapes at once; otherwise the first
+    failed first attempt (by orbital index) is rethrown."""
+    for c, (f, g) in enumerate(zip(first, final)):
+        if f == ITER_LIMIT and g != OK:
+            return g, c
+    for c, f in enumerate(first):
+        if f not in (OK, ITER_LIMIT):
+            return f, c
+    return OK, -1
+
+
+class Dist:
+    """torch.distributed plumbing (NCCL on GPUs, gloo on CPU); world 1 = no-op."""
+
+    def __init__(self, group=None):
+        import torch.distributed as td
+
+        self.td = td if td.is_available() and td.is_initialized() else None
+        self.group = group
+        self.world = self.td.get_world_size(group) if self.td else 1
+        self.rank = self.td.get_rank(group) if self.td else 0
+
+    def shard(self, K: int):
+        base, rem = divmod(K, self.world)
+        counts = [base + (1 if r < rem else 0) for r in range(self.world)]
+        c0 = sum(counts[: self.rank])
+        return c0, c0 + counts[self.rank], counts
+
+    def allgather_columns(self, local: torch.Tensor, counts, out: torch.Tensor):
+        """[k_r, n] blocks -> out[:K] in rank order (padded to max(counts))."""
+        if self.world == 1:
+            if local.data_ptr() != out.data_ptr():
+                out[: local.shape[0]].copy_(local)
+            return out
+        kmax = max(counts)
+        n = local.shape[1]
+        send = local.new_zeros((kmax, n)) if local.shape[0] < kmax else local
+        if local.shape[0] < kmax:
+            send[: local.shape[0]].copy_(local)
+        recv = local.new_empty((self.world * kmax, n))
+        self.td.all_gather_into_tensor(recv, send.contiguous(), group=self.group)
+        row = 0
+        for r, cnt in enumerate(counts):
+            out[row: row + cnt].copy_(recv[r * kmax: r * kmax + cnt])
+            row += cnt
+        return out
+
+    def allgather_ints(self, values, counts, device):
+        if self.world == 1:
+            return list(values)
+        kmax = max(counts)
+        t = torch.full((kmax,), -1, dtype=torch.int64, device=device)
+        if len(values):
+            t[: len(values)] = torch.tensor(values, dtype=torch.int64, device=device)
+        out = torch.empty(self.world * kmax, dtype=torch.int64, device=device)
+        self.td.all_gather_into_tensor(out, t, group=self.group)
+        out = out.cpu().tolist()
+        res = []
+        for r, cnt in enumerate(counts):
+            res += out[r * kmax: r * kmax + cnt]
+        return res
+
+
+class GpuBackend:
+    """The product backend: every call lands in the native sm_100a library."""
+
+    def __init__(self, workload: Workload, device: int = 0):
+        from . import core
+
+        self.core = core
+        self.w = workload
+        self.ctx = core.Context(device).grid(workload.subdivisions, workload.lo, workload.hi)
+        self.n = self.ctx.n
+        self.device = self.ctx.device
+        c = core
+        self.mass = c.assemble_mass(self.ctx)
+        if workload.kind == "ks":
+            self.kinetic = c.assemble_stiffness(self.ctx, 0.5)
+            self.poisson = c.assemble_stiffness(self.ctx, 1.0)
+            self.vext = c.assemble_vext(self.ctx, workload.charges, workload.positions, workload.eps)
+            self.forms = {"in": c.Operator.variable_empty(self.ctx), "half": c.Operator.variable_empty(self.ctx)}
+            self.scratch = self.ctx.empty(self.n)
+        else:
+            a = c.assemble_stiffness(self.ctx, 0.5)
+            if workload.potential == "harmonic":
+                c.add_scaled(a, c.assemble_harmonic(self.ctx, 0.5))
+            else:
+                c.add_scaled(a, c.assemble_vext(self.ctx, workload.charges, workload.positions, workload.eps))
+            self.form = a
+
+    # tensors
+    def empty(self, *shape):
+        return self.ctx.empty(*shape)
+
+    def from_host(self, a):
+        return torch.as_tensor(a, device=self.device).contiguous()
+
+    def sync(self):
+        torch.cuda.synchronize(self.device)
+
+    # operators
+    def core_hamiltonian(self):
+        a0 = self.core.assemble_stiffness(self.ctx, 0.5)
+        return self.core.add_scaled(a0, self.vext)
+
+    def ks_form(self, rho, vh, slot):
+        op, clamped = self.core.ks_form_matrix(self.kinetic, self.vext, rho, vh, out=self.forms[slot])
+        return op, clamped
+
+    # steps
+    def hartree(self, rho, out=None):
+        return self.core.hartree_solve_with(self.poisson, self.mass, rho, 1e-11, out=out)
+
+    def source_solve(self, a, u, lambdas, sigma, tol, max_iter, out):
+        return self.core.source_solve_columns(a, self.mass, u, lambdas, tol, max_iter, sigma, out)
+
+    def ritz(self, cands, a, min_keep, drop_tol, out):
+        r = self.core.rayleigh_ritz(cands, a, self.mass, min_keep, drop_tol, out=out)
+        return r.orbitals, list(r.lambdas), r.gram_defect
+
+    def density(self, U, occ, out=None):
+        return self.core.density_from_orbitals(self.ctx, U, occ, out=out)[0]
+
+    def energy(self, lambdas, occ, rho, vh):
+        return self.core.total_energy(self.ctx, lambdas, occ, rho, vh, self.w.charges, self.w.positions)
+
+    def mix(self, rin, rout, alpha, out):
+        return self.core.mix_density(self.ctx, rin, rout, alpha, out=out)
+
+    def rho_residual(self, rout, rin):
+        return self.core.rho_residual(self.ctx, rout, rin, self.scratch)
+
+    def launches(self) -> int:
+        return self.ctx.launches()
+
+
+@dataclass
+class Trace:
+    iter: int
+    lambdas: list
+    e_tot: float | None
+    rho_residual: float | None
+    sigma: float
+    gram_defect: float
+    cg_iterations: list
+    t_source: float
+    t_project: float
+    t_total: float
+
+
+class ParoRun:
+    """One fixed-mesh ParO run (KS or linear) on a backend, sharded by `dist`."""
+
+    def __init__(self, w: Workload, backend, dist: Dist | None = None, guess=None, timers: bool = True):
+        self.w = w
+        self.be = backend
+        self.dist = dist or Dist()
+        self.timers = timers
+        K = w.K
+        n = backend.n
+        self.half = backend.empty(K, n)
+        self.orb = backend.empty(K, n)
+        self._half_local = None
+        g = guess if guess is not None else guess_vectors(w)
+        cands = backend.from_host(g) if not torch.is_tensor(g) else g
+        if w.kind == "ks":
+            self.occ = [2.0] * (w.n_electrons // 2)
+            if len(self.occ) != w.n_orbitals:
+                raise N.InvalidArgumentError("kohn-sham: config.n_orbitals must equal N_e / 2")
+            a0 = backend.core_hamiltonian()
+            # initial guess: V_H = V_xc = 0 linearisation (paro.cpp:499-505)
+            orb, lam, _ = backend.ritz(cands, a0, K, w.drop_tol, self.orb)
+            self.rho_in = backend.density(orb, self.occ, out=backend.empty(n))
+            self.rho_half = backend.empty(n)
+            self.rho_out = backend.empty(n)
+            self.vh = backend.empty(n)
+        else:
+            orb, lam, _ = backend.ritz(cands, backend.form, K, w.drop_tol, self.orb)
+        self.k = orb.shape[0]
+        self.lambdas = lam
+        self.clamped = 0
+
+    def _sync(self):
+        if self.timers:
+            self.be.sync()
+
+    def step3(self, a, it: int):
+        """shifted_source_step (paro.cpp:194-210) over the sharded columns + allgather."""
+        w, be, d = self.w, self.be, self.dist
+        K = self.k
+        c0, c1, counts = d.shard(K)
+        tol = w.cg_tol_for_iteration(it)
+        sigma = max(0.0, 0.5 - self.lambdas[0])
+        local = self.half[c0:c1] if d.world == 1 else self._local(c1 - c0)
+        for attempt in range(5):
+            first, final, iters, _ = be.source_solve(a, self.orb[c0:c1], self.lambdas[c0:c1], sigma, tol,
+                                                     w.cg_max_iter, local)
+            first = d.allgather_ints(first, counts, self._idev())
+            final = d.allgather_ints(final, counts, self._idev())
+            code, col = step3_outcome(first, final)
+            if code == NOT_SPD and attempt < 4:
+                sigma = 2.0 * sigma + 1.0
+                continue
+            if code != OK:
+                raise N.ERRORS.get(code, N.Error)(f"source_solve_step: orbital {col} failed")
+            break
+        all_iters = d.allgather_ints(iters, counts, self._idev())
+        d.allgather_columns(local, counts, self.half)
+        return sigma, all_iters
+
+    def _local(self, k):
+        if self._half_local is None or self._half_local.shape[0] < k:
+            self._half_local = self.be.empty(max(k, 1), self.be.n)
+        return self._half_local[:k]
+
+    def _idev(self):
+        """Device for the small status all-gathers: the GPU under NCCL, else CPU."""
+        d = self.dist
+        if d.world > 1 and d.td.get_backend(d.group) == "nccl":
+            return self.be.device
+        return torch.device("cpu")
+
+    def step(self, it: int) -> Trace:
+        if self.w.kind == "ks":
+            return self._ks_step(it)
+        return self._linear_step(it)
+
+    def _ks_step(self, it: int) -> Trace:
+        """paro.cpp:514-638 with adaptive = false; no stop tests."""
+        w, be = self.w, self.be
+        N_ = w.n_orbitals
+        t0 = time.perf_counter()
+        vh_in = be.hartree(self.rho_in, out=self.vh)
+        a_in, cl = be.ks_form(self.rho_in, vh_in, "in")
+        self.clamped += cl
+        ts = time.perf_counter()
+        sigma, iters = self.step3(a_in, it)
+        self._sync()
+        t_source = time.perf_counter() - ts
+        tp = time.perf_counter()
+        half = self.half[: self.k]
+        rho_half = be.density(half[:N_], self.occ, out=self.rho_half)
+        vh_half = be.hartree(rho_half, out=self.vh)
+        a_half, cl = be.ks_form(rho_half, vh_half, "half")
+        self.clamped += cl
+        orb, lam, defect = be.ritz(half, a_half, N_, w.drop_tol, self.orb)
+        self._sync()
+        t_project = time.perf_counter() - tp
+        self.k, self.lambdas = orb.shape[0], lam
+        rho_out = be.density(orb[:N_], self.occ, out=self.rho_out)
+        vh_out = be.hartree(rho_out, out=self.vh)
+        e_tot = be.energy(lam, self.occ, rho_out, vh_out)
+        res = be.rho_residual(rho_out, self.rho_in)
+        be.mix(self.rho_in, rho_out, w.mixing_alpha, out=self.rho_in)
+        self._sync()
+        return Trace(it + 1, lam[: w.n_orbitals], e_tot, res, sigma, defect, iters, t_source, t_project,
+                     time.perf_counter() - t0)
+
+    def _linear_step(self, it: int) -> Trace:
+        """paro.cpp:340-354."""
+        w, be = self.w, self.be
+        t0 = time.perf_counter()
+        sigma, iters = self.step3(be.form, it)
+        self._sync()
+        t_source = time.perf_counter() - t0
+        tp = time.perf_counter()
+        orb, lam, defect = be.ritz(self.half[: self.k], be.form, w.n_orbitals, w.drop_tol, self.orb)
+        self._sync()
+        self.k, self.lambdas = orb.shape[0], lam
+        return Trace(it + 1, lam[: w.n_orbitals], None, None, sigma, defect, iters, t_source,
+                     time.perf_counter() - tp, time.perf_counter() - t0)
+
+    def run(self, iterations: int | None = None):
+        return [self.step(i) for i in range(iterations if iterations is not None else self.w.iterations)]

@@ -61,6 +61,29 @@ def test_rayleigh_ritz_matches_reference(ref, gpu_ctx_factory):
         np.testing.assert_allclose(orb[j], orb_ref[j], rtol=0, atol=1e-8 * np.abs(orb_ref[j]).max())
 
 
+def test_rayleigh_ritz_gram_schmidt_path(ref, gpu_ctx_factory):
+    """The explicit two-pass Gram-Schmidt path (used for near-dependent
+    candidates) gives the same Ritz pairs; near-parallel candidates included."""
+    from paro_b200 import _native as N
+    from paro_b200 import core
+
+    sp, ks, a0, mass = _system(ref)
+    ctx = gpu_ctx_factory(sp.s, sp.lo, sp.hi)
+    ga = core.Operator.from_csr(ctx, *a0.csr())
+    gm = core.Operator.from_csr(ctx, *mass.csr())
+    rng = np.random.default_rng(11)
+    base = rng.uniform(-1, 1, (5, sp.n))
+    cands = np.concatenate([base, base[:2] + 1e-7 * rng.uniform(-1, 1, (2, sp.n))])  # ratio ~1e-7
+    lam_ref, orb_ref, _, _ = ref.rayleigh_ritz(sp, cands, a0, mass, 5)
+    for mode in (0, 1):
+        ctx.check(N.lib().paro_ctx_set_ritz_mode(ctx.h, mode))
+        out = core.rayleigh_ritz(_dev(cands), ga, gm, 5)
+        assert len(out.lambdas) == len(lam_ref)
+        np.testing.assert_allclose(out.lambdas[:5], lam_ref[:5], rtol=1e-9)
+        assert out.gram_defect <= 1e-8
+    ctx.check(N.lib().paro_ctx_set_ritz_mode(ctx.h, 0))
+
+
 def test_rayleigh_ritz_known_answers(ref, gpu_ctx_factory):
     """test_paro.cpp:156-218: invariant subspace, K=1 Rayleigh quotient, degenerate span."""
     from paro_b200 import DegenerateSpanError, core
