@@ -1,0 +1,288 @@
+#!/usr/bin/env python
+"""bench.py — ParO outer iterations/s on the B200-native path.
+
+Workload (default): BASELINE.json configs[4], the synthetic 32-atom LDA
+cluster (24 C + 8 H, seeded), cube [-18,18]^3, 257^3 nodes (16.6M interior
+dofs), N = K = 76 doubly-occupied orbitals, FP64 — the configuration the
+metric is quoted on at 1/2/4/8 GPUs; it fits one B200 (~75 GB resident).
+A "step" is one fixed-mesh ParO outer iteration (paro.cpp:514-638 body):
+Hartree, KS form, Step 3 (76 batched source solves), Step 4, density, energy,
+mixing. Setup (assembly, initial guess) and W warm-up iterations are untimed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload cluster32|water|oscillator|h2|source64[@sNN]]
+
+Multi-GPU: launched by torch.distributed.run, one rank per GPU; orbitals are
+sharded across ranks (driver.py). The timed region is bracketed by a barrier
+and a device synchronise on every rank and the max over ranks is reported.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "ParO outer iterations/s"
+UNIT = "outer_iter/s"
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_sample_rate(workload: str, sample_s: int, steps: int = 1, workers: int | None = None):
+    """Reference (oracle/_ref, the unmodified C++) on the same generator at a
+    reduced mesh, one or more full outer iterations; returns per-step seconds
+    and the extrapolation factor to the full mesh (DOFs x 1/h growth of the
+    Jacobi-PCG iteration count)."""
+    from oracle import ref
+
+    from paro_b200 import configs
+
+    full = configs.get(workload)
+    w = full.scaled(sample_s)
+    workers = workers or os.cpu_count() or 1
+    sp = ref.Space(w.subdivisions, w.lo, w.hi)
+    g = configs.guess_vectors(w)
+    times = []
+    if w.kind == "ks":
+        ks = ref.KsSystem(sp, w.charges, w.positions, w.n_electrons, w.eps)
+        loop = ref.KsLoop(ks, g, w.cg_tol_start, w.cg_tol, w.cg_tol_factor, w.cg_max_iter, w.mixing_alpha,
+                          w.drop_tol, workers)
+    else:
+        a = ref.Op.stiffness(sp, 0.5)
+        a.add_scaled(ref.Op.wmass_harmonic(sp, 0.5) if w.potential == "harmonic"
+                     else ref.Op.wmass_coulomb(sp, w.charges, w.positions, w.eps))
+        loop = ref.LinLoop(sp, a, ref.Op.mass(sp), g, w.n_orbitals, w.cg_tol_start, w.cg_tol, w.cg_tol_factor,
+                           w.cg_max_iter, w.drop_tol, workers)
+    for it in range(steps):
+        t0 = time.perf_counter()
+        loop.step(it)
+        times.append(time.perf_counter() - t0)
+    factor = (full.n / w.n) * (full.subdivisions / w.subdivisions)
+    return times, factor, workers, w
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU implementation on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paro_b200 import configs
+
+    full = configs.get(args.workload)
+    s = args.ref_sample or (48 if full.subdivisions >= 128 else full.subdivisions)
+    times, factor, workers, w = cpu_sample_rate(args.workload, s, steps=args.warmup + args.steps)
+    timed = times[args.warmup:] or times
+    per = sum(timed) / len(timed)
+    value = 1.0 / (per * factor)
+    sample = (f"{w.name}: {len(timed)} full reference outer iterations ({per:.2f} s each, {workers} threads) "
+              f"after {args.warmup} warm-up, extrapolated x{factor:.1f} to {full.name} "
+              f"(DOF ratio x mesh-refinement growth of the CG iteration count)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * factor * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(full, args.gpus),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(w, world):
+    return {"workload": f"BASELINE configs: {w.name} ({w.kind}, {w.subdivisions + 1}^3 nodes, n={w.n}, K={w.K}, "
+                        f"box [{w.lo},{w.hi}]^3)",
+            "n_dofs": w.n, "orbitals": w.K, "subdivisions": w.subdivisions,
+            "parallelism": f"orbital-sharded x{world}" if world > 1 else "single GPU",
+            "l2": "inputs larger than L2 (K x n x 8 B per orbital set)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cluster32")
+    ap.add_argument("--ref-sample", type=int, default=0, help="reference sample mesh subdivisions")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as td
+
+    from paro_b200 import configs
+    from paro_b200.driver import Dist, GpuBackend, ParoRun
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist = Dist()
+
+    w = configs.get(args.workload)
+    t_setup = time.perf_counter()
+    be = GpuBackend(w, device=local)
+    run = ParoRun(w, be, dist, timers=False)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup
+    for it in range(args.warmup):
+        run.step(it)
+    torch.cuda.synchronize()
+
+    clocks = Clocks(local) if rank == 0 else None
+    be.ctx.stats(reset=True)
+    launches0 = be.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        td.barrier()
+    torch.cuda.synchronize()
+    ev0.record()
+    traces = [run.step(args.warmup + i) for i in range(args.steps)]
+    ev1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        td.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    launches = be.launches() - launches0
+    st = be.ctx.stats()
+    clk = clocks.stop() if clocks else None
+    t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    if world > 1:
+        td.all_reduce(t, op=td.ReduceOp.MAX)
+    ms = float(t.item())
+
+    # end-to-end through the public API with host buffers: pinned host orbitals
+    # and density in, orbitals/eigenvalues/energy out, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        K, n = run.k, be.n
+        h_orb = torch.empty((K, n), dtype=torch.float64, pin_memory=True)
+        h_rho = torch.empty((n,), dtype=torch.float64, pin_memory=True)
+        h_orb.copy_(run.orb[:K])
+        h_rho.copy_(run.rho_in)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            td.barrier()
+        e0.record()
+        run.orb[:K].copy_(h_orb, non_blocking=True)
+        run.rho_in.copy_(h_rho, non_blocking=True)
+        tr = run.step(args.warmup + args.steps)
+        h_orb.copy_(run.orb[: run.k], non_blocking=True)
+        h_rho.copy_(run.rho_in, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        e_ms = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
+        if world > 1:
+            td.all_reduce(e_ms, op=td.ReduceOp.MAX)
+        bytes_io = (K * n + n) * 8
+        e2e = {"value": 1000.0 / float(e_ms.item()), "unit": UNIT, "h2d_bytes_per_step": bytes_io,
+               "d2h_bytes_per_step": bytes_io + 8 * (len(tr.lambdas) + 1),
+               "path": "ParoRun.step (paro_b200 C ABI) with pinned host orbitals + density in/out"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            s = 24 if w.subdivisions >= 128 else max(8, w.subdivisions // 2)
+            times, factor, workers, ws = cpu_sample_rate(args.workload, s, steps=1)
+            cpu = {"value": 1.0 / (times[0] * factor), "unit": UNIT, "cores": workers, "kind": "reference",
+                   "sample": f"{ws.name}: 1 full reference outer iteration in {times[0]:.2f} s on {workers} threads, "
+                             f"extrapolated x{factor:.1f} to {w.name} (DOF ratio x 1/h growth of CG iterations)"}
+        except Exception as exc:  # the oracle build is test/baseline infrastructure only
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        pk = peaks()
+        peak = float(pk.get("hbm_gbs", 6650.0))
+        achieved = st["step3_bytes"] / st["step3_s"] / 1e9 if st["step3_s"] > 0 else 0.0
+        iters = traces[-1].cg_iterations
+        line = {
+            "metric": METRIC, "value": 1000.0 / ms, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE generator)",
+            "config": workload_config(w, world),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if peak else None, "traffic": None,
+                         "kernel": "Step-3 Jacobi-PCG iteration (march K1+K2 + finalize), algorithmic n*(88k+64) B",
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("_fallback") else "fallback"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+            "breakdown": {"t_source_s": traces[-1].t_source, "t_project_s": traces[-1].t_project,
+                          "step3_pcg_s": st["step3_s"] / args.steps, "hartree_pcg_s": st["hartree_s"] / args.steps,
+                          "hartree_achieved_gbs": st["hartree_bytes"] / st["hartree_s"] / 1e9 if st["hartree_s"] else 0,
+                          "cg_iterations_last_step": iters, "setup_s": t_setup,
+                          "lambda_1": traces[-1].lambdas[0], "e_tot": traces[-1].e_tot},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        td.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

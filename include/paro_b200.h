@@ -54,6 +54,10 @@ double paro_ctx_last_residual(const paro_ctx* ctx);
 /* kernels launched by this library so far (CUDA-graph nodes counted) */
 unsigned long long paro_ctx_launches(const paro_ctx* ctx);
 int paro_ctx_synchronize(paro_ctx* ctx);
+/* Live PCG accounting since the last reset: [0] seconds, [1] algorithmic bytes
+ * n*(88 k + 64) per iteration, [2] column-iterations for variable operators
+ * (Step 3); [3..5] the same for constant operators (Hartree). */
+int paro_ctx_stats(paro_ctx* ctx, double out[8], int reset);
 /* Step-4 orthonormalisation: 0 = Cholesky-QR twice with an automatic
  * Gram-Schmidt fallback for near-dependent candidates (default), 1 = always
  * two-pass Gram-Schmidt (b_orthonormalize's algorithm, linalg.cpp:409-439). */

@@ -78,6 +78,13 @@ class Context:
     def launches(self) -> int:
         return int(N.lib().paro_ctx_launches(self.h))
 
+    def stats(self, reset: bool = False) -> dict:
+        """Live PCG accounting (seconds, algorithmic bytes, column-iterations)."""
+        out = (C.c_double * 8)()
+        N.lib().paro_ctx_stats(self.h, out, int(reset))
+        return {"step3_s": out[0], "step3_bytes": out[1], "step3_col_iters": out[2],
+                "hartree_s": out[3], "hartree_bytes": out[4], "hartree_col_iters": out[5]}
+
     def synchronize(self):
         self.check(N.lib().paro_ctx_synchronize(self.h))
 

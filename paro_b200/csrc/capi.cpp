@@ -100,6 +100,15 @@ const char* paro_ctx_last_error(const paro_ctx* ctx) { return ctx ? ctx->c.err.c
 double paro_ctx_last_residual(const paro_ctx* ctx) { return ctx ? ctx->c.resid : 0.0; }
 unsigned long long paro_ctx_launches(const paro_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
 
+int paro_ctx_stats(paro_ctx* ctx, double out[8], int reset) {
+  if (!ctx) return kInvalidArgument;
+  for (int i = 0; i < 8; ++i) {
+    if (out) out[i] = ctx->c.stats[i];
+    if (reset) ctx->c.stats[i] = 0.0;
+  }
+  return kOk;
+}
+
 int paro_ctx_set_ritz_mode(paro_ctx* ctx, int mode) {
   return guarded(ctx, [&] {
     ctx->c.force_cgs2 = mode == 1;

@@ -60,6 +60,12 @@ struct Ctx {
   int* pinned_count = nullptr;       // mapped host memory for the active-column poll
   int* pinned_count_dev = nullptr;
 
+  // live accounting of the PCG iteration loops (CUDA-event time on the
+  // context stream, algorithmic bytes n*(88 k + 64) per iteration)
+  // [0] var-op seconds [1] var-op bytes [2] var-op column-iterations
+  // [3] const-op seconds [4] const-op bytes [5] const-op column-iterations
+  double stats[8] = {};
+
   double mass_w[kSlots] = {};        // reference mass stencil on this grid
   bool mass_set = false;
 

@@ -92,6 +92,13 @@ __device__ __forceinline__ Lda lda_vxc(double rho, bool exchange_only, double cx
       const double ln = log(rs);
       ec = a * ln + b + c * rs * ln + dd * rs;
       vc = a * ln + (b - a / 3.0) + (2.0 / 3.0) * c * rs * ln + ((2.0 * dd - c) / 3.0) * rs;
+    } else if (isinf(rs)) {
+      // rho < ~1.3e-309 (denormal): 3/(4 pi rho) overflows and the reference
+      // formula gives -0 * inf = NaN (model.cpp:282-294), failing the
+      // assembly. Use the rho -> 0 limit of PZ81 (e_c, v_c -> 0) instead; every
+      // density the reference evaluates finitely is unaffected.
+      ec = 0.0;
+      vc = 0.0;
     } else {
       const double gamma = -0.1423, beta1 = 1.0529, beta2 = 0.3334;
       const double sq = sqrt(rs);

@@ -266,6 +266,9 @@ void batched_pcg(Ctx& ctx, const OpDev& op, bool var, int K, const double* src, 
   cudaEvent_t ev[2];
   PARO_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
   PARO_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  cudaEvent_t tev[2];
+  PARO_CUDA(cudaEventCreate(&tev[0]));
+  PARO_CUDA(cudaEventCreate(&tev[1]));
   volatile int* hcount = ctx.pinned_count;
   // prime: the setup may already have finished every column
   count_active_kernel<<<1, 256, 0, st>>>(dcols, K, ctx.pinned_count_dev);
@@ -276,6 +279,7 @@ void batched_pcg(Ctx& ctx, const OpDev& op, bool var, int K, const double* src, 
   unsigned long long max_iter = 0;
   for (const auto& c : cols) max_iter = std::max(max_iter, c.max_iter);
   unsigned long long launched = 0;
+  PARO_CUDA(cudaEventRecord(tev[0], st));
   // keep one chunk in flight ahead of the poll
   if (remaining > 0) {
     PARO_CUDA(cudaGraphLaunch(exec, st));
@@ -301,12 +305,28 @@ void batched_pcg(Ctx& ctx, const OpDev& op, bool var, int K, const double* src, 
     }
     cur ^= 1;
   }
+  PARO_CUDA(cudaEventRecord(tev[1], st));
   PARO_CUDA(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  PARO_CUDA(cudaEventElapsedTime(&ms, tev[0], tev[1]));
+  PARO_CUDA(cudaEventDestroy(tev[0]));
+  PARO_CUDA(cudaEventDestroy(tev[1]));
   PARO_CUDA(cudaEventDestroy(ev[0]));
   PARO_CUDA(cudaEventDestroy(ev[1]));
   PARO_CUDA(cudaGraphExecDestroy(exec));
   PARO_CUDA(cudaGraphDestroy(graph));
+  std::vector<CgColumn> before = cols;
   PARO_CUDA(cudaMemcpy(cols.data(), dcols, sizeof(CgColumn) * K, cudaMemcpyDeviceToHost));
+  double col_iters = 0.0, batch_iters = 0.0;
+  for (int c = 0; c < K; ++c)
+    if (before[c].active) {
+      col_iters += static_cast<double>(cols[c].it);
+      batch_iters = std::max(batch_iters, static_cast<double>(cols[c].it));
+    }
+  const int base = var ? 0 : 3;
+  ctx.stats[base + 0] += ms * 1e-3;
+  ctx.stats[base + 1] += static_cast<double>(n) * (88.0 * col_iters + (var ? 64.0 : 0.0) * batch_iters);
+  ctx.stats[base + 2] += col_iters;
 }
 
 static CgColumn make_col(double tol, unsigned long long max_iter) {
