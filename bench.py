@@ -199,9 +199,11 @@ def main():
     if world > 1:
         td.barrier()
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" selects the timed region
     ev0.record()
     traces = [run.step(args.warmup + i) for i in range(args.steps)]
     ev1.record()
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     if world > 1:
         td.barrier()

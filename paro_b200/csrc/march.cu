@@ -46,6 +46,23 @@ __device__ __forceinline__ double row_sum(const double* __restrict__ Pm, const d
   return s;
 }
 
+// own[o] = A[v, v+o] stored at v; back[o] = A[v, v-o] stored at v-o (0 when
+// v-o leaves the lattice, where the plane value is 0 anyway)
+__device__ __forceinline__ void load_weights(const double* __restrict__ cf, long long n, long long idx, int gx, int gy,
+                                             int z, int S, long long S2, double (&own)[kSlots],
+                                             double (&back)[kSlots]) {
+#pragma unroll
+  for (int o = 0; o < kSlots; ++o) own[o] = __ldg(cf + o * n + idx);
+  back[0] = 0.0;
+#pragma unroll
+  for (int o = 1; o < kSlots; ++o) {
+    const int ox = o & 1, oy = (o >> 1) & 1, oz = (o >> 2) & 1;
+    const bool ok = gx >= ox && gy >= oy && z >= oz;
+    const long long nb = idx - ox - static_cast<long long>(oy) * S - static_cast<long long>(oz) * S2;
+    back[o] = ok ? __ldg(cf + o * n + nb) : 0.0;
+  }
+}
+
 template <int MODE, bool VAR, int CB>
 __global__ void __launch_bounds__(kNT, 2) march_kernel(const MarchArgs a) {
   extern __shared__ double smem[];  // [3][CB][kHP]
@@ -187,20 +204,25 @@ __global__ void __launch_bounds__(kNT, 2) march_kernel(const MarchArgs a) {
       // 15 weights of the operator at this point, shifted by sigma*M
       double wb[kSlots], wf[kSlots], w0;
       if (VAR) {
-        const double* cf = a.op.coef;
-        double own[kSlots];
+        double own[kSlots], back[kSlots];
+        load_weights(a.op.coef, n, idx, gx, gy, z, S, S2, own, back);
+        if (a.op.mcoef != nullptr) {  // variable shift stencil (inexact mesh spacing)
+          double mown[kSlots], mback[kSlots];
+          load_weights(a.op.mcoef, n, idx, gx, gy, z, S, S2, mown, mback);
 #pragma unroll
-        for (int o = 0; o < kSlots; ++o) own[o] = __ldg(cf + o * n + idx);
+          for (int o = 1; o < kSlots; ++o) {
+            wb[o] = __dadd_rn(back[o], __dmul_rn(a.op.sigma, mback[o]));
+            wf[o] = __dadd_rn(own[o], __dmul_rn(a.op.sigma, mown[o]));
+          }
+          w0 = __dadd_rn(own[0], __dmul_rn(a.op.sigma, mown[0]));
+        } else {
 #pragma unroll
-        for (int o = 1; o < kSlots; ++o) {
-          const int ox = o & 1, oy = (o >> 1) & 1, oz = (o >> 2) & 1;
-          const bool ok = gx >= ox && gy >= oy && z >= oz;
-          const long long nb = idx - ox - static_cast<long long>(oy) * S - static_cast<long long>(oz) * S2;
-          const double cb = ok ? __ldg(cf + o * n + nb) : 0.0;
-          wb[o] = __dadd_rn(cb, __dmul_rn(a.op.sigma, a.op.m[o]));
-          wf[o] = __dadd_rn(own[o], __dmul_rn(a.op.sigma, a.op.m[o]));
+          for (int o = 1; o < kSlots; ++o) {
+            wb[o] = __dadd_rn(back[o], __dmul_rn(a.op.sigma, a.op.m[o]));
+            wf[o] = __dadd_rn(own[o], __dmul_rn(a.op.sigma, a.op.m[o]));
+          }
+          w0 = __dadd_rn(own[0], __dmul_rn(a.op.sigma, a.op.m[0]));
         }
-        w0 = __dadd_rn(own[0], __dmul_rn(a.op.sigma, a.op.m[0]));
       } else {
 #pragma unroll
         for (int o = 1; o < kSlots; ++o) {
@@ -241,6 +263,11 @@ __global__ void __launch_bounds__(kNT, 2) march_kernel(const MarchArgs a) {
           double bb;
           if (a.rhs != nullptr) {
             bb = a.rhs[gi];  // cg_solve(a, b, x0) with an explicit b
+          } else if (a.mwcoef != nullptr) {
+            double mown[kSlots], mback[kSlots];
+            load_weights(a.mwcoef, n, idx, gx, gy, z, S, S2, mown, mback);
+            const double msum = row_sum(Pm, P0, Pp, ib, mback, mown[0], mown);
+            bb = __dmul_rn(msum, colA[j]);
           } else {
             double wm[kSlots];
 #pragma unroll

@@ -41,6 +41,7 @@ struct OpDev {
   const double* coef = nullptr;  // slot o at coef + o*n; nullptr -> constant w[]
   double w[kSlots] = {};         // constant weights
   double m[kSlots] = {};         // shift stencil (mass) weights
+  const double* mcoef = nullptr; // variable shift stencil (SoA), overrides m[]
   double sigma = 0.0;            // add_scaled(b, sigma): fl(w + fl(sigma*m))
   double invd_const = 0.0;       // 1/diag for the constant case
 };
@@ -54,6 +55,7 @@ struct MarchArgs {
   long long ld = 0;              // column stride of every vector operand
   OpDev op;
   double mw[kSlots] = {};        // right-hand-side mass stencil (setup modes)
+  const double* mwcoef = nullptr;// variable right-hand-side mass (SoA), overrides mw[]
   const double* src = nullptr;   // plane source (x | p | u | f)
   const double* pold = nullptr;  // K1: previous direction
   double* dst = nullptr;         // Apply: y; K1: p_new; Setup: r

@@ -259,7 +259,6 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
                   double drop_tol, double* lambdas, double* V, long long ldv, int* k_out, double* defect,
                   RitzInfo* info) {
   ctx.check_grid();
-  if (B.var) throw ParoError(kInvalidArgument, "rayleigh_ritz: B must be the constant mass stencil");
   if (K <= 0) throw ParoError(kEmptyBasis, "b_orthonormalize: all vectors dropped");
   const long long n = ctx.grid.n;
   if (ld != n || ldv != n) throw ParoError(kInvalidArgument, "rayleigh_ritz: vectors must be contiguous (ld == n)");

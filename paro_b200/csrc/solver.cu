@@ -13,6 +13,7 @@
 // chunks of iterations, keeping one chunk in flight ahead of the poll.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "march.cuh"
@@ -133,10 +134,11 @@ __global__ void zero_marked_kernel(const CgColumn* cols, int K, double* x, long 
 }
 
 // inv_diag = 1 / fl(c0 + fl(sigma*m0)); flags a non-positive diagonal.
-__global__ void invd_kernel(const double* c0, double sigma, double m0, long long n, double* invd, int* bad) {
+__global__ void invd_kernel(const double* c0, double sigma, double m0, const double* m0v, long long n, double* invd,
+                            int* bad) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const double d = __dadd_rn(c0[i], __dmul_rn(sigma, m0));
+    const double d = __dadd_rn(c0[i], __dmul_rn(sigma, m0v ? m0v[i] : m0));
     if (d <= 0.0) *bad = 1;
     invd[i] = 1.0 / d;
   }
@@ -156,6 +158,7 @@ OpDev make_opdev(const Ctx& ctx, const Op& a, const Op* shift, double sigma) {
   for (int o = 0; o < kSlots; ++o) d.w[o] = a.w[o];
   if (shift) {
     for (int o = 0; o < kSlots; ++o) d.m[o] = shift->w[o];
+    d.mcoef = shift->var ? shift->coef : nullptr;
     d.sigma = sigma;
   }
   if (!a.var) d.invd_const = 1.0 / (a.w[0] + d.sigma * d.m[0]);
@@ -184,7 +187,8 @@ void apply_op(Ctx& ctx, const Op& a, const Op* shift, double sigma, int K, const
 // setup pass computes r0 from either (M src)*scale (rhs == nullptr) or rhs.
 // warm: x0 = src (source solves) ; cold: x0 = 0 (Hartree).
 void batched_pcg(Ctx& ctx, const OpDev& op, bool var, int K, const double* src, const double* rhs,
-                 const double* scale_host, bool warm, double* x, long long ld, std::vector<CgColumn>& cols) {
+                 const double* scale_host, bool warm, double* x, long long ld, std::vector<CgColumn>& cols,
+                 const Op* mass) {
   const Grid& g = ctx.grid;
   const long long n = g.n;
   cudaStream_t st = ctx.stream;
@@ -193,7 +197,11 @@ void batched_pcg(Ctx& ctx, const OpDev& op, bool var, int K, const double* src, 
   m.K = K;
   m.ld = ld;
   m.op = op;
-  for (int o = 0; o < kSlots; ++o) m.mw[o] = ctx.mass_w[o];
+  if (mass) {
+    for (int o = 0; o < kSlots; ++o) m.mw[o] = mass->w[o];
+    m.mwcoef = mass->var ? mass->coef : nullptr;
+  }
+  if (!var && op.mcoef) throw ParoError(kInvalidArgument, "pcg: a variable shift needs a variable operator");
   const int cb = pick_cb(K);
 
   CgColumn* dcols = ctx.cols.get<CgColumn>(K);
@@ -213,7 +221,7 @@ void batched_pcg(Ctx& ctx, const OpDev& op, bool var, int K, const double* src, 
   double* invd = nullptr;
   if (var) {
     invd = ctx.invd.get<double>(n);
-    invd_kernel<<<148 * 8, 256, 0, st>>>(op.coef, op.sigma, op.m[0], n, invd, flag);
+    invd_kernel<<<148 * 8, 256, 0, st>>>(op.coef, op.sigma, op.m[0], op.mcoef, n, invd, flag);
     ++ctx.launches;
   } else {
     const double d = op.w[0] + op.sigma * op.m[0];
@@ -236,31 +244,45 @@ void batched_pcg(Ctx& ctx, const OpDev& op, bool var, int K, const double* src, 
   ctx.launches += 3;
   PARO_CUDA(cudaGetLastError());
 
-  // iteration chunks captured once into a CUDA graph
+  // iteration chunks captured once into a CUDA graph (PARO_NO_GRAPH=1 launches
+  // them directly, e.g. for ncu)
   const int chunk = n >= (1 << 22) ? 4 : n >= (1 << 18) ? 8 : 16;  // even: ping-pong parity repeats
+  auto enqueue_chunk = [&](cudaStream_t s) {
+    for (int it = 0; it < chunk; ++it) {
+      MarchArgs k1 = m;
+      k1.pold = (it & 1) ? p1 : p0;
+      k1.dst = (it & 1) ? p0 : p1;
+      k1.r = r;
+      launch_march(kK1, var, cb, k1, s);
+      fin_kernel<<<K, kFinThreads, 0, s>>>(kFinK1, dcols, partials, m.nblk, flag);
+      MarchArgs k2 = m;
+      k2.src = k1.dst;
+      k2.x = x;
+      k2.r = r;
+      launch_march(kK2, var, cb, k2, s);
+      fin_kernel<<<K, kFinThreads, 0, s>>>(kFinK2, dcols, partials, m.nblk, flag);
+    }
+    count_active_kernel<<<1, 256, 0, s>>>(dcols, K, ctx.pinned_count_dev);
+  };
+  static const bool no_graph = [] {
+    const char* e = std::getenv("PARO_NO_GRAPH");
+    return e && e[0] == '1';
+  }();
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
-  cudaStream_t cap;
-  PARO_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-  PARO_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-  for (int it = 0; it < chunk; ++it) {
-    MarchArgs k1 = m;
-    k1.pold = (it & 1) ? p1 : p0;
-    k1.dst = (it & 1) ? p0 : p1;
-    k1.r = r;
-    launch_march(kK1, var, cb, k1, cap);
-    fin_kernel<<<K, kFinThreads, 0, cap>>>(kFinK1, dcols, partials, m.nblk, flag);
-    MarchArgs k2 = m;
-    k2.src = k1.dst;
-    k2.x = x;
-    k2.r = r;
-    launch_march(kK2, var, cb, k2, cap);
-    fin_kernel<<<K, kFinThreads, 0, cap>>>(kFinK2, dcols, partials, m.nblk, flag);
+  if (!no_graph) {
+    cudaStream_t cap;
+    PARO_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    PARO_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    enqueue_chunk(cap);
+    PARO_CUDA(cudaStreamEndCapture(cap, &graph));
+    PARO_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    PARO_CUDA(cudaStreamDestroy(cap));
   }
-  count_active_kernel<<<1, 256, 0, cap>>>(dcols, K, ctx.pinned_count_dev);
-  PARO_CUDA(cudaStreamEndCapture(cap, &graph));
-  PARO_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-  PARO_CUDA(cudaStreamDestroy(cap));
+  auto launch_chunk = [&] {
+    if (no_graph) enqueue_chunk(st);
+    else PARO_CUDA(cudaGraphLaunch(exec, st));
+  };
   const unsigned long long nodes = 4ull * chunk + 1;
 
   cudaEvent_t ev[2];
@@ -282,7 +304,7 @@ void batched_pcg(Ctx& ctx, const OpDev& op, bool var, int K, const double* src, 
   PARO_CUDA(cudaEventRecord(tev[0], st));
   // keep one chunk in flight ahead of the poll
   if (remaining > 0) {
-    PARO_CUDA(cudaGraphLaunch(exec, st));
+    launch_chunk();
     PARO_CUDA(cudaEventRecord(ev[0], st));
     launched += chunk;
     ctx.launches += nodes;
@@ -291,7 +313,7 @@ void batched_pcg(Ctx& ctx, const OpDev& op, bool var, int K, const double* src, 
   while (remaining > 0) {
     const bool more = launched < max_iter;
     if (more) {
-      PARO_CUDA(cudaGraphLaunch(exec, st));
+      launch_chunk();
       PARO_CUDA(cudaEventRecord(ev[cur ^ 1], st));
       launched += chunk;
       ctx.launches += nodes;
@@ -313,8 +335,8 @@ void batched_pcg(Ctx& ctx, const OpDev& op, bool var, int K, const double* src, 
   PARO_CUDA(cudaEventDestroy(tev[1]));
   PARO_CUDA(cudaEventDestroy(ev[0]));
   PARO_CUDA(cudaEventDestroy(ev[1]));
-  PARO_CUDA(cudaGraphExecDestroy(exec));
-  PARO_CUDA(cudaGraphDestroy(graph));
+  if (exec) PARO_CUDA(cudaGraphExecDestroy(exec));
+  if (graph) PARO_CUDA(cudaGraphDestroy(graph));
   std::vector<CgColumn> before = cols;
   PARO_CUDA(cudaMemcpy(cols.data(), dcols, sizeof(CgColumn) * K, cudaMemcpyDeviceToHost));
   double col_iters = 0.0, batch_iters = 0.0;
@@ -343,15 +365,13 @@ int source_solve(Ctx& ctx, const Op& a, const Op& b, double sigma, int K, const 
                  SolveReport* report) {
   ctx.check_grid();
   if (!a.var && false) throw ParoError(kInvalidArgument, "source_solve: A must be variable");
-  if (b.var) throw ParoError(kInvalidArgument, "source_solve: B must be the constant mass stencil");
   if (K <= 0) return kOk;
-  for (int o = 0; o < kSlots; ++o) ctx.mass_w[o] = b.w[o];
   const OpDev op = make_opdev(ctx, a, &b, sigma);
   std::vector<double> scale(K);
   for (int c = 0; c < K; ++c) scale[c] = lambdas[c] + sigma;  // paro.cpp:97
   std::vector<CgColumn> cols(K);
   for (int c = 0; c < K; ++c) cols[c] = make_col(tol, max_iter);
-  batched_pcg(ctx, op, a.var, K, u, nullptr, scale.data(), true, out, ld, cols);
+  batched_pcg(ctx, op, a.var, K, u, nullptr, scale.data(), true, out, ld, cols, &b);
 
   std::vector<int> first_status(K, kOk), retry_status(K, kOk);
   std::vector<double> retry_resid(K, 0.0);
@@ -368,7 +388,7 @@ int source_solve(Ctx& ctx, const Op& a, const Op& b, double sigma, int K, const 
     }
   }
   if (any_retry) {
-    batched_pcg(ctx, op, a.var, K, u, nullptr, scale.data(), true, out, ld, retry);
+    batched_pcg(ctx, op, a.var, K, u, nullptr, scale.data(), true, out, ld, retry, &b);
     for (int c = 0; c < K; ++c)
       if (first_status[c] == kIterationLimit) {
         retry_status[c] = retry[c].status;
@@ -433,7 +453,7 @@ int cg_solve(Ctx& ctx, const Op& a, int K, const double* rhs, const double* x0, 
     PARO_CUDA(cudaMemsetAsync(zeros, 0, sizeof(double) * K * ld, ctx.stream));
     src = zeros;
   }
-  batched_pcg(ctx, op, a.var, K, src, rhs, nullptr, true, x, ld, cols);
+  batched_pcg(ctx, op, a.var, K, src, rhs, nullptr, true, x, ld, cols, nullptr);
   int status = kOk;
   if (report) {
     report->iterations.assign(K, 0);
@@ -462,12 +482,10 @@ int cg_solve(Ctx& ctx, const Op& a, int K, const double* rhs, const double* x0, 
 int hartree_solve(Ctx& ctx, const Op& poisson, const Op& mass, const double* rho, double tol, double* vh,
                   SolveReport* report) {
   ctx.check_grid();
-  if (mass.var) throw ParoError(kInvalidArgument, "hartree: mass must be the constant stencil");
-  for (int o = 0; o < kSlots; ++o) ctx.mass_w[o] = mass.w[o];
   const OpDev op = make_opdev(ctx, poisson, nullptr, 0.0);
   const double four_pi = 4.0 * M_PI;
   std::vector<CgColumn> cols(1, make_col(tol, 200000));
-  batched_pcg(ctx, op, poisson.var, 1, rho, nullptr, &four_pi, false, vh, ctx.grid.n, cols);
+  batched_pcg(ctx, op, poisson.var, 1, rho, nullptr, &four_pi, false, vh, ctx.grid.n, cols, &mass);
   if (report) {
     report->iterations.assign(1, cols[0].it);
     report->residual.assign(1, cols[0].bnorm > 0 ? cols[0].rnorm / cols[0].bnorm : 0.0);

@@ -50,6 +50,13 @@ class Dist:
         self.world = self.td.get_world_size(group) if self.td else 1
         self.rank = self.td.get_rank(group) if self.td else 0
 
+    def _gather(self, out: torch.Tensor, inp: torch.Tensor):
+        """all_gather_into_tensor (NCCL); list all_gather on backends without it (gloo)."""
+        if self.td.get_backend(self.group) == "nccl":
+            self.td.all_gather_into_tensor(out, inp, group=self.group)
+        else:
+            self.td.all_gather(list(out.chunk(self.world)), inp, group=self.group)
+
     def shard(self, K: int):
         base, rem = divmod(K, self.world)
         counts = [base + (1 if r < rem else 0) for r in range(self.world)]
@@ -68,7 +75,7 @@ class Dist:
         if local.shape[0] < kmax:
             send[: local.shape[0]].copy_(local)
         recv = local.new_empty((self.world * kmax, n))
-        self.td.all_gather_into_tensor(recv, send.contiguous(), group=self.group)
+        self._gather(recv, send.contiguous())
         row = 0
         for r, cnt in enumerate(counts):
             out[row: row + cnt].copy_(recv[r * kmax: r * kmax + cnt])
@@ -83,7 +90,7 @@ class Dist:
         if len(values):
             t[: len(values)] = torch.tensor(values, dtype=torch.int64, device=device)
         out = torch.empty(self.world * kmax, dtype=torch.int64, device=device)
-        self.td.all_gather_into_tensor(out, t, group=self.group)
+        self._gather(out, t)
         out = out.cpu().tolist()
         res = []
         for r, cnt in enumerate(counts):

@@ -1,0 +1,33 @@
+"""GPU runs of the BASELINE generators (scaled meshes) against the committed
+golden fixtures produced by the compiled reference (tests/golden/make_golden.py).
+North-star tolerances: eigenvalues 1e-8 relative, energy 1e-8 Ha; the density
+is compared through its size-independent checksums (integral, L2 norm)."""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+@pytest.mark.parametrize("name", ["h2_s16", "water_s24", "cluster32_s24", "oscillator_s16", "source64_s24"])
+def test_gpu_matches_golden_trace(name):
+    from paro_b200 import configs, core
+    from paro_b200.driver import GpuBackend, ParoRun
+
+    fx = json.loads((GOLDEN / f"{name}.json").read_text())
+    w = configs.get(fx["workload"])
+    run = ParoRun(w, GpuBackend(w))
+    np.testing.assert_allclose(run.lambdas[: len(fx["lambdas0"])], fx["lambdas0"], rtol=1e-10)
+    for row in fx["trace"]:
+        tr = run.step(row["iter"] - 1)
+        np.testing.assert_allclose(tr.lambdas, row["lambdas"], rtol=1e-8, atol=0)
+        assert tr.sigma == pytest.approx(row["sigma"], rel=1e-12, abs=1e-14)
+        if "e_tot" in row:
+            assert abs(tr.e_tot - row["e_tot"]) <= 1e-8
+            ctx = run.be.ctx
+            assert core.integrate(ctx, run.rho_out) == pytest.approx(row["rho_integral"], rel=1e-12)
+            assert abs(core.norm_l2(ctx, run.rho_out) - row["rho_l2"]) <= 1e-7
+            assert abs(tr.rho_residual - row["rho_residual"]) <= 1e-7
