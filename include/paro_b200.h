@@ -140,9 +140,10 @@ int paro_rayleigh_ritz(paro_ctx* ctx, const paro_op* a_form, const paro_op* b, i
                        long long ld, size_t min_keep, double drop_tol, double* lambdas, double* orbitals,
                        long long ldo, int* k_out, double* gram_defect);
 /* b_orthonormalize (linalg.cpp:409-439): two-pass Gram-Schmidt in the B inner
- * product with the relative drop rule; u, q: device (ld == n); k_out: host. */
+ * product with the relative drop rule; u, q: device (ld == n); k_out: host;
+ * accepted: host array of k (input index of each kept vector) or NULL. */
 int paro_b_orthonormalize(paro_ctx* ctx, const paro_op* b, int k, const double* u, double drop_tol, double* q,
-                          int* k_out);
+                          int* k_out, int* accepted);
 /* dense_sym_geneig on one warp of the device, host row-major m x m in/out. */
 int paro_dense_sym_geneig(paro_ctx* ctx, int m, const double* a, const double* b, double* values, double* vectors);
 /* fix_sign (linalg.cpp:229-241) on k device columns. */

@@ -1,0 +1,159 @@
+// integration/dropin_test.cpp — the reference's own hot-path test patterns
+// (proj/tests/test_paro.cpp:80-218, test_linalg.cpp:67-283) run against the
+// paro::gpu drop-ins and cross-checked with the CPU reference (paro::*) on a
+// 3-D Kohn-Sham system. Built by `make -C oracle dropin` next to the reference
+// objects; run on a GPU box by tests/test_gpu_dropin.py. Exit code 0 = pass.
+#include <cmath>
+#include <cstdio>
+#include <random>
+
+#include "paro/errors.hpp"
+#include "paro/paro.hpp"
+#include "paro_gpu.hpp"
+
+using namespace paro;
+
+static int failures = 0;
+#define CHECK(cond)                                                           \
+  do {                                                                        \
+    if (!(cond)) {                                                            \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);             \
+      ++failures;                                                             \
+    }                                                                         \
+  } while (0)
+
+template <typename E, typename F>
+bool throws(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+static double maxdiff(const std::vector<double>& a, const std::vector<double>& b) {
+  double d = 0.0;
+  for (std::size_t i = 0; i < a.size(); ++i) d = std::max(d, std::abs(a[i] - b[i]));
+  return d;
+}
+static double maxabs(const std::vector<double>& a) {
+  double d = 0.0;
+  for (double v : a) d = std::max(d, std::abs(v));
+  return d;
+}
+
+int main() {
+  Box box;
+  box.dim = 3;
+  box.lo = {-5, -5, -5};
+  box.hi = {5, 5, 5};
+  auto mesh = std::make_shared<Mesh>(create_box_mesh(box, 10));
+  auto space = FeSpace::create(mesh);
+  const std::size_t n = space->dof_count();
+  const SparseOperator mass = assemble_mass(*space);
+  SparseOperator a0 = assemble_stiffness(*space, constant_diffusion(0.5), constant_field(0.0));
+  Molecule mol;
+  mol.nuclei.push_back({1.0, {0.7, 0.1, 0.0}});
+  mol.nuclei.push_back({1.0, {-0.7, 0.0, 0.2}});
+  mol.n_electrons = 2;
+  const PotentialField vext = external_potential(mol, 0.0);
+  SingularQuadPolicy policy;
+  policy.singular_points = vext.singular_points;
+  a0.add_scaled(assemble_weighted_mass(*space, field_from(vext.value), policy));
+  const SparseOperator poisson = assemble_stiffness(*space, constant_diffusion(1.0), constant_field(0.0));
+
+  gpu::bind(*space);
+  CHECK(gpu::bound_to(*space));
+
+  std::mt19937_64 rng(7);
+  std::uniform_real_distribution<double> u(-1.0, 1.0);
+  std::vector<std::vector<double>> cand(4, std::vector<double>(n));
+  for (auto& c : cand)
+    for (double& x : c) x = u(rng);
+
+  // rayleigh_ritz: GPU vs CPU (paro.cpp:121-177)
+  const OrbitalSet ref_set = rayleigh_ritz(cand, a0, mass, space, 4, 1e-8);
+  const OrbitalSet gpu_set = gpu::rayleigh_ritz(cand, a0, mass, space, 4, 1e-8);
+  CHECK(gpu_set.count() == 4);
+  for (std::size_t j = 0; j < 4; ++j) {
+    CHECK(std::abs(gpu_set.lambdas[j] - ref_set.lambdas[j]) <= 1e-10 * std::abs(ref_set.lambdas[j]));
+    CHECK(maxdiff(gpu_set.orbitals[j], ref_set.orbitals[j]) <= 1e-8 * maxabs(ref_set.orbitals[j]));
+  }
+  CHECK(gpu_set.gram_defect <= 1e-8);
+
+  // Ritz vectors reproduce their values (test_paro.cpp:156-169 pattern)
+  const OrbitalSet back = gpu::rayleigh_ritz(ref_set.orbitals, a0, mass, space, 4, 1e-10);
+  for (std::size_t j = 0; j < 4; ++j)
+    CHECK(std::abs(back.lambdas[j] - ref_set.lambdas[j]) <= 1e-10 * std::abs(ref_set.lambdas[j]));
+
+  // degenerate span raises (test_paro.cpp:196-200)
+  std::vector<double> e0(n, 0.0);
+  e0[0] = 1.0;
+  CHECK(throws<DegenerateSpanError>([&] { gpu::rayleigh_ritz({e0, e0}, a0, mass, space, 2, 1e-8); }));
+
+  // Step 3 (paro.cpp:81-119): GPU vs CPU at the KS shift, determinism
+  SourceSolveOptions so;
+  so.tol = 1e-10;
+  so.sigma = 5.0;  // (A + 5 B) is SPD for this core Hamiltonian (lambda_min > -2)
+  const auto half_ref = source_solve_step(a0, mass, ref_set.orbitals, ref_set.lambdas, so);
+  const auto half1 = gpu::source_solve_step(a0, mass, ref_set.orbitals, ref_set.lambdas, so);
+  const auto half2 = gpu::source_solve_step(a0, mass, ref_set.orbitals, ref_set.lambdas, so);
+  for (std::size_t j = 0; j < 4; ++j) {
+    CHECK(maxdiff(half1[j], half_ref[j]) <= 1e-8 * maxabs(half_ref[j]));
+    CHECK(half1[j] == half2[j]);  // bitwise run-to-run
+  }
+  // iteration-limit failures propagate after the retry (test_paro.cpp:143-154)
+  SourceSolveOptions bad = so;
+  bad.tol = 1e-30;
+  bad.max_iter = 2;
+  CHECK(throws<IterationLimitError>([&] { gpu::source_solve_step(a0, mass, cand, ref_set.lambdas, bad); }));
+  // NotSpd without the shift on an indefinite operator
+  SourceSolveOptions noshift = so;
+  noshift.sigma = -10.0;
+  CHECK(throws<NotSpdError>([&] { gpu::source_solve_step(a0, mass, ref_set.orbitals, ref_set.lambdas, noshift); }));
+
+  // cg_solve (linalg.cpp:143-223)
+  std::vector<double> rhs = mass.apply(cand[0]);
+  CgOptions co;
+  co.tol = 1e-11;
+  const CgResult cr = cg_solve(poisson, rhs, co);
+  const CgResult cg = gpu::cg_solve(poisson, rhs, co);
+  CHECK(cg.converged);
+  CHECK(std::abs(static_cast<long>(cg.iterations) - static_cast<long>(cr.iterations)) <= 1);
+  CHECK(maxdiff(cg.x, cr.x) <= 1e-9 * maxabs(cr.x));
+
+  // b_orthonormalize drops the dependent vector (linalg.cpp:409-439)
+  const auto orr = gpu::b_orthonormalize({cand[0], cand[1], cand[0]}, mass, 1e-8);
+  CHECK(orr.vectors.size() == 2 && orr.dropped.size() == 1 && orr.dropped[0] == 2);
+
+  // dense_sym_geneig: bit-identical for the same pencil (linalg.cpp:341-393)
+  DenseSymPencil p;
+  p.a = DenseMatrix(6, 6);
+  p.b = DenseMatrix(6, 6);
+  for (std::size_t i = 0; i < 6; ++i)
+    for (std::size_t j = 0; j <= i; ++j) {
+      const double x = u(rng), y = u(rng);
+      p.a(i, j) = p.a(j, i) = x;
+      p.b(i, j) = p.b(j, i) = (i == j ? 6.0 : 0.0) + 0.3 * y;
+    }
+  const EigenPairs er = dense_sym_geneig(p), eg = gpu::dense_sym_geneig(p);
+  CHECK(er.values == eg.values);
+  CHECK(er.vectors.data() == eg.vectors.data());
+
+  // density, Hartree, energy (model.cpp:192-360)
+  std::vector<DiscreteFunction> occ{DiscreteFunction(space, ref_set.orbitals[0])};
+  const Density dr = density_from_orbitals(occ, {2.0}), dg = gpu::density_from_orbitals(occ, {2.0});
+  CHECK(maxdiff(dr.rho.coeffs, dg.rho.coeffs) <= 1e-13 * maxabs(dr.rho.coeffs));
+  const DiscreteFunction vr = hartree_solve_with(poisson, mass, dr, space, 1e-11);
+  const DiscreteFunction vg = gpu::hartree_solve_with(poisson, mass, dr, space, 1e-11);
+  CHECK(maxdiff(vr.coeffs, vg.coeffs) <= 1e-9 * maxabs(vr.coeffs));
+  const double Er = total_energy(ref_set.lambdas, dr, vr, XcModel::lda_pz81, mol);
+  const double Eg = gpu::total_energy(ref_set.lambdas, dr, vr, XcModel::lda_pz81, mol);
+  CHECK(std::abs(Er - Eg) <= 1e-12 * std::abs(Er));
+
+  std::printf("%s dropin_test (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
+  return failures ? 1 : 0;
+}

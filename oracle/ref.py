@@ -73,7 +73,10 @@ def build() -> None:
         return
     import subprocess
 
-    subprocess.run(["make", "-s", "-j8", "-C", str(HERE)], check=True)
+    subprocess.run(["make", "-s", "-j8", "-C", str(HERE), "all"], check=True)
+    gpu_lib = HERE.parent / "paro_b200" / "_lib" / "libparo_b200.so"
+    if gpu_lib.exists():  # the C++ drop-in check links the product library
+        subprocess.run(["make", "-s", "-C", str(HERE), "dropin"], check=True)
 
 
 def lib():

@@ -332,7 +332,9 @@ def b_orthonormalize(vectors: torch.Tensor, b: Operator, drop_tol: float) -> tor
     U = _as_cols(vectors, ctx.n).contiguous()
     Q = torch.empty_like(U)
     k = C.c_int(0)
-    ctx.check(N.lib().paro_b_orthonormalize(ctx.h, b.h, U.shape[0], _ptr(U), float(drop_tol), _ptr(Q), C.byref(k)))
+    acc = (C.c_int * max(1, U.shape[0]))()
+    ctx.check(N.lib().paro_b_orthonormalize(ctx.h, b.h, U.shape[0], _ptr(U), float(drop_tol), _ptr(Q), C.byref(k),
+                                            acc))
     return Q[: k.value]
 
 

@@ -415,8 +415,8 @@ int paro_rayleigh_ritz(paro_ctx* ctx, const paro_op* a, const paro_op* b, int k,
 }
 
 int paro_b_orthonormalize(paro_ctx* ctx, const paro_op* b, int k, const double* u, double drop_tol, double* q,
-                          int* k_out) {
-  return guarded(ctx, [&] { return b_orthonormalize(ctx->c, b->o, k, u, drop_tol, q, k_out); });
+                          int* k_out, int* accepted) {
+  return guarded(ctx, [&] { return b_orthonormalize(ctx->c, b->o, k, u, drop_tol, q, k_out, accepted); });
 }
 
 int paro_dense_sym_geneig(paro_ctx* ctx, int m, const double* a, const double* b, double* vals, double* vecs) {

@@ -220,7 +220,7 @@ double ddot(Ctx& ctx, const double* x, const double* y) {
 // Q (k columns) B-orthonormal, BQ = B Q. Used when the candidates are too
 // ill-conditioned for the Cholesky-QR path (e.g. right after a noise start).
 int cgs2_orthonormalize(Ctx& ctx, const Op& B, int K, const double* U, double drop_tol, double* Q, double* BQ,
-                        int* kout) {
+                        int* kout, int* accepted = nullptr) {
   const long long n = ctx.grid.n;
   cudaStream_t st = ctx.stream;
   double* h = ctx.ws_e.get<double>(2 * static_cast<size_t>(n) + K);
@@ -247,6 +247,7 @@ int cgs2_orthonormalize(Ctx& ctx, const Op& B, int K, const double* U, double dr
     div_kernel<<<blocks, 256, 0, st>>>(Q + k * n, h, nb, n);
     ++ctx.launches;
     apply_op(ctx, B, nullptr, 0.0, 1, Q + k * n, n, BQ + k * n, n);
+    if (accepted) accepted[k] = j;
     ++k;
   }
   *kout = k;
@@ -361,12 +362,13 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
   return kOk;
 }
 
-int b_orthonormalize(Ctx& ctx, const Op& B, int K, const double* U, double drop_tol, double* Q, int* k_out) {
+int b_orthonormalize(Ctx& ctx, const Op& B, int K, const double* U, double drop_tol, double* Q, int* k_out,
+                     int* accepted) {
   ctx.check_grid();
   const long long n = ctx.grid.n;
   cublasSetStream(ctx.cublas, ctx.stream);
   double* BQ = ctx.ws_b.get<double>(static_cast<size_t>(K) * n);
-  cgs2_orthonormalize(ctx, B, K, U, drop_tol, Q, BQ, k_out);
+  cgs2_orthonormalize(ctx, B, K, U, drop_tol, Q, BQ, k_out, accepted);
   PARO_CUDA(cudaStreamSynchronize(ctx.stream));
   if (*k_out == 0 && K > 0) {
     ctx.err = "b_orthonormalize: all vectors dropped";
