@@ -1,5 +1,12 @@
 // Plane-marching stencil kernels: operator apply, the two fused Jacobi-PCG
 // passes and the PCG setup pass. See march.cuh for the design.
+//
+// v2 pipeline: planes are moved global -> shared with cp.async (LDGSTS, zero
+// fill outside the lattice) two planes ahead of the compute, so no registers
+// hold in-flight data and the DRAM requests of the next plane overlap the
+// stencil of the current one. K2 additionally stages the own-point x, r of
+// the next plane. K1 stages the raw r, p_old (and diagonal) planes and
+// transforms them into p_new = z + beta p_old once they land.
 #include <algorithm>
 
 #include "march.cuh"
@@ -7,6 +14,22 @@
 namespace paro_b200 {
 
 namespace {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// 8-byte async copy; src_size 0 zero-fills the destination (Dirichlet halo)
+__device__ __forceinline__ void cp8(double* dst, const double* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -18,9 +41,18 @@ __device__ __forceinline__ double warp_sum(double v) {
 __device__ __forceinline__ double madd(double s, double w, double x) { return __dadd_rn(s, __dmul_rn(w, x)); }
 
 template <int MODE>
-struct Acc {
-  static constexpr int N = MODE == kApply ? 1 : MODE == kK1 ? 1 : MODE == kK2 ? 2 : 3;
+struct Cfg {
+  static constexpr int NA = MODE == kApply ? 1 : MODE == kK1 ? 1 : MODE == kK2 ? 2 : 3;  // partial sums
+  static constexpr int NR = MODE == kK1 ? 3 : 4;  // ring slots of stencil-source planes
 };
+
+template <int MODE, int CB>
+constexpr size_t smem_bytes() {
+  size_t d = static_cast<size_t>(Cfg<MODE>::NR) * CB * kHP;
+  if (MODE == kK2) d += static_cast<size_t>(2) * CB * 2 * kNT;   // x, r stages
+  if (MODE == kK1) d += static_cast<size_t>(2) * (2 * CB + 1) * kHP;  // raw r, p_old, invd stages
+  return d * sizeof(double);
+}
 
 // 15-point row sum in ascending column order (linalg.cpp:88-94 on the Kuhn
 // pattern). wb[o]: A[v, v-off(o)], wf[o]: A[v, v+off(o)], w0: diagonal.
@@ -48,9 +80,8 @@ __device__ __forceinline__ double row_sum(const double* __restrict__ Pm, const d
 
 // own[o] = A[v, v+o] stored at v; back[o] = A[v, v-o] stored at v-o (0 when
 // v-o leaves the lattice, where the plane value is 0 anyway)
-__device__ __forceinline__ void load_weights(const double* __restrict__ cf, long long n, long long idx, int gx, int gy,
-                                             int z, int S, long long S2, double (&own)[kSlots],
-                                             double (&back)[kSlots]) {
+__device__ __forceinline__ void load_weights(const double* __restrict__ cf, long long n, int idx, int gx, int gy,
+                                             int z, int S, int S2, double (&own)[kSlots], double (&back)[kSlots]) {
 #pragma unroll
   for (int o = 0; o < kSlots; ++o) own[o] = __ldg(cf + o * n + idx);
   back[0] = 0.0;
@@ -58,18 +89,26 @@ __device__ __forceinline__ void load_weights(const double* __restrict__ cf, long
   for (int o = 1; o < kSlots; ++o) {
     const int ox = o & 1, oy = (o >> 1) & 1, oz = (o >> 2) & 1;
     const bool ok = gx >= ox && gy >= oy && z >= oz;
-    const long long nb = idx - ox - static_cast<long long>(oy) * S - static_cast<long long>(oz) * S2;
+    const int nb = idx - ox - oy * S - oz * S2;
     back[o] = ok ? __ldg(cf + o * n + nb) : 0.0;
   }
 }
 
 template <int MODE, bool VAR, int CB>
 __global__ void __launch_bounds__(kNT, 2) march_kernel(const MarchArgs a) {
-  extern __shared__ double smem[];  // [3][CB][kHP]
-  constexpr int NA = Acc<MODE>::N;
+  extern __shared__ __align__(16) double smem[];
+  constexpr int NA = Cfg<MODE>::NA;
+  constexpr int NR = Cfg<MODE>::NR;
   __shared__ double red[kNT / 32][CB * NA];
+  __shared__ double colA[CB], colB[CB];
+  __shared__ int colFirst[CB];
+
+  double* ring = smem;                                   // [NR][CB][kHP]
+  double* stage = ring + NR * CB * kHP;                  // K2: [2][CB][2][kNT]
+  double* raw = stage + (MODE == kK2 ? 2 * CB * 2 * kNT : 0);  // K1: [2][2CB+1][kHP]
 
   const int S = a.S;
+  const int S2 = S * S;
   const long long n = a.n;
   const int tid = threadIdx.x;
   const int b = blockIdx.y;
@@ -84,6 +123,22 @@ __global__ void __launch_bounds__(kNT, 2) march_kernel(const MarchArgs a) {
     any |= act[j];
   }
   if (!any) return;
+  if (tid < CB) {
+    const int c = c0 + tid;
+    double va = 0.0, vb = 0.0;
+    int f = 0;
+    if (act[tid]) {
+      if (MODE == kK1) {
+        vb = a.cols[c].beta;
+        f = a.cols[c].first != 0;
+      }
+      if (MODE == kK2) va = a.cols[c].alpha;
+      if (MODE == kSetupWarm || MODE == kSetupCold) va = a.scale[c];
+    }
+    colA[tid] = va;
+    colB[tid] = vb;
+    colFirst[tid] = f;
+  }
 
   const int bx = b % a.nTX;
   const int by = (b / a.nTX) % a.nTY;
@@ -94,13 +149,11 @@ __global__ void __launch_bounds__(kNT, 2) march_kernel(const MarchArgs a) {
   const int tx = tid % kTX, ty = tid / kTX;
   const int gx = x0 + tx, gy = y0 + ty;
   const bool inside = gx < S && gy < S;
-  const long long S2 = static_cast<long long>(S) * S;
+  const int own = gy * S + gx;  // in-plane offset of this thread's point
 
-  // the (up to) two halo'd-plane positions this thread loads
-  int pos[kLoadsPerThread];
-  long long roff[kLoadsPerThread];
-  bool pval[kLoadsPerThread];
-  bool pown[kLoadsPerThread];
+  // the (up to) two halo'd-plane positions this thread copies
+  int pos[kLoadsPerThread], roff[kLoadsPerThread];
+  bool pval[kLoadsPerThread], pown[kLoadsPerThread];
 #pragma unroll
   for (int l = 0; l < kLoadsPerThread; ++l) {
     const int i = tid + l * kNT;
@@ -109,27 +162,83 @@ __global__ void __launch_bounds__(kNT, 2) march_kernel(const MarchArgs a) {
     const int px = x0 + hx - 1, py = y0 + hy - 1;
     pval[l] = i < kHP && px >= 0 && px < S && py >= 0 && py < S;
     pown[l] = pval[l] && hx >= 1 && hx <= kTX && hy >= 1 && hy <= kTY;
-    roff[l] = pval[l] ? static_cast<long long>(py) * S + px : 0;
+    roff[l] = pval[l] ? py * S + px : 0;
   }
+  __syncthreads();  // colA/colB/colFirst
 
-  // per-column scalars
-  double colA[CB], colB[CB];
-  bool colFirst[CB];
+  auto rs = [&](int z) { return (z - z0 + 1 + NR) % NR; };
+
+  // stencil-source plane z -> ring slot (non-K1 modes)
+  auto issue_plane = [&](int z) {
+    const bool zin = z >= 0 && z < S;
+    const int zoff = zin ? z * S2 : 0;
+    double* slot = ring + rs(z) * CB * kHP;
 #pragma unroll
-  for (int j = 0; j < CB; ++j) {
-    colA[j] = 0.0;
-    colB[j] = 0.0;
-    colFirst[j] = false;
-    if (act[j]) {
-      const int c = c0 + j;
-      if (MODE == kK1) {
-        colB[j] = a.cols[c].beta;
-        colFirst[j] = a.cols[c].first != 0;
+    for (int l = 0; l < kLoadsPerThread; ++l) {
+      if (pos[l] >= kHP) continue;
+#pragma unroll
+      for (int j = 0; j < CB; ++j) {
+        const double* col = a.src + static_cast<long long>(c0 + j) * a.ld;
+        const bool v = zin && pval[l] && act[j];
+        cp8(slot + j * kHP + pos[l], v ? col + zoff + roff[l] : col, v);
       }
-      if (MODE == kK2) colA[j] = a.cols[c].alpha;
-      if (MODE == kSetupWarm || MODE == kSetupCold) colA[j] = a.scale[c];
     }
-  }
+  };
+  // K1 raw planes r, p_old (+ diagonal) -> raw stage (z & 1)
+  auto issue_raw = [&](int z) {
+    const bool zin = z >= 0 && z < S;
+    const int zoff = zin ? z * S2 : 0;
+    double* rw = raw + (z & 1) * (2 * CB + 1) * kHP;
+#pragma unroll
+    for (int l = 0; l < kLoadsPerThread; ++l) {
+      if (pos[l] >= kHP) continue;
+#pragma unroll
+      for (int j = 0; j < CB; ++j) {
+        const long long co = static_cast<long long>(c0 + j) * a.ld;
+        const bool v = zin && pval[l] && act[j];
+        cp8(rw + j * kHP + pos[l], v ? a.r + co + zoff + roff[l] : a.r + co, v);
+        const bool vp = v && !colFirst[j];
+        cp8(rw + (CB + j) * kHP + pos[l], vp ? a.pold + co + zoff + roff[l] : a.pold + co, vp);
+      }
+      if (VAR) {
+        const bool v = zin && pval[l];
+        cp8(rw + 2 * CB * kHP + pos[l], v ? a.invd + zoff + roff[l] : a.invd, v);
+      }
+    }
+  };
+  // K2 own-point x, r of plane z -> stage (z & 1)
+  auto issue_xr = [&](int z) {
+    if (!inside || z >= z1) return;
+    const int zoff = z * S2;
+    double* st = stage + (z & 1) * CB * 2 * kNT;
+#pragma unroll
+    for (int j = 0; j < CB; ++j) {
+      if (!act[j]) continue;
+      const long long co = static_cast<long long>(c0 + j) * a.ld;
+      cp8(st + (j * 2 + 0) * kNT + tid, a.x + co + zoff + own, true);
+      cp8(st + (j * 2 + 1) * kNT + tid, a.r + co + zoff + own, true);
+    }
+  };
+  // K1: raw plane z -> p_new = z + beta p_old in ring slot; own points also to global
+  auto transform = [&](int z) {
+    const double* rw = raw + (z & 1) * (2 * CB + 1) * kHP;
+    double* slot = ring + rs(z) * CB * kHP;
+    const bool zown = z >= z0 && z < z1;
+    const int zoff = z * S2;
+#pragma unroll
+    for (int l = 0; l < kLoadsPerThread; ++l) {
+      if (pos[l] >= kHP) continue;
+      const double d = VAR ? rw[2 * CB * kHP + pos[l]] : (pval[l] ? a.op.invd_const : 0.0);
+#pragma unroll
+      for (int j = 0; j < CB; ++j) {
+        // z = inv_diag * r ; p = z + beta * p   (linalg.cpp:179, 210)
+        const double zz = __dmul_rn(d, rw[j * kHP + pos[l]]);
+        const double v = colFirst[j] ? zz : __dadd_rn(zz, __dmul_rn(colB[j], rw[(CB + j) * kHP + pos[l]]));
+        slot[j * kHP + pos[l]] = v;
+        if (zown && pown[l] && act[j]) a.dst[static_cast<long long>(c0 + j) * a.ld + zoff + roff[l]] = v;
+      }
+    }
+  };
 
   double acc[CB][NA];
 #pragma unroll
@@ -137,91 +246,65 @@ __global__ void __launch_bounds__(kNT, 2) march_kernel(const MarchArgs a) {
 #pragma unroll
     for (int q = 0; q < NA; ++q) acc[j][q] = 0.0;
 
-  // prefetch registers
-  double pv0[CB][kLoadsPerThread];
-  double pv1[CB][kLoadsPerThread];  // K1: p_old
-  double pd[kLoadsPerThread];       // K1: invd
-
-  auto fetch = [&](int z) {
-    const bool zin = z >= 0 && z < S;
-#pragma unroll
-    for (int l = 0; l < kLoadsPerThread; ++l) {
-      const bool ok = zin && pval[l];
-      const long long idx = static_cast<long long>(z) * S2 + roff[l];
-      if (MODE == kK1) pd[l] = ok ? (VAR ? __ldg(a.invd + idx) : a.op.invd_const) : 0.0;
-#pragma unroll
-      for (int j = 0; j < CB; ++j) {
-        const long long gi = static_cast<long long>(c0 + j) * a.ld + idx;
-        if (MODE == kK1) {
-          pv0[j][l] = (ok && act[j]) ? a.r[gi] : 0.0;
-          pv1[j][l] = (ok && act[j] && !colFirst[j]) ? a.pold[gi] : 0.0;
-        } else {
-          pv0[j][l] = (ok && act[j]) ? __ldg(a.src + gi) : 0.0;
-        }
-      }
-    }
-  };
-
-  auto store = [&](int z, int slot) {
-    const bool zown = z >= z0 && z < z1;
-#pragma unroll
-    for (int l = 0; l < kLoadsPerThread; ++l) {
-      if (pos[l] >= kHP) continue;
-#pragma unroll
-      for (int j = 0; j < CB; ++j) {
-        double v = pv0[j][l];
-        if (MODE == kK1) {
-          // z = inv_diag * r ; p = z + beta * p   (linalg.cpp:179, 210)
-          const double zz = __dmul_rn(pd[l], pv0[j][l]);
-          v = colFirst[j] ? zz : __dadd_rn(zz, __dmul_rn(colB[j], pv1[j][l]));
-          if (zown && pown[l] && act[j]) {
-            const long long idx = static_cast<long long>(z) * S2 + roff[l];
-            a.dst[static_cast<long long>(c0 + j) * a.ld + idx] = v;
-          }
-        }
-        smem[(slot * CB + j) * kHP + pos[l]] = v;
-      }
-    }
-  };
-
-  // ring: slots hold planes z-1, z, z+1
-  int sm = 0, s0 = 1, sp = 2;
-  fetch(z0 - 1);
-  store(z0 - 1, sm);
-  fetch(z0);
-  store(z0, s0);
-  fetch(z0 + 1);
+  // prologue
+  if (MODE == kK1) {
+    issue_raw(z0 - 1);
+    issue_raw(z0);
+    cp_commit();
+    cp_wait<0>();
+    __syncthreads();
+    transform(z0 - 1);
+    transform(z0);
+    __syncthreads();
+    issue_raw(z0 + 1);
+    cp_commit();
+  } else {
+    issue_plane(z0 - 1);
+    issue_plane(z0);
+    issue_plane(z0 + 1);
+    if (MODE == kK2) issue_xr(z0);
+    cp_commit();
+  }
 
   const int ib = (ty + 1) * kHX + (tx + 1);
   for (int z = z0; z < z1; ++z) {
-    __syncthreads();  // all reads of slot sp (plane z-2) are finished
-    store(z + 1, sp);
+    if (MODE == kK1) {
+      if (z + 2 <= z1) issue_raw(z + 2);
+    } else {
+      if (z + 2 <= z1) issue_plane(z + 2);
+      if (MODE == kK2) issue_xr(z + 1);
+    }
+    cp_commit();
+    cp_wait<1>();
     __syncthreads();
-    if (z + 2 <= z1) fetch(z + 2);
+    if (MODE == kK1) {
+      transform(z + 1);
+      __syncthreads();
+    }
 
     if (inside) {
-      const long long idx = static_cast<long long>(z) * S2 + static_cast<long long>(gy) * S + gx;
+      const int idx = z * S2 + own;
       // 15 weights of the operator at this point, shifted by sigma*M
       double wb[kSlots], wf[kSlots], w0;
       if (VAR) {
-        double own[kSlots], back[kSlots];
-        load_weights(a.op.coef, n, idx, gx, gy, z, S, S2, own, back);
+        double ow[kSlots], bk[kSlots];
+        load_weights(a.op.coef, n, idx, gx, gy, z, S, S2, ow, bk);
         if (a.op.mcoef != nullptr) {  // variable shift stencil (inexact mesh spacing)
           double mown[kSlots], mback[kSlots];
           load_weights(a.op.mcoef, n, idx, gx, gy, z, S, S2, mown, mback);
 #pragma unroll
           for (int o = 1; o < kSlots; ++o) {
-            wb[o] = __dadd_rn(back[o], __dmul_rn(a.op.sigma, mback[o]));
-            wf[o] = __dadd_rn(own[o], __dmul_rn(a.op.sigma, mown[o]));
+            wb[o] = __dadd_rn(bk[o], __dmul_rn(a.op.sigma, mback[o]));
+            wf[o] = __dadd_rn(ow[o], __dmul_rn(a.op.sigma, mown[o]));
           }
-          w0 = __dadd_rn(own[0], __dmul_rn(a.op.sigma, mown[0]));
+          w0 = __dadd_rn(ow[0], __dmul_rn(a.op.sigma, mown[0]));
         } else {
 #pragma unroll
           for (int o = 1; o < kSlots; ++o) {
-            wb[o] = __dadd_rn(back[o], __dmul_rn(a.op.sigma, a.op.m[o]));
-            wf[o] = __dadd_rn(own[o], __dmul_rn(a.op.sigma, a.op.m[o]));
+            wb[o] = __dadd_rn(bk[o], __dmul_rn(a.op.sigma, a.op.m[o]));
+            wf[o] = __dadd_rn(ow[o], __dmul_rn(a.op.sigma, a.op.m[o]));
           }
-          w0 = __dadd_rn(own[0], __dmul_rn(a.op.sigma, a.op.m[0]));
+          w0 = __dadd_rn(ow[0], __dmul_rn(a.op.sigma, a.op.m[0]));
         }
       } else {
 #pragma unroll
@@ -234,15 +317,16 @@ __global__ void __launch_bounds__(kNT, 2) march_kernel(const MarchArgs a) {
       wb[0] = wf[0] = 0.0;
       double invd = 0.0;
       if (MODE == kK2 || MODE == kSetupWarm || MODE == kSetupCold) invd = VAR ? __ldg(a.invd + idx) : a.op.invd_const;
+      const double* Pm = ring + rs(z - 1) * CB * kHP;
+      const double* P0 = ring + rs(z) * CB * kHP;
+      const double* Pp = ring + rs(z + 1) * CB * kHP;
+      const double* st = stage + (z & 1) * CB * 2 * kNT;
 
 #pragma unroll
       for (int j = 0; j < CB; ++j) {
         if (!act[j]) continue;
-        const double* Pm = smem + (sm * CB + j) * kHP;
-        const double* P0 = smem + (s0 * CB + j) * kHP;
-        const double* Pp = smem + (sp * CB + j) * kHP;
-        const double s = row_sum(Pm, P0, Pp, ib, wb, w0, wf);
-        const double ctr = P0[ib];
+        const double s = row_sum(Pm + j * kHP, P0 + j * kHP, Pp + j * kHP, ib, wb, w0, wf);
+        const double ctr = P0[j * kHP + ib];
         const long long gi = static_cast<long long>(c0 + j) * a.ld + idx;
         if (MODE == kApply) {
           a.dst[gi] = s;
@@ -251,8 +335,9 @@ __global__ void __launch_bounds__(kNT, 2) march_kernel(const MarchArgs a) {
           acc[j][0] += ctr * s;  // p'q
         } else if (MODE == kK2) {
           // x += alpha p ; r -= alpha q ; z = invd r  (linalg.cpp:202-206)
-          const double xn = __dadd_rn(a.x[gi], __dmul_rn(colA[j], ctr));
-          const double rn = __dsub_rn(a.r[gi], __dmul_rn(colA[j], s));
+          const double al = colA[j];
+          const double xn = __dadd_rn(st[(j * 2 + 0) * kNT + tid], __dmul_rn(al, ctr));
+          const double rn = __dsub_rn(st[(j * 2 + 1) * kNT + tid], __dmul_rn(al, s));
           a.x[gi] = xn;
           a.r[gi] = rn;
           const double zz = __dmul_rn(invd, rn);
@@ -266,13 +351,13 @@ __global__ void __launch_bounds__(kNT, 2) march_kernel(const MarchArgs a) {
           } else if (a.mwcoef != nullptr) {
             double mown[kSlots], mback[kSlots];
             load_weights(a.mwcoef, n, idx, gx, gy, z, S, S2, mown, mback);
-            const double msum = row_sum(Pm, P0, Pp, ib, mback, mown[0], mown);
+            const double msum = row_sum(Pm + j * kHP, P0 + j * kHP, Pp + j * kHP, ib, mback, mown[0], mown);
             bb = __dmul_rn(msum, colA[j]);
           } else {
             double wm[kSlots];
 #pragma unroll
             for (int o = 0; o < kSlots; ++o) wm[o] = a.mw[o];
-            const double msum = row_sum(Pm, P0, Pp, ib, wm, wm[0], wm);
+            const double msum = row_sum(Pm + j * kHP, P0 + j * kHP, Pp + j * kHP, ib, wm, wm[0], wm);
             bb = __dmul_rn(msum, colA[j]);
           }
           double rr;
@@ -291,11 +376,9 @@ __global__ void __launch_bounds__(kNT, 2) march_kernel(const MarchArgs a) {
         }
       }
     }
-    const int t = sm;
-    sm = s0;
-    s0 = sp;
-    sp = t;
+    __syncthreads();  // slots read this step are overwritten by the next issue
   }
+  cp_wait<0>();
 
   if (MODE == kApply && !a.with_dot) return;
   // deterministic block reduction: warp tree, then warps in order
@@ -322,7 +405,7 @@ __global__ void __launch_bounds__(kNT, 2) march_kernel(const MarchArgs a) {
 template <int MODE, bool VAR, int CB>
 void launch_t(const MarchArgs& a, cudaStream_t st) {
   const int groups = (a.K + CB - 1) / CB;
-  const size_t sm = static_cast<size_t>(3) * CB * kHP * sizeof(double);
+  constexpr size_t sm = smem_bytes<MODE, CB>();
   static bool configured = false;
   if (!configured) {
     PARO_CUDA(cudaFuncSetAttribute(march_kernel<MODE, VAR, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -339,8 +422,7 @@ void launch_cb(int cb, const MarchArgs& a, cudaStream_t st) {
   switch (cb) {
     case 1: launch_t<MODE, VAR, 1>(a, st); break;
     case 2: launch_t<MODE, VAR, 2>(a, st); break;
-    case 4: launch_t<MODE, VAR, 4>(a, st); break;
-    default: launch_t<MODE, VAR, 8>(a, st); break;
+    default: launch_t<MODE, VAR, 4>(a, st); break;
   }
 }
 
@@ -353,6 +435,7 @@ void launch_var(bool var, int cb, const MarchArgs& a, cudaStream_t st) {
 }  // namespace
 
 void launch_march(int mode, bool var, int cb, const MarchArgs& a, cudaStream_t st) {
+  if (a.n > (1ll << 31) - 1) throw ParoError(kCapacity, "march: more than 2^31 interior dofs per column");
   switch (mode) {
     case kApply: launch_var<kApply>(var, cb, a, st); break;
     case kK1: launch_var<kK1>(var, cb, a, st); break;
