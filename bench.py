@@ -278,6 +278,8 @@ def main():
                           "step3_pcg_s": st["step3_s"] / args.steps, "hartree_pcg_s": st["hartree_s"] / args.steps,
                           "hartree_achieved_gbs": st["hartree_bytes"] / st["hartree_s"] / 1e9 if st["hartree_s"] else 0,
                           "cg_iterations_last_step": iters, "setup_s": t_setup,
+                          "sigma_last_step": traces[-1].sigma, "step3_attempts_last_step": run.last_attempts,
+                          "step3_col_iters_per_step": st["step3_col_iters"] / args.steps,
                           "lambda_1": traces[-1].lambdas[0], "e_tot": traces[-1].e_tot},
         }
         print(json.dumps(line), flush=True)

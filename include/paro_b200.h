@@ -62,6 +62,11 @@ int paro_ctx_stats(paro_ctx* ctx, double out[8], int reset);
  * Gram-Schmidt fallback for near-dependent candidates (default), 1 = always
  * two-pass Gram-Schmidt (b_orthonormalize's algorithm, linalg.cpp:409-439). */
 int paro_ctx_set_ritz_mode(paro_ctx* ctx, int mode);
+/* Hartree solve: 0 = cold-start Jacobi-PCG to tol (the reference algorithm,
+ * model.cpp:242-255), 1 = exact 3-D DST-I solve when the Poisson stiffness is
+ * the constant 7-point stencil, else PCG (default). The tol-1e-11 PCG iterate
+ * lies within ~1e-12 (relative) of the exact solution. */
+int paro_ctx_set_hartree_mode(paro_ctx* ctx, int mode);
 
 /* Device memory helpers for callers without their own allocator. */
 int paro_malloc(paro_ctx* ctx, size_t bytes, void** dev);

@@ -88,6 +88,16 @@ class Context:
     def synchronize(self):
         self.check(N.lib().paro_ctx_synchronize(self.h))
 
+    def set_hartree_mode(self, mode: str) -> "Context":
+        """'cg': Jacobi-PCG to tol (reference algorithm); 'dst': exact DST-I solve when applicable."""
+        self.check(N.lib().paro_ctx_set_hartree_mode(self.h, {"cg": 0, "dst": 1}[mode]))
+        return self
+
+    def set_ritz_mode(self, mode: str) -> "Context":
+        """'cholqr': Cholesky-QR twice with Gram-Schmidt fallback; 'cgs2': always Gram-Schmidt."""
+        self.check(N.lib().paro_ctx_set_ritz_mode(self.h, {"cholqr": 0, "cgs2": 1}[mode]))
+        return self
+
     def empty(self, *shape) -> torch.Tensor:
         return torch.empty(*shape, dtype=torch.float64, device=self.device)
 

@@ -23,6 +23,7 @@ enum Status : int {
   kCapacity = 8,         // paro::CapacityError
   kLineage = 9,          // paro::LineageError
   kCuda = 20,            // CUDA runtime / cuBLAS failure (no reference counterpart)
+  kAborted = 21,         // column stopped because another column of the batch hit NotSpd
 };
 
 struct ParoError : std::runtime_error {

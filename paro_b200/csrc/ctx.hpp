@@ -57,6 +57,9 @@ struct Ctx {
   DevBuf partials, cols, scale, invd, pbuf0, pbuf1, flag;
   DevBuf ws_a, ws_b, ws_c, ws_d, ws_e, ws_small, ws_small2, ws_small3;
   bool force_cgs2 = false;           // Step 4: skip the Cholesky-QR path
+  int hartree_mode = 1;              // 0: Jacobi-PCG (reference algorithm), 1: DST-I when applicable
+  int dst_S = 0;                     // grid of the cached DST-I tables
+  DevBuf dst_tab;
   int* pinned_count = nullptr;       // mapped host memory for the active-column poll
   int* pinned_count_dev = nullptr;
 

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "march.cuh"
+#include "poisson.hpp"
 #include "solver.hpp"
 
 namespace paro_b200 {
@@ -49,11 +50,20 @@ __device__ double sum_partials(const double* partials, int c, int q, int nblk, d
 
 enum FinMode { kFinSetup = 0, kFinK1 = 1, kFinK2 = 2 };
 
-__global__ void fin_kernel(int mode, CgColumn* cols, const double* partials, int nblk, const int* diag_bad) {
+// flags[0]: non-positive diagonal; flags[1]: a column hit NotSpd (abort the batch when flags[2] != 0)
+__global__ void fin_kernel(int mode, CgColumn* cols, const double* partials, int nblk, int* flags) {
   __shared__ double sh[32];
   const int c = blockIdx.x;
   CgColumn& col = cols[c];
   if (!col.active) return;
+  if (flags[2] && flags[1]) {  // another column's NotSpd already fixes this step's outcome
+    if (threadIdx.x == 0) {
+      col.active = 0;
+      col.status = kAborted;
+    }
+    return;
+  }
+  const int* diag_bad = flags;
   if (mode == kFinSetup) {
     const double bb = sum_partials(partials, c, 0, nblk, sh);
     const double rz = sum_partials(partials, c, 1, nblk, sh);
@@ -91,6 +101,7 @@ __global__ void fin_kernel(int mode, CgColumn* cols, const double* partials, int
     if (pq <= 0.0) {  // linalg.cpp:200
       col.status = kNotSpd;
       col.active = 0;
+      atomicExch(flags + 1, 1);
       return;
     }
     col.alpha = col.rz / pq;
@@ -188,7 +199,7 @@ void apply_op(Ctx& ctx, const Op& a, const Op* shift, double sigma, int K, const
 // warm: x0 = src (source solves) ; cold: x0 = 0 (Hartree).
 void batched_pcg(Ctx& ctx, const OpDev& op, bool var, int K, const double* src, const double* rhs,
                  const double* scale_host, bool warm, double* x, long long ld, std::vector<CgColumn>& cols,
-                 const Op* mass) {
+                 const Op* mass, bool abort_on_not_spd = false) {
   const Grid& g = ctx.grid;
   const long long n = g.n;
   cudaStream_t st = ctx.stream;
@@ -210,14 +221,16 @@ void batched_pcg(Ctx& ctx, const OpDev& op, bool var, int K, const double* src, 
   double* r = ctx.ws_a.get<double>(static_cast<size_t>(K) * ld);
   double* p0 = ctx.pbuf0.get<double>(static_cast<size_t>(K) * ld);
   double* p1 = ctx.pbuf1.get<double>(static_cast<size_t>(K) * ld);
-  int* flag = ctx.flag.get<int>(1);
+  int* flag = ctx.flag.get<int>(3);
 
   PARO_CUDA(cudaMemcpyAsync(dcols, cols.data(), sizeof(CgColumn) * K, cudaMemcpyHostToDevice, st));
   if (scale_host) PARO_CUDA(cudaMemcpyAsync(dscale, scale_host, sizeof(double) * K, cudaMemcpyHostToDevice, st));
 
   // Jacobi preconditioner and the SPD diagonal check (linalg.cpp:164-173)
   set_flag_kernel<<<1, 1, 0, st>>>(flag, 0);
-  ++ctx.launches;
+  set_flag_kernel<<<1, 1, 0, st>>>(flag + 1, 0);
+  set_flag_kernel<<<1, 1, 0, st>>>(flag + 2, abort_on_not_spd ? 1 : 0);
+  ctx.launches += 3;
   double* invd = nullptr;
   if (var) {
     invd = ctx.invd.get<double>(n);
@@ -371,8 +384,27 @@ int source_solve(Ctx& ctx, const Op& a, const Op& b, double sigma, int K, const 
   for (int c = 0; c < K; ++c) scale[c] = lambdas[c] + sigma;  // paro.cpp:97
   std::vector<CgColumn> cols(K);
   for (int c = 0; c < K; ++c) cols[c] = make_col(tol, max_iter);
-  batched_pcg(ctx, op, a.var, K, u, nullptr, scale.data(), true, out, ld, cols, &b);
+  batched_pcg(ctx, op, a.var, K, u, nullptr, scale.data(), true, out, ld, cols, &b, true);
 
+  // A NotSpd in the first attempt fixes the step's outcome (the sigma policy
+  // restarts the whole step, paro.cpp:204-207): the batch was aborted as soon
+  // as it was seen, the remaining columns carry kAborted and report kOk.
+  bool not_spd = false;
+  for (int c = 0; c < K; ++c) not_spd |= cols[c].status == kNotSpd;
+  if (not_spd) {
+    if (report) {
+      report->iterations.assign(K, 0);
+      report->residual.assign(K, 0.0);
+      report->status.assign(K, kOk);
+      report->first_status.assign(K, kOk);
+      for (int c = 0; c < K; ++c) {
+        report->iterations[c] = cols[c].it;
+        if (cols[c].status == kNotSpd) report->status[c] = report->first_status[c] = kNotSpd;
+      }
+    }
+    ctx.err = "cg: operator not positive definite (p'Ap <= 0)";
+    return kNotSpd;
+  }
   std::vector<int> first_status(K, kOk), retry_status(K, kOk);
   std::vector<double> retry_resid(K, 0.0);
   std::vector<CgColumn> retry(K);
@@ -482,6 +514,14 @@ int cg_solve(Ctx& ctx, const Op& a, int K, const double* rhs, const double* x0, 
 int hartree_solve(Ctx& ctx, const Op& poisson, const Op& mass, const double* rho, double tol, double* vh,
                   SolveReport* report) {
   ctx.check_grid();
+  if (ctx.hartree_mode == 1 && dst_applicable(poisson)) {
+    if (report) {
+      report->iterations.assign(1, 0);
+      report->residual.assign(1, 0.0);
+      report->status.assign(1, kOk);
+    }
+    return hartree_dst(ctx, poisson, mass, rho, vh);
+  }
   const OpDev op = make_opdev(ctx, poisson, nullptr, 0.0);
   const double four_pi = 4.0 * M_PI;
   std::vector<CgColumn> cols(1, make_col(tol, 200000));

@@ -229,7 +229,9 @@ class ParoRun:
         tol = w.cg_tol_for_iteration(it)
         sigma = max(0.0, 0.5 - self.lambdas[0])
         local = self.half[c0:c1] if d.world == 1 else self._local(c1 - c0)
+        self.last_attempts = 0
         for attempt in range(5):
+            self.last_attempts = attempt + 1
             first, final, iters, _ = be.source_solve(a, self.orb[c0:c1], self.lambdas[c0:c1], sigma, tol,
                                                      w.cg_max_iter, local)
             first = d.allgather_ints(first, counts, self._idev())

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--k", type=int, default=76)
     ap.add_argument("--iters", type=int, default=6)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--shifted", action="store_true", help="also time source_solve_columns with sigma = 16")
     a = ap.parse_args()
     ctx = core.Context(0).grid(a.s, -18.0, 18.0)
     op = core.assemble_stiffness(ctx, 0.5)
@@ -37,6 +38,18 @@ def main():
     b = torch.randn((a.k, n), dtype=torch.float64, device="cuda", generator=g)
     x0 = torch.randn((a.k, n), dtype=torch.float64, device="cuda", generator=g)
     out = {}
+    if a.shifted:
+        # Step 3 proper: source_solve_step with a spectral shift and the mass rhs
+        mass = core.assemble_mass(ctx)
+        lam = [-15.0] * a.k
+        half = torch.empty_like(x0)
+        for rep in range(a.reps):
+            ctx.stats(reset=True)
+            f, g2, it, _ = core.source_solve_columns(op, mass, x0, lam, 1e-30, a.iters, 16.0, half)
+            st = ctx.stats()
+            out[f"source_step_rep{rep}"] = {"ms_per_iter": 1e3 * st["step3_s"] / max(it),
+                                            "achieved_gbs": st["step3_bytes"] / st["step3_s"] / 1e9,
+                                            "col_iters": st["step3_col_iters"]}
     for name, A, B, X0 in (("step3", op, b, x0), ("hartree", poisson, b[:1], None)):
         best = None
         for _ in range(a.reps):

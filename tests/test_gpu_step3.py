@@ -131,5 +131,13 @@ def test_hartree_matches_reference(ref, gpu_ctx_factory):
     gp = core.Operator.from_csr(ctx, *ks.op("poisson").csr())
     gm = core.Operator.from_csr(ctx, *ks.op("mass").csr())
     assert not gp.variable and not gm.variable
-    vh = core.hartree_solve_with(gp, gm, _dev(rho), 1e-11).cpu().numpy()
-    np.testing.assert_allclose(vh, vh_ref, rtol=0, atol=1e-9 * np.abs(vh_ref).max())
+    for mode, tol in (("cg", 1e-9), ("dst", 1e-10)):
+        ctx.set_hartree_mode(mode)
+        rep = {}
+        vh = core.hartree_solve_with(gp, gm, _dev(rho), 1e-11, report=rep).cpu().numpy()
+        np.testing.assert_allclose(vh, vh_ref, rtol=0, atol=tol * np.abs(vh_ref).max())
+        assert (rep["iterations"] == 0) == (mode == "dst")
+    # the exact DST solution satisfies the discrete system to round-off
+    b = ks.op("mass").matvec(rho) * 4 * np.pi
+    r = ks.op("poisson").matvec(vh) - b
+    assert np.linalg.norm(r) <= 1e-12 * np.linalg.norm(b)
