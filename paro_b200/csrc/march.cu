@@ -8,6 +8,7 @@
 // the next plane. K1 stages the raw r, p_old (and diagonal) planes and
 // transforms them into p_new = z + beta p_old once they land.
 #include <algorithm>
+#include <cstdlib>
 
 #include "march.cuh"
 
@@ -56,9 +57,13 @@ constexpr size_t smem_bytes() {
 
 // 15-point row sum in ascending column order (linalg.cpp:88-94 on the Kuhn
 // pattern). wb[o]: A[v, v-off(o)], wf[o]: A[v, v+off(o)], w0: diagonal.
+// FMA = true (the PCG passes only) contracts each term into one DFMA; the
+// operator apply keeps the reference's separate multiply and add.
+template <bool FMA = false>
 __device__ __forceinline__ double row_sum(const double* __restrict__ Pm, const double* __restrict__ P0,
                                           const double* __restrict__ Pp, int ib, const double (&wb)[kSlots],
                                           double w0, const double (&wf)[kSlots]) {
+  auto madd = [](double s, double w, double x) { return FMA ? fma(w, x, s) : __dadd_rn(s, __dmul_rn(w, x)); };
   double s = 0.0;
   s = madd(s, wb[7], Pm[ib - kHX - 1]);
   s = madd(s, wb[6], Pm[ib - kHX]);
@@ -95,7 +100,7 @@ __device__ __forceinline__ void load_weights(const double* __restrict__ cf, long
 }
 
 template <int MODE, bool VAR, int CB>
-__global__ void __launch_bounds__(kNT, 2) march_kernel(const MarchArgs a) {
+__global__ void __launch_bounds__(kNT, CB <= 2 ? 3 : 2) march_kernel(const MarchArgs a) {
   extern __shared__ __align__(16) double smem[];
   constexpr int NA = Cfg<MODE>::NA;
   constexpr int NR = Cfg<MODE>::NR;
@@ -275,6 +280,14 @@ __global__ void __launch_bounds__(kNT, 2) march_kernel(const MarchArgs a) {
       if (MODE == kK2) issue_xr(z + 1);
     }
     cp_commit();
+    // this plane's operator coefficients: issued before the wait and barrier
+    // below so that their L2 latency overlaps them (profiles/r01: the first
+    // use of these loads was the top stall of both PCG kernels)
+    const int idx = z * S2 + own;
+    double ow[kSlots], bk[kSlots], invd = 0.0;
+    if (VAR && inside) load_weights(a.op.coef, n, idx, gx, gy, z, S, S2, ow, bk);
+    if ((MODE == kK2 || MODE == kSetupWarm || MODE == kSetupCold) && inside)
+      invd = VAR ? __ldg(a.invd + idx) : a.op.invd_const;
     cp_wait<1>();
     __syncthreads();
     if (MODE == kK1) {
@@ -283,12 +296,9 @@ __global__ void __launch_bounds__(kNT, 2) march_kernel(const MarchArgs a) {
     }
 
     if (inside) {
-      const int idx = z * S2 + own;
       // 15 weights of the operator at this point, shifted by sigma*M
       double wb[kSlots], wf[kSlots], w0;
       if (VAR) {
-        double ow[kSlots], bk[kSlots];
-        load_weights(a.op.coef, n, idx, gx, gy, z, S, S2, ow, bk);
         if (a.op.mcoef != nullptr) {  // variable shift stencil (inexact mesh spacing)
           double mown[kSlots], mback[kSlots];
           load_weights(a.op.mcoef, n, idx, gx, gy, z, S, S2, mown, mback);
@@ -315,8 +325,6 @@ __global__ void __launch_bounds__(kNT, 2) march_kernel(const MarchArgs a) {
         w0 = __dadd_rn(a.op.w[0], __dmul_rn(a.op.sigma, a.op.m[0]));
       }
       wb[0] = wf[0] = 0.0;
-      double invd = 0.0;
-      if (MODE == kK2 || MODE == kSetupWarm || MODE == kSetupCold) invd = VAR ? __ldg(a.invd + idx) : a.op.invd_const;
       const double* Pm = ring + rs(z - 1) * CB * kHP;
       const double* P0 = ring + rs(z) * CB * kHP;
       const double* Pp = ring + rs(z + 1) * CB * kHP;
@@ -325,7 +333,7 @@ __global__ void __launch_bounds__(kNT, 2) march_kernel(const MarchArgs a) {
 #pragma unroll
       for (int j = 0; j < CB; ++j) {
         if (!act[j]) continue;
-        const double s = row_sum(Pm + j * kHP, P0 + j * kHP, Pp + j * kHP, ib, wb, w0, wf);
+        const double s = row_sum<MODE == kK1 || MODE == kK2>(Pm + j * kHP, P0 + j * kHP, Pp + j * kHP, ib, wb, w0, wf);
         const double ctr = P0[j * kHP + ib];
         const long long gi = static_cast<long long>(c0 + j) * a.ld + idx;
         if (MODE == kApply) {
@@ -419,6 +427,11 @@ void launch_t(const MarchArgs& a, cudaStream_t st) {
 
 template <int MODE, bool VAR>
 void launch_cb(int cb, const MarchArgs& a, cudaStream_t st) {
+  static const int forced = [] {
+    const char* e = std::getenv("PARO_MARCH_CB");  // experiment knob: column-group width
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced > 0 && cb > forced) cb = forced;
   switch (cb) {
     case 1: launch_t<MODE, VAR, 1>(a, st); break;
     case 2: launch_t<MODE, VAR, 2>(a, st); break;
