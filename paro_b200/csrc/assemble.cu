@@ -44,6 +44,7 @@ struct AsmArgs {
   const double* vext_coef = nullptr;
   double* out = nullptr;
   int* flags = nullptr;      // bit0 singular point hit, bit1 non-finite weight
+  const double* wtab = nullptr;  // 4-point rules: precomputed w(x_q) per (cell, tet, point)
 };
 
 __device__ __forceinline__ double eval_in_element(const double* f, int s, const int (&vtx)[4][3],
@@ -83,6 +84,34 @@ __device__ double weight_at(const AsmArgs& a, const V3 (&P)[4], const int (&vtx)
   const double rho_q = eval_in_element(a.rho, a.box.s, vtx, bary);
   const Lda l = lda_vxc(rho_q, a.exchange_only != 0, a.cx);
   return eval_in_element(a.vh, a.box.s, vtx, bary) + l.v;
+}
+
+// w(x_q) of every (cell, Kuhn tet, quadrature point) of a 4-point rule, each
+// evaluated once (the dof gather below otherwise evaluates it for each of the
+// tet's 4 vertices); same floating-point operations as in the gather.
+__global__ void __launch_bounds__(128) wtable_kernel(const AsmArgs a, double* wtab) {
+  const int s = a.box.s;
+  const long long ncell = static_cast<long long>(s) * s * s;
+  const long long cidx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (cidx >= ncell) return;
+  const int ci = static_cast<int>(cidx % s), cj = static_cast<int>((cidx / s) % s),
+            ck = static_cast<int>(cidx / (static_cast<long long>(s) * s));
+  for (int p = 0; p < 6; ++p) {
+    int tc[4][3];
+    tet_corners(p, tc);
+    int vtx[4][3];
+    V3 P[4];
+    for (int i = 0; i < 4; ++i) {
+      vtx[i][0] = ci + tc[i][0];
+      vtx[i][1] = cj + tc[i][1];
+      vtx[i][2] = ck + tc[i][2];
+      P[i] = V3{a.box.coord(vtx[i][0]), a.box.coord(vtx[i][1]), a.box.coord(vtx[i][2])};
+    }
+    for (int q = 0; q < a.nq; ++q) {
+      const V3 x = quad_point(P, a.qp + 4 * q);
+      wtab[(cidx * 6 + p) * 4 + q] = weight_at(a, P, vtx, x);
+    }
+  }
 }
 
 __global__ void __launch_bounds__(128) assemble_kernel(const AsmArgs a) {
@@ -174,7 +203,9 @@ __global__ void __launch_bounds__(128) assemble_kernel(const AsmArgs a) {
             }
             for (int q = 0; q < nq; ++q) {
               const V3 x = quad_point(P, qp + 4 * q);
-              const double wq = weight_at(a, P, vtx, x);
+              const double wq =
+                  a.wtab ? a.wtab[((((static_cast<long long>(ck) * s) + cj) * s + ci) * 6 + p) * 4 + q]
+                         : weight_at(a, P, vtx, x);
               if (!isfinite(wq)) atomicOr(a.flags, 2);
               const double ww = qw[q] * vol * wq;
               for (int j = 0; j < 4; ++j) {
@@ -284,6 +315,13 @@ void assemble(Ctx& ctx, const AssembleSpec& spec, Op& out) {
     }
     a.vext_coef = spec.vext ? spec.vext->coef : nullptr;
     if (spec.vext && !spec.vext->var) throw ParoError(kInvalidArgument, "ks form: V_ext mass must be variable");
+  }
+  if (wmass && !singular && a.nq == 4) {
+    const long long ncell = static_cast<long long>(g.s) * g.s * g.s;
+    double* wt = ctx.wtab.get<double>(static_cast<size_t>(ncell) * 24);
+    wtable_kernel<<<static_cast<unsigned>((ncell + 127) / 128), 128, 0, ctx.stream>>>(a, wt);
+    ++ctx.launches;
+    a.wtab = wt;
   }
   const long long blocks = (g.n + 127) / 128;
   assemble_kernel<<<static_cast<unsigned>(blocks), 128, 0, ctx.stream>>>(a);

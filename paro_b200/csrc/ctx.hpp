@@ -60,6 +60,7 @@ struct Ctx {
   int hartree_mode = 1;              // 0: Jacobi-PCG (reference algorithm), 1: DST-I when applicable
   int dst_S = 0;                     // grid of the cached DST-I tables
   DevBuf dst_tab;
+  DevBuf wtab;                       // assembly: per-(cell, tet, point) weight values
   int* pinned_count = nullptr;       // mapped host memory for the active-column poll
   int* pinned_count_dev = nullptr;
 
