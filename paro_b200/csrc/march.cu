@@ -32,6 +32,14 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// read-only load pinned in program order (volatile asm is not moved across
+// the pipeline wait / barrier, so its latency overlaps them)
+__device__ __forceinline__ double ldnc(const double* p) {
+  double v;
+  asm volatile("ld.global.f64 %0, [%1];\n" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
@@ -410,8 +418,390 @@ __global__ void __launch_bounds__(kNT, CB <= 2 ? 3 : 2) march_kernel(const March
   }
 }
 
+// ---------------------------------------------------------------------------
+// v3 (Apply, K1, K2): streaming row sums. The 15 stencil points of row z lie
+// on planes z-1 (4 points), z (7) and z+1 (4), and the union of the in-plane
+// offsets a thread touches on one plane over its three uses is the 7 points
+// of the centre pattern. So when plane t lands, each thread reads those 7
+// values once per column and adds them to three running sums: the Pm terms
+// of row t+1, the centre terms of row t and the Pp terms of row t-1, which
+// is then complete. Planes arrive in ascending z, so every row is still
+// summed term by term in ascending column order (the same operation sequence
+// as row_sum), with 7 shared-memory reads per point-column instead of 15 and
+// one barrier per plane.
+template <int MODE, int CB>
+constexpr size_t stream_smem() {
+  size_t d = static_cast<size_t>(MODE == kK1 ? 2 : 3) * CB * kHP;           // stencil-source ring
+  if (MODE == kK2) d += static_cast<size_t>(3) * CB * 2 * kNT;              // own x, r stages
+  if (MODE == kK1) d += static_cast<size_t>(3) * (2 * CB + 1) * kHP;        // raw r, p_old, invd stages
+  return d * sizeof(double);
+}
+
+template <int MODE, bool VAR, int CB>
+__global__ void __launch_bounds__(kNT, CB <= 2 ? 3 : 2) stream_kernel(const MarchArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  constexpr int NR = MODE == kK1 ? 2 : 3;
+  constexpr int NA = MODE == kK2 ? 2 : 1;
+  constexpr bool FMA = MODE != kApply;
+  __shared__ double red[kNT / 32][CB * NA];
+
+  double* ring = smem;                    // [NR][CB][kHP]
+  double* stage = ring + NR * CB * kHP;   // K2: [3][CB][2][kNT]; K1: raw [3][2CB+1][kHP]
+
+  const int S = a.S;
+  const int S2 = S * S;
+  const long long n = a.n;
+  const int tid = threadIdx.x;
+  const int b = blockIdx.y;
+  const int c0 = blockIdx.x * CB;
+
+  unsigned actm = 0, firstm = 0;  // per-column bits: active, first PCG iteration
+  double colA[CB], colB[CB];
+#pragma unroll
+  for (int j = 0; j < CB; ++j) {
+    const int c = c0 + j;
+    const bool on = c < a.K && (a.cols == nullptr || a.cols[c].active != 0);
+    colA[j] = colB[j] = 0.0;
+    if (on) {
+      actm |= 1u << j;
+      if (MODE == kK1) {
+        colB[j] = a.cols[c].beta;
+        if (a.cols[c].first != 0) firstm |= 1u << j;
+      }
+      if (MODE == kK2) colA[j] = a.cols[c].alpha;
+    }
+  }
+  if (actm == 0) return;
+  auto act = [&](int j) { return (actm >> j) & 1u; };
+  auto first = [&](int j) { return (firstm >> j) & 1u; };
+
+  const int bx = b % a.nTX;
+  const int by = (b / a.nTX) % a.nTY;
+  const int bz = b / (a.nTX * a.nTY);
+  const int x0 = bx * kTX, y0 = by * kTY;
+  const int z0 = bz * a.ZC;
+  const int z1 = min(S, z0 + a.ZC);
+  const int tx = tid % kTX, ty = tid / kTX;
+  const int gx = x0 + tx, gy = y0 + ty;
+  const bool inside = gx < S && gy < S;
+  const int own = gy * S + gx;
+
+  int pos[kLoadsPerThread], roff[kLoadsPerThread];
+  bool pval[kLoadsPerThread], pown[kLoadsPerThread];
+#pragma unroll
+  for (int l = 0; l < kLoadsPerThread; ++l) {
+    const int i = tid + l * kNT;
+    pos[l] = i;
+    const int hx = i % kHX, hy = i / kHX;
+    const int px = x0 + hx - 1, py = y0 + hy - 1;
+    pval[l] = i < kHP && px >= 0 && px < S && py >= 0 && py < S;
+    pown[l] = pval[l] && hx >= 1 && hx <= kTX && hy >= 1 && hy <= kTY;
+    roff[l] = pval[l] ? py * S + px : 0;
+  }
+
+  // column-group base pointers (uniform); per-thread offsets stay 32-bit
+  const long long ld = a.ld;
+  const long long cbase = static_cast<long long>(c0) * ld;
+  // in-plane offset of halo position l on plane z (0 where zero-filled)
+  auto hoff = [&](int l, bool zin, int zoff) { return zin && pval[l] ? zoff + roff[l] : 0; };
+
+  // stencil-source plane z -> ring slot `slot` (Apply, K2)
+  auto issue_plane = [&](int z, int slot) {
+    const bool zin = z >= 0 && z < S;
+    const int zoff = z * S2;
+    double* dst = ring + slot * CB * kHP;
+#pragma unroll
+    for (int l = 0; l < kLoadsPerThread; ++l) {
+      if (pos[l] >= kHP) continue;
+      const bool v = zin && pval[l];
+      const double* q = a.src + cbase + hoff(l, zin, zoff);
+#pragma unroll
+      for (int j = 0; j < CB; ++j) {
+        if (act(j)) cp8(dst + j * kHP + pos[l], q, v);
+        q += ld;
+      }
+    }
+  };
+  // K1: raw planes r, p_old (+ inverse diagonal) -> raw stage `slot`
+  auto issue_raw = [&](int z, int slot) {
+    const bool zin = z >= 0 && z < S;
+    const int zoff = z * S2;
+    double* rw = stage + slot * (2 * CB + 1) * kHP;
+#pragma unroll
+    for (int l = 0; l < kLoadsPerThread; ++l) {
+      if (pos[l] >= kHP) continue;
+      const bool v = zin && pval[l];
+      const int off = hoff(l, zin, zoff);
+      const double* qr = a.r + cbase + off;
+      const double* qp = a.pold + cbase + off;
+#pragma unroll
+      for (int j = 0; j < CB; ++j) {
+        if (act(j)) {
+          cp8(rw + j * kHP + pos[l], qr, v);
+          if (!first(j)) cp8(rw + (CB + j) * kHP + pos[l], qp, v);
+        }
+        qr += ld;
+        qp += ld;
+      }
+      if (VAR) cp8(rw + 2 * CB * kHP + pos[l], a.invd + off, v);
+    }
+  };
+  // K1: raw stage `rslot_` of plane z -> p_new = z + beta p_old in ring slot
+  // (z - z0 + 1) & 1; own points also to global
+  auto transform = [&](int z, int rslot_) {
+    const double* rw = stage + rslot_ * (2 * CB + 1) * kHP;
+    double* slot = ring + ((z - z0 + 1) & 1) * CB * kHP;
+    const bool zown = z >= z0 && z < z1;
+    const int zoff = z * S2;
+#pragma unroll
+    for (int l = 0; l < kLoadsPerThread; ++l) {
+      if (pos[l] >= kHP) continue;
+      const double d = VAR ? rw[2 * CB * kHP + pos[l]] : (pval[l] ? a.op.invd_const : 0.0);
+      const bool wr = zown && pown[l];
+      double* q = a.dst + cbase + (zoff + roff[l]);
+#pragma unroll
+      for (int j = 0; j < CB; ++j) {
+        if (act(j)) {
+          // z = inv_diag * r ; p = z + beta * p   (linalg.cpp:179, 210)
+          const double zz = __dmul_rn(d, rw[j * kHP + pos[l]]);
+          const double v = first(j) ? zz : __dadd_rn(zz, __dmul_rn(colB[j], rw[(CB + j) * kHP + pos[l]]));
+          slot[j * kHP + pos[l]] = v;
+          if (wr) *q = v;
+        }
+        q += ld;
+      }
+    }
+  };
+  // K2: own-point x, r of row z -> stage `slot`
+  auto issue_xr = [&](int z, int slot) {
+    if (!inside || z < z0 || z >= z1) return;
+    double* st = stage + slot * CB * 2 * kNT;
+    const long long off = cbase + z * S2 + own;
+    const double* qx = a.x + off;
+    const double* qr = a.r + off;
+#pragma unroll
+    for (int j = 0; j < CB; ++j) {
+      if (act(j)) {
+        cp8(st + (j * 2 + 0) * kNT + tid, qx, true);
+        cp8(st + (j * 2 + 1) * kNT + tid, qr, true);
+      }
+      qx += ld;
+      qr += ld;
+    }
+  };
+  auto madd = [](double s, double w, double x) { return FMA ? fma(w, x, s) : __dadd_rn(s, __dmul_rn(w, x)); };
+  // Coefficient offsets relative to a point of plane t: back slot o of row
+  // t (o = 1..3) and of row t+1 (o = 4..7) lie in plane t at -(ox + oy S);
+  // own slots 0..3 of row t in plane t, own 4..7 of row t-1 in plane t-1.
+  // Loads are unconditional (planes clamped into the lattice): a back weight
+  // whose neighbour leaves the lattice multiplies a zero-filled plane value,
+  // and a row sum that starts at +0 is unchanged by adding +-0 in
+  // round-to-nearest, so the row sums equal the CSR ones bit for bit.
+  long long offB[kSlots], offF[kSlots];
+#pragma unroll
+  for (int o = 0; o < kSlots; ++o) {
+    offF[o] = o * n;
+    offB[o] = o * n - (o & 1) - ((o >> 1) & 1) * S;
+  }
+
+  double sC[CB], sN[CB], cCur[CB];  // row t partial, row t+1 partial, centre value of plane t
+  double acc[CB][NA];
+#pragma unroll
+  for (int j = 0; j < CB; ++j) {
+    sC[j] = sN[j] = cCur[j] = 0.0;
+#pragma unroll
+    for (int q = 0; q < NA; ++q) acc[j][q] = 0.0;
+  }
+
+  // prologue
+  if (MODE == kK1) {
+    issue_raw(z0 - 1, 0);
+    cp_commit();
+    issue_raw(z0, 1);
+    cp_commit();
+    issue_raw(z0 + 1, 2);
+    cp_commit();
+    cp_wait<2>();
+    __syncthreads();
+    transform(z0 - 1, 0);
+  } else {
+    issue_plane(z0 - 1, 0);
+    cp_commit();
+    issue_plane(z0, 1);
+    cp_commit();
+  }
+
+  const int ib = (ty + 1) * kHX + (tx + 1);
+  const int ownc = inside ? own : 0;
+  int s0 = 0;  // rslot(t); rslot(t+1) = s1, rslot(t-1) = rslot(t+2) = s2
+  for (int t = z0 - 1; t <= z1; ++t, s0 = s0 == 2 ? 0 : s0 + 1) {
+    const int s1 = s0 == 2 ? 0 : s0 + 1;
+    const int s2 = s1 == 2 ? 0 : s1 + 1;
+    const bool rowP = t - 1 >= z0;  // row t-1 completes at this step
+    // this step's coefficients, issued before the pipeline wait
+    double cN[4], cC[7], cPp[4], invdP = 0.0;
+    if (VAR) {
+      const long long pt = static_cast<long long>(min(max(t, 0), S - 1)) * S2 + ownc;
+      const long long pm = static_cast<long long>(max(t - 1, 0)) * S2 + ownc;
+      const double* cf = a.op.coef;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cN[i] = ldnc(cf + pt + offB[4 + i]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) cC[i] = ldnc(cf + pt + offB[1 + i]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cC[3 + i] = ldnc(cf + pt + offF[i]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cPp[i] = ldnc(cf + pm + offF[4 + i]);
+      if (MODE == kK2) invdP = ldnc(a.invd + pm);
+    }
+    if (!VAR && MODE == kK2) invdP = a.op.invd_const;
+
+    cp_wait<1>();
+    __syncthreads();
+    if (MODE == kK1) {
+      if (t + 3 <= z1) issue_raw(t + 3, s0);  // rslot(t+3) = rslot(t)
+    } else {
+      if (t + 2 <= z1) issue_plane(t + 2, s2);
+      if (MODE == kK2) issue_xr(t + 1, s1);
+    }
+    cp_commit();
+
+    if (inside) {
+      // shifted weights of the three rows touched by plane t
+      double wN[4], wC[7], wP[4];
+      if (VAR) {  // constant shift: fl(c + sm[o]) with sm = fl(sigma m[o]) from the host
+#pragma unroll
+        for (int i = 0; i < 4; ++i) wN[i] = __dadd_rn(cN[i], a.op.sm[4 + i]);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) wC[i] = __dadd_rn(cC[i], a.op.sm[1 + i]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) wC[3 + i] = __dadd_rn(cC[3 + i], a.op.sm[i]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) wP[i] = __dadd_rn(cPp[i], a.op.sm[4 + i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) wN[i] = a.op.wc[4 + i];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) wC[i] = a.op.wc[1 + i];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) wC[3 + i] = a.op.wc[i];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) wP[i] = a.op.wc[4 + i];
+      }
+      const double* P = ring + (MODE == kK1 ? ((t - z0 + 1) & 1) : s0) * CB * kHP;
+      const double* st = stage + (MODE == kK2 ? s2 : 0) * CB * 2 * kNT;
+      const int u = t - 1;
+#pragma unroll
+      for (int j = 0; j < CB; ++j) {
+        if (!act(j)) continue;
+        const double* Pj = P + j * kHP;
+        const double vmm = Pj[ib - kHX - 1], v0m = Pj[ib - kHX], vm0 = Pj[ib - 1], v00 = Pj[ib];
+        const double vp0 = Pj[ib + 1], v0p = Pj[ib + kHX], vpp = Pj[ib + kHX + 1];
+        if (rowP) {  // Pp terms of row t-1: A[v, v+o], o = 4..7
+          double s = sC[j];
+          s = madd(s, wP[0], v00);
+          s = madd(s, wP[1], vp0);
+          s = madd(s, wP[2], v0p);
+          s = madd(s, wP[3], vpp);
+          const double ctr = cCur[j];  // p (or x) at row t-1
+          const long long gi = static_cast<long long>(c0 + j) * a.ld + (u * S2 + own);
+          if (MODE == kApply) {
+            a.dst[gi] = s;
+            acc[j][0] += ctr * s;
+          } else if (MODE == kK1) {
+            acc[j][0] += ctr * s;  // p'q
+          } else {
+            // x += alpha p ; r -= alpha q ; z = invd r  (linalg.cpp:202-206)
+            const double al = colA[j];
+            const double xn = __dadd_rn(st[(j * 2 + 0) * kNT + tid], __dmul_rn(al, ctr));
+            const double rn = __dsub_rn(st[(j * 2 + 1) * kNT + tid], __dmul_rn(al, s));
+            a.x[gi] = xn;
+            a.r[gi] = rn;
+            const double zz = __dmul_rn(invdP, rn);
+            acc[j][0] += rn * zz;
+            acc[j][1] += rn * rn;
+          }
+        }
+        // centre terms of row t (back 3..1, diagonal, forward 1..3) and Pm
+        // terms of row t+1 (back 7..4); computed unconditionally, a row
+        // outside [z0, z1) is never completed
+        double c = sN[j];
+        {
+          c = madd(c, wC[2], vmm);
+          c = madd(c, wC[1], v0m);
+          c = madd(c, wC[0], vm0);
+          c = madd(c, wC[3], v00);
+          c = madd(c, wC[4], vp0);
+          c = madd(c, wC[5], v0p);
+          c = madd(c, wC[6], vpp);
+        }
+        double nx = 0.0;
+        {
+          nx = madd(nx, wN[3], vmm);
+          nx = madd(nx, wN[2], v0m);
+          nx = madd(nx, wN[1], vm0);
+          nx = madd(nx, wN[0], v00);
+        }
+        sC[j] = c;
+        sN[j] = nx;
+        cCur[j] = v00;
+      }
+    }
+    if (MODE == kK1 && t + 1 <= z1) transform(t + 1, s1);
+  }
+  cp_wait<0>();
+
+  if (MODE == kApply && !a.with_dot) return;
+  const int warp = tid >> 5, lane = tid & 31;
+#pragma unroll
+  for (int j = 0; j < CB; ++j)
+#pragma unroll
+    for (int q = 0; q < NA; ++q) {
+      const double v = warp_sum(acc[j][q]);
+      if (lane == 0) red[warp][j * NA + q] = v;
+    }
+  __syncthreads();
+  if (tid < CB * NA) {
+    const int j = tid / NA, q = tid % NA;
+    if (act(j)) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kNT / 32; ++w) s += red[w][tid];
+      a.partials[(static_cast<long long>(c0 + j) * 3 + q) * a.nblk + b] = s;
+    }
+  }
+}
+
+template <int MODE, bool VAR, int CB>
+void launch_s(const MarchArgs& a, cudaStream_t st) {
+  const int groups = (a.K + CB - 1) / CB;
+  constexpr size_t sm = stream_smem<MODE, CB>();
+  static bool configured = false;
+  if (!configured) {
+    PARO_CUDA(cudaFuncSetAttribute(stream_kernel<MODE, VAR, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(sm)));
+    configured = true;
+  }
+  dim3 grid(groups, a.nblk);
+  stream_kernel<MODE, VAR, CB><<<grid, kNT, sm, st>>>(a);
+  PARO_CUDA(cudaGetLastError());
+}
+
+bool use_v2() {
+  static const bool v2 = [] {
+    const char* e = std::getenv("PARO_MARCH_V2");  // experiment knob: previous kernel generation
+    return e && e[0] == '1';
+  }();
+  return v2;
+}
+
 template <int MODE, bool VAR, int CB>
 void launch_t(const MarchArgs& a, cudaStream_t st) {
+  if constexpr (MODE == kApply || MODE == kK1 || MODE == kK2) {
+    // the streaming kernel takes a constant shift stencil; a variable one
+    // (inexact mesh spacing) stays on the v2 kernel
+    if (!use_v2() && a.op.mcoef == nullptr) return launch_s<MODE, VAR, CB>(a, st);
+  }
   const int groups = (a.K + CB - 1) / CB;
   constexpr size_t sm = smem_bytes<MODE, CB>();
   static bool configured = false;

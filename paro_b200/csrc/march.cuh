@@ -44,6 +44,8 @@ struct OpDev {
   const double* mcoef = nullptr; // variable shift stencil (SoA), overrides m[]
   double sigma = 0.0;            // add_scaled(b, sigma): fl(w + fl(sigma*m))
   double invd_const = 0.0;       // 1/diag for the constant case
+  double sm[kSlots] = {};        // fl(sigma * m[o]), host-computed (constant shift)
+  double wc[kSlots] = {};        // fl(w[o] + sm[o]): the shifted constant operator
 };
 
 struct MarchArgs {

@@ -173,6 +173,12 @@ OpDev make_opdev(const Ctx& ctx, const Op& a, const Op* shift, double sigma) {
     d.sigma = sigma;
   }
   if (!a.var) d.invd_const = 1.0 / (a.w[0] + d.sigma * d.m[0]);
+  // the same two roundings the kernels would apply per point: fl(w + fl(sigma m))
+  for (int o = 0; o < kSlots; ++o) {
+    const double sm = d.sigma * d.m[o];
+    d.sm[o] = sm;
+    d.wc[o] = d.w[o] + sm;
+  }
   (void)ctx;
   return d;
 }
