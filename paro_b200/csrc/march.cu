@@ -634,15 +634,13 @@ __global__ void __launch_bounds__(kNT, CB <= 2 ? 3 : 2) stream_kernel(const Marc
   const int ib = (ty + 1) * kHX + (tx + 1);
   const int ownc = inside ? own : 0;
   int s0 = 0;  // rslot(t); rslot(t+1) = s1, rslot(t-1) = rslot(t+2) = s2
-  for (int t = z0 - 1; t <= z1; ++t, s0 = s0 == 2 ? 0 : s0 + 1) {
-    const int s1 = s0 == 2 ? 0 : s0 + 1;
-    const int s2 = s1 == 2 ? 0 : s1 + 1;
-    const bool rowP = t - 1 >= z0;  // row t-1 completes at this step
-    // this step's coefficients, issued before the pipeline wait
-    double cN[4], cC[7], cPp[4], invdP = 0.0;
+  // coefficients of step t (planes t and t-1), loaded one step ahead so their
+  // L2/DRAM latency overlaps the previous step's compute
+  double cN[4], cC[7], cPp[4], invdP = 0.0;
+  auto load_coefs = [&](int t) {
     if (VAR) {
       const long long pt = static_cast<long long>(min(max(t, 0), S - 1)) * S2 + ownc;
-      const long long pm = static_cast<long long>(max(t - 1, 0)) * S2 + ownc;
+      const long long pm = static_cast<long long>(min(max(t - 1, 0), S - 1)) * S2 + ownc;
       const double* cf = a.op.coef;
 #pragma unroll
       for (int i = 0; i < 4; ++i) cN[i] = ldnc(cf + pt + offB[4 + i]);
@@ -655,6 +653,12 @@ __global__ void __launch_bounds__(kNT, CB <= 2 ? 3 : 2) stream_kernel(const Marc
       if (MODE == kK2) invdP = ldnc(a.invd + pm);
     }
     if (!VAR && MODE == kK2) invdP = a.op.invd_const;
+  };
+  load_coefs(z0 - 1);
+  for (int t = z0 - 1; t <= z1; ++t, s0 = s0 == 2 ? 0 : s0 + 1) {
+    const int s1 = s0 == 2 ? 0 : s0 + 1;
+    const int s2 = s1 == 2 ? 0 : s1 + 1;
+    const bool rowP = t - 1 >= z0;  // row t-1 completes at this step
 
     cp_wait<1>();
     __syncthreads();
@@ -669,15 +673,13 @@ __global__ void __launch_bounds__(kNT, CB <= 2 ? 3 : 2) stream_kernel(const Marc
     if (inside) {
       // shifted weights of the three rows touched by plane t
       double wN[4], wC[7], wP[4];
-      if (VAR) {  // constant shift: fl(c + sm[o]) with sm = fl(sigma m[o]) from the host
+      if (VAR) {  // coefficients of (A + sigma M), the shift folded in by preshift()
 #pragma unroll
-        for (int i = 0; i < 4; ++i) wN[i] = __dadd_rn(cN[i], a.op.sm[4 + i]);
+        for (int i = 0; i < 4; ++i) wN[i] = cN[i];
 #pragma unroll
-        for (int i = 0; i < 3; ++i) wC[i] = __dadd_rn(cC[i], a.op.sm[1 + i]);
+        for (int i = 0; i < 7; ++i) wC[i] = cC[i];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) wC[3 + i] = __dadd_rn(cC[3 + i], a.op.sm[i]);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) wP[i] = __dadd_rn(cPp[i], a.op.sm[4 + i]);
+        for (int i = 0; i < 4; ++i) wP[i] = cPp[i];
       } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i) wN[i] = a.op.wc[4 + i];
@@ -748,6 +750,7 @@ __global__ void __launch_bounds__(kNT, CB <= 2 ? 3 : 2) stream_kernel(const Marc
       }
     }
     if (MODE == kK1 && t + 1 <= z1) transform(t + 1, s1);
+    if (t < z1) load_coefs(t + 1);
   }
   cp_wait<0>();
 
@@ -800,7 +803,10 @@ void launch_t(const MarchArgs& a, cudaStream_t st) {
   if constexpr (MODE == kApply || MODE == kK1 || MODE == kK2) {
     // the streaming kernel takes a constant shift stencil; a variable one
     // (inexact mesh spacing) stays on the v2 kernel
-    if (!use_v2() && a.op.mcoef == nullptr) return launch_s<MODE, VAR, CB>(a, st);
+    if (!use_v2() && a.op.mcoef == nullptr) {
+      if (VAR && a.op.sigma != 0.0) throw ParoError(kInvalidArgument, "march: shifted variable operator not preshifted");
+      return launch_s<MODE, VAR, CB>(a, st);
+    }
   }
   const int groups = (a.K + CB - 1) / CB;
   constexpr size_t sm = smem_bytes<MODE, CB>();

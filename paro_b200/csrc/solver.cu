@@ -157,6 +157,40 @@ __global__ void invd_kernel(const double* c0, double sigma, double m0, const dou
 
 __global__ void set_flag_kernel(int* flag, int v) { *flag = v; }
 
+struct Slots8 {
+  double v[kSlots];
+};
+
+// out[o][i] = fl(coef[o][i] + sm[o]), sm[o] = fl(sigma m[o])
+__global__ void preshift_kernel(const double* __restrict__ coef, Slots8 sm, long long n, double* __restrict__ out) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+#pragma unroll
+    for (int o = 0; o < kSlots; ++o) out[o * n + i] = __dadd_rn(coef[o * n + i], sm.v[o]);
+  }
+}
+
+// Fold a constant shift into a variable operator: (A + sigma M) as 8 SoA
+// arrays in ctx.shifted, each slot the same fl(c + fl(sigma m)) the kernels
+// would otherwise form per point, so the stencil passes read it directly.
+OpDev preshift(Ctx& ctx, OpDev d) {
+  if (d.coef == nullptr || d.mcoef != nullptr || d.sigma == 0.0) return d;
+  const long long n = ctx.grid.n;
+  double* out = ctx.shifted.get<double>(static_cast<size_t>(kSlots) * n);
+  Slots8 sm;
+  for (int o = 0; o < kSlots; ++o) sm.v[o] = d.sm[o];
+  preshift_kernel<<<148 * 8, 256, 0, ctx.stream>>>(d.coef, sm, n, out);
+  PARO_CUDA(cudaGetLastError());
+  ++ctx.launches;
+  d.coef = out;
+  d.sigma = 0.0;
+  for (int o = 0; o < kSlots; ++o) {
+    d.sm[o] = 0.0;
+    d.wc[o] = d.w[o];
+  }
+  return d;
+}
+
 int pick_cb(int K) { return K >= 8 ? 8 : K >= 4 ? 4 : K >= 2 ? 2 : 1; }
 
 }  // namespace
@@ -193,7 +227,7 @@ void apply_op(Ctx& ctx, const Op& a, const Op* shift, double sigma, int K, const
   plan_march(m, ctx.grid.S);
   m.K = K;
   m.ld = ldx;
-  m.op = make_opdev(ctx, a, shift, sigma);
+  m.op = preshift(ctx, make_opdev(ctx, a, shift, sigma));
   m.src = x;
   m.dst = y;
   launch_march(kApply, a.var, pick_cb(K), m, ctx.stream);
@@ -203,9 +237,10 @@ void apply_op(Ctx& ctx, const Op& a, const Op* shift, double sigma, int K, const
 // Core batched PCG. On entry `cols` (host) holds tol/max_iter per column; the
 // setup pass computes r0 from either (M src)*scale (rhs == nullptr) or rhs.
 // warm: x0 = src (source solves) ; cold: x0 = 0 (Hartree).
-void batched_pcg(Ctx& ctx, const OpDev& op, bool var, int K, const double* src, const double* rhs,
+void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* src, const double* rhs,
                  const double* scale_host, bool warm, double* x, long long ld, std::vector<CgColumn>& cols,
                  const Op* mass, bool abort_on_not_spd = false) {
+  const OpDev op = preshift(ctx, op_in);
   const Grid& g = ctx.grid;
   const long long n = g.n;
   cudaStream_t st = ctx.stream;
