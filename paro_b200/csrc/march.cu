@@ -377,14 +377,16 @@ __global__ void __launch_bounds__(kNT, CB <= 2 ? 3 : 2) march_kernel(const March
             bb = __dmul_rn(msum, colA[j]);
           }
           double rr;
+          // x, r may live in the solver's padded buffers (stride ldw)
+          const long long gw = a.ldw ? static_cast<long long>(c0 + j) * a.ldw + idx : gi;
           if (MODE == kSetupWarm) {
             rr = __dsub_rn(bb, s);  // r = b - A x0 (linalg.cpp:184-185)
-            a.x[gi] = ctr;          // x = x0
+            a.x[gw] = ctr;          // x = x0
           } else {
             rr = bb;                // x0 = 0: A x0 = 0, r = b
-            a.x[gi] = 0.0;
+            a.x[gw] = 0.0;
           }
-          a.dst[gi] = rr;
+          a.dst[gw] = rr;
           const double zz = __dmul_rn(invd, rr);
           acc[j][0] += bb * bb;
           acc[j][1] += rr * zz;

@@ -69,9 +69,16 @@ struct MarchArgs {
   const double* rhs = nullptr;   // Setup (warm): explicit right-hand side instead of (M u)*scale
   double* partials = nullptr;    // [K][3][nblk]
   int with_dot = 0;              // Apply: accumulate x.y
+  long long ldw = 0;             // Setup: stride of the x, r outputs (0: ld)
+  int bulk = 0;                  // K1/K2: operands in padded solver buffers -> bulk-copy kernel
 };
 
 void launch_march(int mode, bool var, int cb, const MarchArgs& a, cudaStream_t st);
+// K1/K2 on padded solver buffers (bulk.cu): every vector operand is 16-byte
+// aligned, has an even column stride and at least kBulkPad readable elements
+// before its first and after its last column.
+constexpr long long kBulkPad = 64;
+void launch_bulk(int mode, bool var, int cb, const MarchArgs& a, cudaStream_t st);
 void plan_march(MarchArgs& a, int S);
 
 }  // namespace paro_b200

@@ -259,9 +259,25 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
   CgColumn* dcols = ctx.cols.get<CgColumn>(K);
   double* dscale = ctx.scale.get<double>(K);
   double* partials = ctx.partials.get<double>(static_cast<size_t>(K) * 3 * m.nblk);
-  double* r = ctx.ws_a.get<double>(static_cast<size_t>(K) * ld);
-  double* p0 = ctx.pbuf0.get<double>(static_cast<size_t>(K) * ld);
-  double* p1 = ctx.pbuf1.get<double>(static_cast<size_t>(K) * ld);
+  // the iteration vectors live in padded solver buffers (even stride ldi,
+  // kBulkPad readable margins) that the bulk-copy PCG kernels require; x is
+  // copied back to the caller's layout at the end
+  const long long ldi = ((n + 2 * kBulkPad + 31) / 32) * 32;
+  auto padded = [&](DevBuf& buf, int cols) {
+    return buf.get<double>(static_cast<size_t>(cols) * ldi + 2 * kBulkPad) + kBulkPad;
+  };
+  double* r = padded(ctx.ws_a, K);
+  double* p0 = padded(ctx.pbuf0, K);
+  double* p1 = padded(ctx.pbuf1, K);
+  double* xi = padded(ctx.pcg_x, K);
+  // margins and column gaps are read as halo of the first/last points of a
+  // row and must hold finite values (they meet zero weights)
+  auto zero_margins = [&](double* v, int cols, long long len) {
+    PARO_CUDA(cudaMemsetAsync(v - kBulkPad, 0, sizeof(double) * kBulkPad, st));
+    PARO_CUDA(cudaMemset2DAsync(v + len, sizeof(double) * ldi, 0, sizeof(double) * (ldi - len), cols, st));
+    PARO_CUDA(cudaMemsetAsync(v + static_cast<long long>(cols) * ldi, 0, sizeof(double) * kBulkPad, st));
+  };
+  for (double* v : {r, p0, p1, xi}) zero_margins(v, K, n);
   int* flag = ctx.flag.get<int>(3);
 
   PARO_CUDA(cudaMemcpyAsync(dcols, cols.data(), sizeof(CgColumn) * K, cudaMemcpyHostToDevice, st));
@@ -274,7 +290,8 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
   ctx.launches += 3;
   double* invd = nullptr;
   if (var) {
-    invd = ctx.invd.get<double>(n);
+    invd = padded(ctx.invd, 1);
+    zero_margins(invd, 1, n);
     invd_kernel<<<148 * 8, 256, 0, st>>>(op.coef, op.sigma, op.m[0], op.mcoef, n, invd, flag);
     ++ctx.launches;
   } else {
@@ -289,31 +306,42 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
   // setup: r0, x0, bnorm, rz0, rnorm0
   m.src = src;
   m.dst = r;
-  m.x = x;
+  m.x = xi;
+  m.ldw = ldi;
   m.scale = dscale;
   m.rhs = rhs;
   launch_march(warm ? kSetupWarm : kSetupCold, var, cb, m, st);
   fin_kernel<<<K, kFinThreads, 0, st>>>(kFinSetup, dcols, partials, m.nblk, flag);
-  zero_marked_kernel<<<dim3(148, K), 256, 0, st>>>(dcols, K, x, ld, n);
+  zero_marked_kernel<<<dim3(148, K), 256, 0, st>>>(dcols, K, xi, ldi, n);
   ctx.launches += 3;
   PARO_CUDA(cudaGetLastError());
 
   // iteration chunks captured once into a CUDA graph (PARO_NO_GRAPH=1 launches
   // them directly, e.g. for ncu)
   const int chunk = n >= (1 << 22) ? 4 : n >= (1 << 18) ? 8 : 16;  // even: ping-pong parity repeats
+  static const bool k1_bulk = [] {
+    const char* e = std::getenv("PARO_K1_BULK");  // experiment knob
+    return e && e[0] == '1';
+  }();
   auto enqueue_chunk = [&](cudaStream_t s) {
     for (int it = 0; it < chunk; ++it) {
       MarchArgs k1 = m;
+      k1.ld = ldi;
       k1.pold = (it & 1) ? p1 : p0;
       k1.dst = (it & 1) ? p0 : p1;
       k1.r = r;
-      launch_march(kK1, var, cb, k1, s);
+      // K1 stays on the LDGSTS streaming kernel (faster than its bulk-copy
+      // variant, profiles/r01b); K2 takes the bulk-copy kernel
+      if (op.mcoef || !k1_bulk) launch_march(kK1, var, cb, k1, s);
+      else launch_bulk(kK1, var, cb, k1, s);
       fin_kernel<<<K, kFinThreads, 0, s>>>(kFinK1, dcols, partials, m.nblk, flag);
       MarchArgs k2 = m;
+      k2.ld = ldi;
       k2.src = k1.dst;
-      k2.x = x;
+      k2.x = xi;
       k2.r = r;
-      launch_march(kK2, var, cb, k2, s);
+      if (op.mcoef || K < 4) launch_march(kK2, var, cb, k2, s);  // narrow batches: LDGSTS kernel
+      else launch_bulk(kK2, var, cb, k2, s);
       fin_kernel<<<K, kFinThreads, 0, s>>>(kFinK2, dcols, partials, m.nblk, flag);
     }
     count_active_kernel<<<1, 256, 0, s>>>(dcols, K, ctx.pinned_count_dev);
@@ -393,6 +421,10 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
   if (graph) PARO_CUDA(cudaGraphDestroy(graph));
   std::vector<CgColumn> before = cols;
   PARO_CUDA(cudaMemcpy(cols.data(), dcols, sizeof(CgColumn) * K, cudaMemcpyDeviceToHost));
+  for (int c = 0; c < K; ++c)
+    if (before[c].active)
+      PARO_CUDA(cudaMemcpyAsync(x + c * ld, xi + c * ldi, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  PARO_CUDA(cudaStreamSynchronize(st));
   double col_iters = 0.0, batch_iters = 0.0;
   for (int c = 0; c < K; ++c)
     if (before[c].active) {
