@@ -216,6 +216,9 @@ class ParoRun:
         self.k = orb.shape[0]
         self.lambdas = lam
         self.clamped = 0
+        self._chunks = None      # step_host: (c0, c1, copy event) of the local Step-3 columns
+        self._out = None         # step_host: (copy stream, host orbitals) filled after Step 4
+        self._copy_stream = None
 
     def _sync(self):
         if self.timers:
@@ -230,10 +233,26 @@ class ParoRun:
         sigma = max(0.0, 0.5 - self.lambdas[0])
         local = self.half[c0:c1] if d.world == 1 else self._local(c1 - c0)
         self.last_attempts = 0
+        # column chunks whose inputs may still be in flight (step_host): each
+        # waits for its copy, then solves; the first NotSpd ends the attempt
+        # like the batch abort does (the remaining columns report OK)
+        chunks = self._chunks if self._chunks is not None else [(c0, c1, None)]
         for attempt in range(5):
             self.last_attempts = attempt + 1
-            first, final, iters, _ = be.source_solve(a, self.orb[c0:c1], self.lambdas[c0:c1], sigma, tol,
-                                                     w.cg_max_iter, local)
+            first, final, iters = [], [], []
+            for k0, k1, ev in chunks:
+                if ev is not None and attempt == 0:
+                    torch.cuda.current_stream(be.device).wait_event(ev)
+                if NOT_SPD in first:
+                    first += [OK] * (k1 - k0)
+                    final += [OK] * (k1 - k0)
+                    iters += [0] * (k1 - k0)
+                    continue
+                f, g, i, _ = be.source_solve(a, self.orb[k0:k1], self.lambdas[k0:k1], sigma, tol, w.cg_max_iter,
+                                             local[k0 - c0:k1 - c0])
+                first += f
+                final += g
+                iters += i
             first = d.allgather_ints(first, counts, self._idev())
             final = d.allgather_ints(final, counts, self._idev())
             code, col = step3_outcome(first, final)
@@ -264,6 +283,55 @@ class ParoRun:
             return self._ks_step(it)
         return self._linear_step(it)
 
+    def _copy_out(self, orb):
+        """step_host: this rank's block of the new orbitals to the host (side stream)."""
+        cs, h_orb = self._out
+        o0, o1, _ = self.dist.shard(orb.shape[0])
+        cs.wait_stream(torch.cuda.current_stream(self.be.device))
+        with torch.cuda.stream(cs):
+            h_orb[o0:o1].copy_(orb[o0:o1], non_blocking=True)
+
+    def step_host(self, it: int, h_orb: torch.Tensor, h_rho: torch.Tensor | None = None,
+                  chunks: int = 2) -> Trace:
+        """One outer iteration with the state in (pinned) host memory, the way
+        a host caller of the reference interface holds it: the orbitals (and,
+        for Kohn-Sham, the input density) are copied in, the new orbitals and
+        the mixed density copied back out. The copies run on a side stream:
+        the orbitals arrive in column chunks while the density-only work and
+        the Step-3 solves of the earlier chunks run, and leave while the
+        post-Step-4 density work runs. Returns when everything is back on the
+        host side (h_orb, h_rho updated in place)."""
+        be, d = self.be, self.dist
+        dev = be.device
+        main = torch.cuda.current_stream(dev)
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream(dev)
+        cs = self._copy_stream
+        K = self.k
+        c0, c1, _ = d.shard(K)
+        cs.wait_stream(main)
+        with torch.cuda.stream(cs):
+            if h_rho is not None:
+                self.rho_in.copy_(h_rho, non_blocking=True)
+                main.wait_event(cs.record_event())
+            bounds = [c0 + ((c1 - c0) * i) // chunks for i in range(chunks + 1)]
+            ranges = [(bounds[i], bounds[i + 1]) for i in range(chunks) if bounds[i + 1] > bounds[i]]
+            evs = []
+            for k0, k1 in ranges:
+                self.orb[k0:k1].copy_(h_orb[k0:k1], non_blocking=True)
+                evs.append(cs.record_event())
+        self._chunks = [(k0, k1, ev) for (k0, k1), ev in zip(ranges, evs)]
+        self._out = (cs, h_orb)
+        try:
+            tr = self.step(it)
+        finally:
+            self._chunks, self._out = None, None
+        main.wait_event(evs[-1])
+        if h_rho is not None:
+            h_rho.copy_(self.rho_in, non_blocking=True)
+        main.wait_stream(cs)
+        return tr
+
     def _ks_step(self, it: int) -> Trace:
         """paro.cpp:514-638 with adaptive = false; no stop tests."""
         w, be = self.w, self.be
@@ -283,6 +351,8 @@ class ParoRun:
         a_half, cl = be.ks_form(rho_half, vh_half, "half")
         self.clamped += cl
         orb, lam, defect = be.ritz(half, a_half, N_, w.drop_tol, self.orb)
+        if self._out is not None:  # step_host: the orbitals leave while the density work runs
+            self._copy_out(orb)
         self._sync()
         t_project = time.perf_counter() - tp
         self.k, self.lambdas = orb.shape[0], lam
@@ -304,6 +374,8 @@ class ParoRun:
         t_source = time.perf_counter() - t0
         tp = time.perf_counter()
         orb, lam, defect = be.ritz(self.half[: self.k], be.form, w.n_orbitals, w.drop_tol, self.orb)
+        if self._out is not None:
+            self._copy_out(orb)
         self._sync()
         self.k, self.lambdas = orb.shape[0], lam
         return Trace(it + 1, lam[: w.n_orbitals], None, None, sigma, defect, iters, t_source,

@@ -69,3 +69,29 @@ def test_oscillator_linear_matches_reference(ref):
         np.testing.assert_allclose(tr.lambdas, rr["lambdas"][: w.n_orbitals], rtol=LAM_RTOL)
     # sanity: the lowest oscillator level is 1.5 (up to P1 error on this coarse mesh)
     assert abs(tr.lambdas[0] - 1.5) < 0.2
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_step_host_matches_device_step(chunks):
+    """ParoRun.step_host (state in pinned host memory, copies overlapped on a
+    side stream, Step 3 in column chunks) = ParoRun.step bit for bit."""
+    from paro_b200 import configs
+    from paro_b200.driver import GpuBackend, ParoRun
+
+    w = configs.h2().scaled(16)
+    a = ParoRun(w, GpuBackend(w))
+    b = ParoRun(w, GpuBackend(w))
+    h_orb = torch.empty((b.k, b.be.n), dtype=torch.float64, pin_memory=True)
+    h_rho = torch.empty((b.be.n,), dtype=torch.float64, pin_memory=True)
+    h_orb.copy_(b.orb[: b.k])
+    h_rho.copy_(b.rho_in)
+    for it in range(3):
+        ta = a.step(it)
+        tb = b.step_host(it, h_orb, h_rho, chunks=chunks)
+        torch.cuda.synchronize()
+        assert ta.lambdas == tb.lambdas and ta.e_tot == tb.e_tot and ta.cg_iterations == tb.cg_iterations
+        assert torch.equal(h_orb[: a.k], a.orb[: a.k].cpu())
+        assert torch.equal(h_rho, a.rho_in.cpu())
+        # scramble the device copies: step_host must take its inputs from the host
+        b.orb.normal_()
+        b.rho_in.normal_()
