@@ -61,6 +61,7 @@ struct Ctx {
   int dst_S = 0;                     // grid of the cached DST-I tables
   DevBuf dst_tab;
   DevBuf wtab;                       // assembly: per-(cell, tet, point) weight values
+  DevBuf ws_gram;                    // split-K partial Grams
   DevBuf pcg_x;                      // PCG iterate in the padded solver layout
   DevBuf shifted;                    // (A + sigma M) coefficients of the current shifted solve
   int* pinned_count = nullptr;       // mapped host memory for the active-column poll

@@ -26,10 +26,182 @@ void cublas_check(cublasStatus_t s, const char* what) {
   if (s != CUBLAS_STATUS_SUCCESS) throw ParoError(kCuda, std::string("cuBLAS failure in ") + what);
 }
 
+// ---------------------------------------------------------------------------
+// Symmetric tall-skinny Gram G = X^T Y (n x k operands, k <= kGMaxK; X^T Y is
+// symmetric because Y = B X or A X with B, A symmetric). cuBLAS parallelises
+// one DGEMM only over the k x k output (n ~ 10^7 is the reduction), so: split
+// n into P row chunks, one CTA per chunk computing the upper block triangle of
+// its partial on the FP64 tensor cores (mma.sync m8n8k4 f64, 8x8 tiles, 4
+// warps x <= 15 tiles), rows staged in shared memory by cp.async double
+// buffering; then add the partials in a fixed order and mirror the upper
+// triangle (deterministic, exactly symmetric).
+constexpr int kGB = 8;                    // tile edge
+constexpr int kGR = 32;                   // rows per stage
+constexpr int kGMaxK = 80;                // columns (10 tile blocks -> 55 upper tiles)
+constexpr int kGRow = 96;                 // staged row stride (room for the column swizzle)
+constexpr int kGThreads = 128;            // 4 warps
+constexpr int kGPairsMax = 55;
+
+__device__ __forceinline__ void gcp8(double* dst, const double* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(static_cast<unsigned>(
+                   __cvta_generic_to_shared(dst))),
+               "l"(src), "r"(valid ? 8 : 0)
+               : "memory");
+}
+
+// staged element (row, col) lives at [row][col ^ gswz(row)]: a warp copying 32
+// rows of one column hits 16 distinct bank pairs, and an m8n8k4 operand load
+// (4 consecutive rows x 8 consecutive columns) hits 32 distinct ones
+__device__ __forceinline__ int gswz(int row) { return ((row & 3) << 3) ^ (((row >> 2) & 3) << 1); }
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// upper-triangular tile index of block pair (bi <= bj) among nb blocks
+__device__ __forceinline__ int gpair(int bi, int bj, int nb) { return bi * nb - bi * (bi - 1) / 2 + (bj - bi); }
+
+__global__ void __launch_bounds__(kGThreads) gram_sym_kernel(const double* __restrict__ X, long long ldx,
+                                                             const double* __restrict__ Y, long long ldy, int k,
+                                                             long long n, long long chunk, double* __restrict__ part) {
+  extern __shared__ __align__(16) double gsm[];
+  auto xs = reinterpret_cast<double(*)[kGR][kGRow]>(gsm);
+  auto ys = reinterpret_cast<double(*)[kGR][kGRow]>(gsm + 2 * kGR * kGRow);
+  const long long r0 = blockIdx.x * chunk;
+  const long long r1 = min(n, r0 + chunk);
+  const int nb = (k + kGB - 1) / kGB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // warp w's tile set: row blocks R x column blocks C, upper triangle only.
+  // h = ceil(nb/2): w0 [0,h)x[0,h), w1 [0,h)x[h,h+m), w2 [0,h)x[h+m,nb), w3 [h,nb)x[h,nb)
+  const int h = (nb + 1) / 2, m = (nb - h) / 2;
+  int rlo, rhi, clo, chi;
+  switch (warp) {
+    case 0: rlo = 0, rhi = h, clo = 0, chi = h; break;
+    case 1: rlo = 0, rhi = h, clo = h, chi = h + m; break;
+    case 2: rlo = 0, rhi = h, clo = h + m, chi = nb; break;
+    default: rlo = h, rhi = nb, clo = h, chi = nb; break;
+  }
+  constexpr int kMaxB = 5;
+  double acc[kMaxB][kMaxB][2];
+#pragma unroll
+  for (int i = 0; i < kMaxB; ++i)
+#pragma unroll
+    for (int j = 0; j < kMaxB; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // loads: thread copies row (tid % kGR) of columns tid / kGR + 4 q
+  constexpr int kCStep = kGThreads / kGR;
+  const int lrow = threadIdx.x % kGR, lcol = threadIdx.x / kGR;
+  const int lsw = gswz(lrow);
+  const double* xb = X + lcol * ldx + lrow;
+  const double* yb = Y + lcol * ldy + lrow;
+  auto issue = [&](int st, long long rb) {
+    const bool rin = rb + lrow < r1;
+    const double* px = xb + rb;
+    const double* py = yb + rb;
+#pragma unroll
+    for (int q = 0; q < kGMaxK / kCStep; ++q) {
+      const int col = lcol + q * kCStep;
+      const bool v = rin && col < k;
+      const int sc = col ^ lsw;
+      gcp8(&xs[st][lrow][sc], v ? px : X, v);
+      gcp8(&ys[st][lrow][sc], v ? py : Y, v);
+      px += kCStep * ldx;
+      py += kCStep * ldy;
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+
+  const int fr = lane & 3, fc = lane >> 2;  // fragment row (k) and column (tile row / col)
+  int st = 0;
+  issue(0, r0);
+  for (long long rb = r0; rb < r1; rb += kGR, st ^= 1) {
+    if (rb + kGR < r1) {
+      issue(st ^ 1, rb + kGR);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int k0 = 0; k0 < kGR; k0 += 4) {
+      const int row = k0 + fr;
+      const int sw = gswz(row);
+      double a[kMaxB], b[kMaxB];
+#pragma unroll
+      for (int i = 0; i < kMaxB; ++i) {
+        a[i] = rlo + i < rhi ? xs[st][row][((rlo + i) * kGB + fc) ^ sw] : 0.0;
+        b[i] = clo + i < chi ? ys[st][row][((clo + i) * kGB + fc) ^ sw] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < kMaxB; ++i)
+#pragma unroll
+        for (int j = 0; j < kMaxB; ++j)
+          if (rlo + i < rhi && clo + j < chi && clo + j >= rlo + i) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+  // tile (bi, bj): lane holds C[fc][2 fr + {0,1}]
+#pragma unroll
+  for (int i = 0; i < kMaxB; ++i)
+#pragma unroll
+    for (int j = 0; j < kMaxB; ++j) {
+      const int bi = rlo + i, bj = clo + j;
+      if (bi < rhi && bj < chi && bj >= bi) {
+        double* o = part + (static_cast<long long>(blockIdx.x) * kGPairsMax + gpair(bi, bj, nb)) * (kGB * kGB);
+        o[fc * kGB + 2 * fr] = acc[i][j][0];
+        o[fc * kGB + 2 * fr + 1] = acc[i][j][1];
+      }
+    }
+}
+
+// G[row, col] (column-major, k x k) from the partials of tile t, in a fixed
+// order over chunks; the upper triangle is mirrored.
+__global__ void gram_sym_reduce_kernel(const double* __restrict__ part, int P, int k, double* __restrict__ G) {
+  const int nb = (k + kGB - 1) / kGB;
+  const int t = blockIdx.x;
+  int bi = 0, q = t;
+  while (bi < nb && q >= nb - bi) {
+    q -= nb - bi;
+    ++bi;
+  }
+  const int bj = bi + q;
+  const int e = threadIdx.x;  // 0..63
+  const int i = e / kGB, j = e % kGB;
+  const int row = bi * kGB + i, col = bj * kGB + j;
+  if (row >= k || col >= k || row > col) return;
+  double s = 0.0;
+  for (int p = 0; p < P; ++p) s += part[(static_cast<long long>(p) * kGPairsMax + t) * (kGB * kGB) + e];
+  G[row + static_cast<long long>(col) * k] = s;
+  G[col + static_cast<long long>(row) * k] = s;
+}
+
 // G (k1 x k2, column-major) = X^T Y, X: n x k1 (ldx), Y: n x k2 (ldy)
 void gram(Ctx& ctx, int k1, int k2, const double* X, long long ldx, const double* Y, long long ldy, double* G) {
+  const long long n = ctx.grid.n;
+  if (k1 == k2 && k1 <= kGMaxK) {
+    const int P = 148 * 4;
+    const long long chunk = ((n + P - 1) / P + kGR - 1) / kGR * kGR;
+    const int Pn = static_cast<int>((n + chunk - 1) / chunk);
+    double* part = ctx.ws_gram.get<double>(static_cast<size_t>(Pn) * kGPairsMax * kGB * kGB);
+    constexpr size_t smem = sizeof(double) * 4 * kGR * kGRow;
+    static bool configured = false;
+    if (!configured) {
+      PARO_CUDA(cudaFuncSetAttribute(gram_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+      configured = true;
+    }
+    gram_sym_kernel<<<Pn, kGThreads, smem, ctx.stream>>>(X, ldx, Y, ldy, k1, n, chunk, part);
+    const int nb = (k1 + kGB - 1) / kGB;
+    gram_sym_reduce_kernel<<<nb * (nb + 1) / 2, kGB * kGB, 0, ctx.stream>>>(part, Pn, k1, G);
+    PARO_CUDA(cudaGetLastError());
+    ctx.launches += 2;
+    return;
+  }
   const double one = 1.0, zero = 0.0;
-  cublas_check(cublasDgemm(ctx.cublas, CUBLAS_OP_T, CUBLAS_OP_N, k1, k2, static_cast<int>(ctx.grid.n), &one, X,
+  cublas_check(cublasDgemm(ctx.cublas, CUBLAS_OP_T, CUBLAS_OP_N, k1, k2, static_cast<int>(n), &one, X,
                            static_cast<int>(ldx), Y, static_cast<int>(ldy), &zero, G, k1),
                "gram");
   ++ctx.launches;
