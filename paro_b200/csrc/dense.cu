@@ -81,9 +81,22 @@ __device__ void fix_sign_seq(int n, double* v, int stride) {
 
 // jacobi_eig (linalg.cpp:243-302): a (n x n, destroyed), v (n x n) eigenvectors,
 // vals sorted ascending, vecs columns reordered accordingly into `out`.
-__device__ void warp_jacobi(int n, double* a, double* v, double tol, int max_sweeps, double* vals, double* out,
+__device__ void warp_jacobi(int n, double* a_g, double* v_g, double tol, int max_sweeps, double* vals, double* out,
                             int* order) {
   const int lane = threadIdx.x;
+  // the rotation sequence is latency-bound: run it on shared-memory copies
+  // when the launch provided 2 n^2 doubles of dynamic shared memory
+  extern __shared__ double jsm[];
+  unsigned dyn;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+  double* a = a_g;
+  double* v = v_g;
+  if (dyn >= 2u * n * n * sizeof(double)) {
+    a = jsm;
+    v = jsm + n * n;
+    for (int i = lane; i < n * n; i += 32) a[i] = a_g[i];
+    __syncwarp();
+  }
   warp_fill(v, n * n, 0.0);
   for (int i = lane; i < n; i += 32) v[i * n + i] = 1.0;
   __syncwarp();
@@ -423,6 +436,21 @@ __global__ void pencil_kernel(int k, const double* GA, const double* C2, const d
     Y[i + j * k] = s;
   }
   if (lane == 0) *status = kOk;
+}
+
+size_t dense_jacobi_smem(int n) {
+  const size_t bytes = 2ull * n * n * sizeof(double);
+  return bytes <= 220u * 1024u ? bytes : 0;
+}
+
+void dense_configure() {
+  static bool done = false;
+  if (done) return;
+  const int mx = 227 * 1024;
+  PARO_CUDA(cudaFuncSetAttribute(geneig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  PARO_CUDA(cudaFuncSetAttribute(pencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  PARO_CUDA(cudaFuncSetAttribute(pencil_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  done = true;
 }
 
 }  // namespace paro_b200

@@ -15,6 +15,10 @@ struct DenseScratch {
   int* order = nullptr;
 };
 
+// dynamic shared memory for a kernel running warp_jacobi on n x n (0 = global)
+size_t dense_jacobi_smem(int n);
+void dense_configure();
+
 __global__ void geneig_kernel(int n, const double* A, const double* B, double* vals, double* X, DenseScratch w,
                               int* status);
 __global__ void ortho_from_gram_kernel(int K, const double* G, double drop_tol, int allow_drop, double* C, int* acc,
