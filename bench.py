@@ -143,6 +143,19 @@ def run_reference(args):
     return 0
 
 
+def pcg_traffic():
+    """DRAM bytes of one PCG iteration (K1 + K2 at k = 76) from the committed
+    ncu --set full capture, next to the algorithmic n(88k+64)."""
+    path = ROOT / "profiles" / "r01" / "pcg_traffic.json"
+    try:
+        t = json.loads(path.read_text())
+    except (OSError, ValueError):
+        return {}
+    return {"bytes": t["traffic_bytes_per_iteration"],
+            "note": f"dram read+write per PCG iteration at k=76 (K1+K2), {path.relative_to(ROOT)}; "
+                    f"algorithmic {t['algorithmic_bytes_per_iteration']:.4g} B"}
+
+
 def workload_config(w, world):
     return {"workload": f"BASELINE configs: {w.name} ({w.kind}, {w.subdivisions + 1}^3 nodes, n={w.n}, K={w.K}, "
                         f"box [{w.lo},{w.hi}]^3)",
@@ -266,6 +279,7 @@ def main():
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {exc}"}
 
     if rank == 0:
+        traffic = pcg_traffic()
         pk = peaks()
         peak = float(pk.get("hbm_gbs", 6650.0))
         achieved = st["step3_bytes"] / st["step3_s"] / 1e9 if st["step3_s"] > 0 else 0.0
@@ -276,7 +290,8 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE generator)",
             "config": workload_config(w, world),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak if peak else None, "traffic": None,
+                         "frac": achieved / peak if peak else None, "traffic": traffic.get("bytes"),
+                         "traffic_note": traffic.get("note"),
                          "kernel": "Step-3 Jacobi-PCG iteration (march K1+K2 + finalize), algorithmic n*(88k+64) B",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("_fallback") else "fallback"},
             "cpu_baseline": cpu,
