@@ -192,6 +192,20 @@ int paro_integrate_product(paro_ctx* ctx, const double* u, const double* v, doub
 /* ||rho_out - rho_in||_L2 (paro.cpp:608-612); scratch: n device doubles */
 int paro_rho_residual(paro_ctx* ctx, const double* rho_out, const double* rho_in, double* scratch, double* out);
 /* total_energy (model.cpp:329-360); lambdas, occ, charges, positions: host */
+/* Step 2 on a fixed mesh: eta_total of combine_max over the
+ * first N orbitals of estimate_eigen_residual (proj/src/adapt.cpp:104-129,
+ * estimate_source_residual :58-102, ErrorIndicators::total :14-18), as the
+ * drivers run it every outer iteration (Kohn-Sham proj/src/paro.cpp:521-538,
+ * linear :306-315). Diffusion D = diffusion * I; reaction 0 = Kohn-Sham
+ * V_ext + V_H(rho) + v_xc(rho) at the point (rho, vh device arrays, nuclei
+ * and eps as in paro_assemble_vext), 1 = c |x|^2, 2 = external_potential(nuclei,
+ * eps). U: device, N columns of stride ld; lambdas: host. eta (device, 6 s^3
+ * doubles in the reference element order, may be NULL) receives the combined
+ * per-element indicators; *eta_total the total. */
+int paro_estimate_eta(paro_ctx* ctx, int N, const double* U, long long ld, const double* lambdas, double diffusion,
+                      int reaction, double c, int nnuc, const double* charges, const double* positions, double eps,
+                      const double* rho, const double* vh, int exchange_only, double* eta, double* eta_total);
+
 int paro_total_energy(paro_ctx* ctx, int n_lambdas, const double* lambdas, int nocc, const double* occ,
                       const double* rho, const double* vh, int exchange_only, int nnuc, const double* charges,
                       const double* positions, double* e_out);

@@ -154,6 +154,19 @@ int main() {
   const double Eg = gpu::total_energy(ref_set.lambdas, dr, vr, XcModel::lda_pz81, mol);
   CHECK(std::abs(Er - Eg) <= 1e-12 * std::abs(Er));
 
+  // Step 2 on a fixed mesh: the driver's estimator loop (paro.cpp:521-538)
+  const ElemScalarFn veff = [&](std::size_t e, const Vec3& x) {
+    const auto bary = space->mesh().barycentric(e, x);
+    const double rho_q = evaluate_in_element(dr.rho, e, bary);
+    return vext.value(x) + evaluate_in_element(vr, e, bary) + lda_vxc(rho_q, XcModel::lda_pz81).v_xc;
+  };
+  const ErrorIndicators ir =
+      combine_max({estimate_eigen_residual(*space, occ[0], ref_set.lambdas[0], occ[0], constant_diffusion(0.5), veff, 1)});
+  const ErrorIndicators ig = gpu::ks_step2_indicators(occ, ref_set.lambdas, dr, vr, mol, 0.0, XcModel::lda_pz81);
+  CHECK(ig.eta.size() == ir.eta.size() && ig.mesh_id == ir.mesh_id);
+  CHECK(std::abs(ig.total() - ir.total()) <= 1e-10 * ir.total());
+  CHECK(maxdiff(ig.eta, ir.eta) <= 1e-10 * maxabs(ir.eta));
+
   std::printf("%s dropin_test (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
   return failures ? 1 : 0;
 }

@@ -286,4 +286,38 @@ double total_energy(const std::vector<double>& lambdas, const Density& density, 
   return e;
 }
 
+ErrorIndicators ks_step2_indicators(const std::vector<DiscreteFunction>& occupied,
+                                    const std::vector<double>& lambdas, const Density& rho_in,
+                                    const DiscreteFunction& vh_in, const Molecule& molecule, double vext_smoothing,
+                                    XcModel xc) {
+  if (occupied.empty()) throw InvalidArgumentError("combine_max: empty input");
+  if (lambdas.size() < occupied.size()) throw InvalidArgumentError("estimate: missing eigenvalue estimates");
+  const std::size_t n = rho_in.rho.coeffs.size();
+  need(n);
+  std::vector<std::vector<double>> cols;
+  for (const auto& u : occupied) {
+    if (u.space->mesh().id() != rho_in.rho.space->mesh().id())
+      throw LineageError("estimate: previous iterate lives on a different mesh generation");
+    cols.push_back(u.coeffs);
+  }
+  DevVec du = pack(cols, n), dr(n), dv(n);
+  dr.up(rho_in.rho.coeffs.data(), n);
+  dv.up(vh_in.coeffs.data(), n);
+  std::vector<double> z, pos;
+  for (const auto& nuc : molecule.nuclei) {
+    z.push_back(nuc.charge);
+    pos.insert(pos.end(), {nuc.position.x, nuc.position.y, nuc.position.z});
+  }
+  ErrorIndicators out;
+  out.mesh_id = rho_in.rho.space->mesh().id();
+  out.eta.resize(rho_in.rho.space->mesh().element_count());
+  DevVec deta(out.eta.size());
+  double total = 0.0;
+  check(paro_estimate_eta(g.ctx, static_cast<int>(cols.size()), du.p, static_cast<long long>(n), lambdas.data(), 0.5,
+                          0, 0.0, static_cast<int>(z.size()), z.data(), pos.data(), vext_smoothing, dr.p, dv.p,
+                          xc == XcModel::exchange_only ? 1 : 0, deta.p, &total));
+  deta.down(out.eta.data(), out.eta.size());
+  return out;
+}
+
 }  // namespace paro::gpu

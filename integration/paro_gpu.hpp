@@ -9,6 +9,7 @@
 #include <memory>
 #include <vector>
 
+#include "paro/adapt.hpp"
 #include "paro/fem.hpp"
 #include "paro/linalg.hpp"
 #include "paro/model.hpp"
@@ -53,5 +54,14 @@ DiscreteFunction hartree_solve_with(const SparseOperator& poisson_stiffness, con
 /// total_energy (model.cpp:329-360)
 double total_energy(const std::vector<double>& lambdas, const Density& density, const DiscreteFunction& v_hartree,
                     XcModel xc, const Molecule& molecule);
+
+/// Step 2 of the Kohn-Sham driver on a fixed mesh (paro.cpp:521-538):
+/// combine_max over the occupied orbitals of estimate_eigen_residual
+/// (adapt.cpp:104-129) with diffusion 1/2 and reaction V_ext + V_H + v_xc;
+/// eta in the reference element order, mesh_id of the orbitals' mesh.
+ErrorIndicators ks_step2_indicators(const std::vector<DiscreteFunction>& occupied,
+                                    const std::vector<double>& lambdas, const Density& rho_in,
+                                    const DiscreteFunction& vh_in, const Molecule& molecule, double vext_smoothing,
+                                    XcModel xc);
 
 }  // namespace paro::gpu

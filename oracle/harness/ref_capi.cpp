@@ -150,6 +150,19 @@ struct LinState {
   OrbitalSet orbitals;
 };
 
+double eta_total_with(const std::shared_ptr<const FeSpace>& space, std::size_t N, const double* U,
+                      const double* lambdas, const ElemMatrixFn& diffusion, const ElemScalarFn& reaction,
+                      double* eta_out) {
+  const std::size_t n = space->dof_count();
+  std::vector<ErrorIndicators> per_orbital;
+  for (std::size_t i = 0; i < N; ++i) {
+    const DiscreteFunction ui(space, std::vector<double>(U + i * n, U + (i + 1) * n));
+    per_orbital.push_back(estimate_eigen_residual(*space, ui, lambdas[i], ui, diffusion, reaction, 1));
+  }
+  const ErrorIndicators ind = combine_max(per_orbital);
+  if (eta_out) std::memcpy(eta_out, ind.eta.data(), ind.eta.size() * sizeof(double));
+  return ind.total();
+}
 }  // namespace
 
 extern "C" {
@@ -603,6 +616,49 @@ void ref_ks_state_get(void* sv, int which, double* out) {
     for (std::size_t j = 0; j < s->orbitals.count(); ++j) out[j] = s->orbitals.lambdas[j];
 }
 long ref_ks_state_clamped(void* sv) { return static_cast<KsState*>(sv)->clamped; }
+
+// ------------------------------------------------------ Step-2 estimator ----
+// combine_max over the first N orbitals of estimate_eigen_residual and its
+// total, exactly as the reference drivers run Step 2 on a fixed mesh.
+
+// Kohn-Sham: reaction = V_ext + V_H(rho_in) + v_xc(rho_in) at the point
+// (paro.cpp:521-538).
+int ref_ks_eta_total(void* h, std::size_t N, const double* U, const double* lambdas, const double* rho,
+                     const double* vh, double* eta_out, double* total) {
+  return guarded([&] {
+    auto* k = static_cast<KsH*>(h);
+    auto space = k->space;
+    const std::size_t n = space->dof_count();
+    const DiscreteFunction rho_f(space, std::vector<double>(rho, rho + n));
+    const DiscreteFunction vh_in(space, std::vector<double>(vh, vh + n));
+    const KsModel& model = k->model;
+    const ElemScalarFn veff = [&](std::size_t e, const Vec3& x) {
+      const auto bary = space->mesh().barycentric(e, x);
+      const double rho_q = evaluate_in_element(rho_f, e, bary);
+      return model.vext.value(x) + evaluate_in_element(vh_in, e, bary) + lda_vxc(rho_q, model.xc).v_xc;
+    };
+    *total = eta_total_with(space, N, U, lambdas, constant_diffusion(0.5), veff, eta_out);
+  });
+}
+
+// Linear problems (paro.cpp:306-315): diffusion = diff_scale * I, reaction
+// kind 1 = c |x|^2, kind 2 = external_potential(nuclei, eps).
+int ref_lin_eta_total(void* sp, std::size_t N, const double* U, const double* lambdas, double diff_scale, int kind,
+                      double c, int nnuc, const double* z, const double* r, double eps, double* eta_out,
+                      double* total) {
+  return guarded([&] {
+    auto space = static_cast<SpaceH*>(sp)->space;
+    ElemScalarFn reaction;
+    if (kind == 1) {
+      reaction = field_from([c](const Vec3& x) { return c * (x.x * x.x + x.y * x.y + x.z * x.z); });
+    } else {
+      const Molecule mol = make_molecule(nnuc, z, r, 2);
+      reaction = field_from(external_potential(mol, eps).value);
+    }
+    *total = eta_total_with(space, N, U, lambdas, constant_diffusion(diff_scale), reaction, eta_out);
+  });
+}
+
 
 // --------------------------------------------------------- linear loop ------
 void* ref_lin_state_create(void* sp, void* a, void* b, std::size_t k, std::size_t n_orbitals,

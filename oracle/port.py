@@ -385,3 +385,95 @@ def total_energy(lambdas, occ, rho, vh, Z, R, s, lo, hi, exchange_only=False):
         vx, ex, _ = lda_vxc(rq, exchange_only)
         e_xc += float(np.sum(0.25 * vol * (ex - vx) * rq))
     return e_band - e_h + e_xc + nuclear_repulsion(Z, R)
+
+
+# -------------------------------------------------------------- Step 2 ----
+
+def _tet_geometry(s, lo, hi):
+    """Vertex coordinates (mesh.cpp:432-434), diameters (mesh.cpp:109-118),
+    volumes and barycentric gradients (fem.cpp:65-88) of every Kuhn tet."""
+    t = kuhn_elements(s)
+    P = lo + (hi - lo) * t.astype(float) / s
+    diam = np.zeros(len(t))
+    for i in range(4):
+        for j in range(i + 1, 4):
+            diam = np.maximum(diam, np.linalg.norm(P[:, i] - P[:, j], axis=1))
+    a, b, c = P[:, 1] - P[:, 0], P[:, 2] - P[:, 0], P[:, 3] - P[:, 0]
+    det = np.einsum("ij,ij->i", a, np.cross(b, c))
+    g = np.zeros((len(t), 4, 3))
+    g[:, 1] = np.cross(b, c) / det[:, None]
+    g[:, 2] = np.cross(c, a) / det[:, None]
+    g[:, 3] = np.cross(a, b) / det[:, None]
+    g[:, 0] = -(g[:, 1] + g[:, 2] + g[:, 3])
+    return t, P, diam, np.abs(det) / 6.0, g
+
+
+def _interior_faces(t, s):
+    """Interior faces (two tets sharing three vertices): elem pair, normal,
+    diameter and measure (adapt.cpp:27-56)."""
+    vid = (t[:, :, 2] * (s + 1) + t[:, :, 1]) * (s + 1) + t[:, :, 0]
+    owner = {}
+    pairs = []
+    for e in range(len(t)):
+        for k in range(4):
+            key = tuple(sorted(int(vid[e, m]) for m in range(4) if m != k))
+            if key in owner:
+                pairs.append((owner.pop(key), e, key))
+            else:
+                owner[key] = e
+    return pairs
+
+
+def estimate_eta(U, lambdas, s, lo, hi, reaction, diffusion=0.5):
+    """combine_max over the columns of estimate_eigen_residual and its total
+    (adapt.cpp:58-129): eta2_e = h_e^2 sum_q w_q |e| (lambda u - c u)^2(x_q)
+    + sum_faces 1/2 diam |f| ((F_e - F_e').n)^2 with F = diffusion grad u.
+    `reaction(x [E,4,3], bary [4,4]) -> [E,4]` evaluates c at the quadrature
+    points. Returns (total, eta [6 s^3])."""
+    t, P, diam, vol, g = _tet_geometry(s, lo, hi)
+    bary = np.full((4, 4), QUAD4_B)
+    np.fill_diagonal(bary, QUAD4_A)
+    X = np.einsum("qi,eid->eqd", bary, P)
+    react = reaction(X, bary, t)
+    faces = _interior_faces(t, s)
+    coords = lambda key: np.array([[k % (s + 1), (k // (s + 1)) % (s + 1), k // (s + 1) ** 2] for k in key],
+                                  float) * (hi - lo) / s + lo
+    fgeo = []
+    for e0, e1, key in faces:
+        A, B, Cc = coords(key)
+        n = np.cross(B - A, Cc - A)
+        area = 0.5 * np.linalg.norm(n)
+        fd = max(np.linalg.norm(A - B), np.linalg.norm(B - Cc), np.linalg.norm(A - Cc))
+        fgeo.append((e0, e1, n / np.linalg.norm(n), 0.5 * fd * area))
+    e0 = np.array([f[0] for f in fgeo])
+    e1 = np.array([f[1] for f in fgeo])
+    nrm = np.array([f[2] for f in fgeo])
+    fac = np.array([f[3] for f in fgeo])
+    best = np.zeros(len(t))
+    for col, lam in zip(np.atleast_2d(U), lambdas):
+        v = _elem_values(col, s, t)
+        uh = v @ bary.T
+        r = lam * uh - react * uh
+        eta2 = diam * diam * np.sum(0.25 * vol[:, None] * r * r, axis=1)
+        flux = diffusion * np.einsum("ei,eid->ed", v, g)
+        jump = np.einsum("fd,fd->f", flux[e0] - flux[e1], nrm)
+        contrib = fac * jump * jump
+        np.add.at(eta2, e0, contrib)
+        np.add.at(eta2, e1, contrib)
+        best = np.maximum(best, np.sqrt(np.maximum(0.0, eta2)))
+    return math.sqrt(float(np.sum(best * best))), best
+
+
+def ks_reaction(Z, R, rho, vh, s, eps=0.0, exchange_only=False):
+    """V_ext(x) + V_H(x) + v_xc(rho(x)) at the quadrature points (paro.cpp:525-531)."""
+    Z = np.asarray(Z, float)
+    R = np.asarray(R, float).reshape(-1, 3)
+
+    def f(X, bary, t):
+        d2 = ((X[:, :, None, :] - R[None, None]) ** 2).sum(-1)
+        vext = -(Z / np.sqrt(d2 + eps * eps)).sum(-1)
+        rq = _elem_values(rho, s, t) @ bary.T
+        vq = _elem_values(vh, s, t) @ bary.T
+        return vext + vq + lda_vxc(rq, exchange_only)[0]
+    return f
+

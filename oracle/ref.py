@@ -133,6 +133,9 @@ def lib():
             "ref_ks_state_k": (_SZ, [_P]),
             "ref_ks_state_step": (C.c_int, [_P, C.c_int, _DP, _DP]),
             "ref_ks_state_get": (None, [_P, C.c_int, _DP]),
+            "ref_ks_eta_total": (C.c_int, [_P, C.c_size_t, _DP, _DP, _DP, _DP, _DP, _DP]),
+            "ref_lin_eta_total": (C.c_int, [_P, C.c_size_t, _DP, _DP, _D, C.c_int, _D, C.c_int, _DP, _DP, _D, _DP,
+                                            _DP]),
             "ref_ks_state_clamped": (C.c_long, [_P]),
             "ref_lin_state_create": (_P, [_P, _P, _P, _SZ, _SZ, _DP, _D, _D, _D, _SZ, _D, C.c_int]),
             "ref_lin_state_free": (None, [_P]),
@@ -423,11 +426,43 @@ class KsSystem:
         idx = {"mass": 0, "kinetic": 1, "vext": 2, "poisson": 3}[which]
         return Op(lib().ref_ks_op(self.h, idx), self)
 
+    def eta_total(self, U, lambdas, rho, vh, with_eta=False):
+        """Step 2 of the KS driver (paro.cpp:521-538) on the first N orbitals."""
+        U = np.ascontiguousarray(U, np.float64)
+        lam = np.ascontiguousarray(lambdas, np.float64)
+        eta = _eta_out(self.sp, with_eta)
+        tot = C.c_double(0.0)
+        _check(lib().ref_ks_eta_total(self.h, U.shape[0], _dp(U), _dp(lam), _dp(np.ascontiguousarray(rho, np.float64)),
+                                      _dp(np.ascontiguousarray(vh, np.float64)),
+                                      _dp(eta) if eta is not None else None, C.byref(tot)))
+        return (tot.value, eta) if with_eta else tot.value
+
     def form(self, rho, vh):
         cl = C.c_long(0)
         op = Op(lib().ref_ks_form(self.h, _dp(np.ascontiguousarray(rho, np.float64)),
                                   _dp(np.ascontiguousarray(vh, np.float64)), C.byref(cl)), self)
         return op, cl.value
+
+
+def _eta_out(sp, with_eta):
+    return np.empty(6 * sp.s ** 3) if with_eta else None
+
+
+def lin_eta_total(sp: Space, U, lambdas, diffusion: float, reaction: str, c: float = 0.0, Z=(), R=(), eps=0.0,
+                  with_eta=False):
+    """Step-2 estimator of the linear driver (paro.cpp:306-315): combine_max over the
+    orbitals of estimate_eigen_residual (adapt.cpp:104-115) and its total."""
+    U = np.ascontiguousarray(U, np.float64)
+    lam = np.ascontiguousarray(lambdas, np.float64)
+    Z = np.ascontiguousarray(Z, np.float64)
+    Rf = np.ascontiguousarray(np.asarray(R, np.float64).reshape(-1))
+    eta = _eta_out(sp, with_eta)
+    tot = C.c_double(0.0)
+    kind = {"harmonic": 1, "well": 2}[reaction]
+    _check(lib().ref_lin_eta_total(sp.h, U.shape[0], _dp(U), _dp(lam), diffusion, kind, c, len(Z),
+                                   _dp(Z) if len(Z) else None, _dp(Rf) if len(Z) else None, eps,
+                                   _dp(eta) if eta is not None else None, C.byref(tot)))
+    return (tot.value, eta) if with_eta else tot.value
 
 
 class KsLoop:

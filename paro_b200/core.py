@@ -473,3 +473,29 @@ def total_energy(ctx: Context, lambdas, occupations, rho: torch.Tensor, vh: torc
     R = np.ascontiguousarray(positions, np.float64).reshape(-1)
     return _scalar(ctx, N.lib().paro_total_energy, len(lambdas), lam, len(occupations), occ, _ptr(rho), _ptr(vh),
                    int(exchange_only), len(Z), Z.ctypes.data_as(_DP), R.ctypes.data_as(_DP))
+
+
+def estimate_eta(ctx: Context, orbitals: torch.Tensor, lambdas, *, diffusion: float = 0.5, reaction: str = "ks",
+                 c: float = 0.0, charges=(), positions=(), eps: float = 0.0, rho: torch.Tensor | None = None,
+                 vh: torch.Tensor | None = None, exchange_only: bool = False, with_eta: bool = False):
+    """Step 2 on a fixed mesh: combine_max over the orbitals (rows of
+    `orbitals`) of estimate_eigen_residual (adapt.cpp:104-129) and its total,
+    as the drivers run it every iteration (paro.cpp:521-538 Kohn-Sham with
+    reaction "ks"; paro.cpp:306-315 linear with "harmonic" (c |x|^2) or "well"
+    (external_potential)). Returns eta_total, or (eta_total, eta[6 s^3]) in
+    the reference element order."""
+    U = _as_cols(orbitals, ctx.n)
+    k = U.shape[0]
+    lam = (C.c_double * k)(*[float(v) for v in lambdas[:k]])
+    kind = {"ks": 0, "harmonic": 1, "well": 2}[reaction]
+    Z = np.ascontiguousarray(charges, np.float64)
+    R = np.ascontiguousarray(positions, np.float64).reshape(-1)
+    eta = torch.empty(6 * ctx.s ** 3, dtype=torch.float64, device=ctx.device) if with_eta else None
+    tot = C.c_double(0.0)
+    ctx.check(N.lib().paro_estimate_eta(ctx.h, k, _ptr(U), U.stride(0) if k > 1 else ctx.n, lam, diffusion, kind, c,
+                                        len(Z), Z.ctypes.data_as(_DP) if len(Z) else None,
+                                        R.ctypes.data_as(_DP) if len(Z) else None, eps,
+                                        _ptr(rho) if rho is not None else None, _ptr(vh) if vh is not None else None,
+                                        int(exchange_only), _ptr(eta) if eta is not None else None, C.byref(tot)))
+    return (tot.value, eta) if with_eta else tot.value
+

@@ -10,6 +10,7 @@
 
 #include "ctx.hpp"
 #include "assemble.hpp"
+#include "estimate.hpp"
 #include "fields.hpp"
 #include "ritz.hpp"
 #include "solver.hpp"
@@ -559,6 +560,30 @@ int paro_rho_residual(paro_ctx* ctx, const double* rho_out, const double* rho_in
   return guarded(ctx, [&] {
     diff(ctx->c, rho_out, rho_in, scratch);
     *out = norm_l2(ctx->c, scratch);
+    return kOk;
+  });
+}
+
+int paro_estimate_eta(paro_ctx* ctx, int N, const double* U, long long ld, const double* lambdas, double diffusion,
+                      int reaction, double c, int nnuc, const double* charges, const double* positions, double eps,
+                      const double* rho, const double* vh, int exchange_only, double* eta, double* eta_total) {
+  return guarded(ctx, [&] {
+    if (!eta_total || !lambdas || !U) throw ParoError(kInvalidArgument, "estimate: null argument");
+    if (reaction < kEstKs || reaction > kEstWell) throw ParoError(kInvalidArgument, "estimate: unknown reaction");
+    EstimateSpec s;
+    s.kind = reaction;
+    s.diffusion = diffusion;
+    s.c = c;
+    s.eps = eps;
+    s.rho = rho;
+    s.vh = vh;
+    s.exchange_only = exchange_only;
+    s.lambdas = lambdas;
+    for (int k = 0; k < nnuc; ++k) {
+      s.nuclei.push_back(charges[k]);
+      for (int d = 0; d < 3; ++d) s.nuclei.push_back(positions[3 * k + d]);
+    }
+    *eta_total = estimate_eta(ctx->c, s, N, U, ld, eta);
     return kOk;
   });
 }

@@ -167,6 +167,17 @@ class GpuBackend:
     def rho_residual(self, rout, rin):
         return self.core.rho_residual(self.ctx, rout, rin, self.scratch)
 
+    def estimate(self, U, lambdas, rho=None, vh=None):
+        """Step 2 (adapt.cpp:104-129): eta_total of the orbitals' residual estimators."""
+        w = self.w
+        if w.kind == "ks":
+            return self.core.estimate_eta(self.ctx, U, lambdas, reaction="ks", charges=w.charges,
+                                          positions=w.positions, eps=w.eps, rho=rho, vh=vh)
+        if w.potential == "harmonic":
+            return self.core.estimate_eta(self.ctx, U, lambdas, reaction="harmonic", c=0.5)
+        return self.core.estimate_eta(self.ctx, U, lambdas, reaction="well", charges=w.charges,
+                                      positions=w.positions, eps=w.eps)
+
     def launches(self) -> int:
         return self.ctx.launches()
 
@@ -183,13 +194,16 @@ class Trace:
     t_source: float
     t_project: float
     t_total: float
+    eta_total: float | None = None   # Step 2 (estimate=True): combine_max(estimate_eigen_residual).total()
 
 
 class ParoRun:
     """One fixed-mesh ParO run (KS or linear) on a backend, sharded by `dist`."""
 
-    def __init__(self, w: Workload, backend, dist: Dist | None = None, guess=None, timers: bool = True):
+    def __init__(self, w: Workload, backend, dist: Dist | None = None, guess=None, timers: bool = True,
+                 estimate: bool = False):
         self.w = w
+        self.estimate = estimate  # run Step 2 (eta_total) like the reference drivers; off in the bench (SURVEY 8d)
         self.be = backend
         self.dist = dist or Dist()
         self.timers = timers
@@ -338,6 +352,8 @@ class ParoRun:
         N_ = w.n_orbitals
         t0 = time.perf_counter()
         vh_in = be.hartree(self.rho_in, out=self.vh)
+        # Step 2 on a fixed mesh: the estimator only feeds eta_total (paro.cpp:521-538)
+        eta = be.estimate(self.orb[:N_], self.lambdas[:N_], self.rho_in, vh_in) if self.estimate else None
         a_in, cl = be.ks_form(self.rho_in, vh_in, "in")
         self.clamped += cl
         ts = time.perf_counter()
@@ -363,12 +379,14 @@ class ParoRun:
         be.mix(self.rho_in, rho_out, w.mixing_alpha, out=self.rho_in)
         self._sync()
         return Trace(it + 1, lam[: w.n_orbitals], e_tot, res, sigma, defect, iters, t_source, t_project,
-                     time.perf_counter() - t0)
+                     time.perf_counter() - t0, eta)
 
     def _linear_step(self, it: int) -> Trace:
         """paro.cpp:340-354."""
         w, be = self.w, self.be
         t0 = time.perf_counter()
+        N_ = w.n_orbitals
+        eta = be.estimate(self.orb[:N_], self.lambdas[:N_]) if self.estimate else None  # paro.cpp:306-315
         sigma, iters = self.step3(be.form, it)
         self._sync()
         t_source = time.perf_counter() - t0
@@ -379,7 +397,7 @@ class ParoRun:
         self._sync()
         self.k, self.lambdas = orb.shape[0], lam
         return Trace(it + 1, lam[: w.n_orbitals], None, None, sigma, defect, iters, t_source,
-                     time.perf_counter() - tp, time.perf_counter() - t0)
+                     time.perf_counter() - tp, time.perf_counter() - t0, eta)
 
     def run(self, iterations: int | None = None):
         return [self.step(i) for i in range(iterations if iterations is not None else self.w.iterations)]

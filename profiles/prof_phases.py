@@ -53,6 +53,8 @@ def main():
     res["ritz_s"], _ = timed(lambda: be.ritz(half, a_half, N, w.drop_tol, run.orb), reps=2)
     res["apply_K_s"], _ = timed(lambda: a_half.apply(half, out=run.orb[: run.k]))
     res["mass_apply_K_s"], _ = timed(lambda: be.mass.apply(half, out=run.orb[: run.k]))
+    res["step2_estimator_s"], res["eta_total"] = timed(
+        lambda: be.estimate(run.orb[:N], run.lambdas[:N], run.rho_in, run.vh), reps=1)
     print(json.dumps(res))
 
 

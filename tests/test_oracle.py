@@ -185,3 +185,27 @@ def test_reference_reproduces_golden(ref, name):
         np.testing.assert_allclose(r["lambdas"][: w.n_orbitals], row["lambdas"], rtol=1e-12)
         if "e_tot" in row:
             assert r["e_tot"] == pytest.approx(row["e_tot"], rel=1e-12)
+
+
+def test_port_estimator_matches_reference(ref):
+    """Step-2 estimator (adapt.cpp:58-129): numpy restatement vs the compiled
+    reference, Kohn-Sham and linear reactions, on a 6^3-cell mesh."""
+    from oracle import port
+
+    s, lo, hi = 6, -4.0, 4.0
+    sp = ref.Space(s, lo, hi)
+    rng = np.random.default_rng(11)
+    U = rng.uniform(-1, 1, (2, sp.n))
+    lam = [-0.4, 0.3]
+    Z, R = np.array([1.0, 1.0]), np.array([[0.7, 0.1, 0.05], [-0.7, -0.1, 0.05]])
+    ks = ref.KsSystem(sp, Z, R, 4)
+    rho = rng.uniform(0, 0.5, sp.n)
+    vh = rng.uniform(0, 1, sp.n)
+    tot_r, eta_r = ks.eta_total(U, lam, rho, vh, with_eta=True)
+    tot_p, eta_p = port.estimate_eta(U, lam, s, lo, hi, port.ks_reaction(Z, R, rho, vh, s))
+    assert abs(tot_p - tot_r) <= 1e-10 * tot_r
+    np.testing.assert_allclose(eta_p, eta_r, rtol=1e-10, atol=1e-12 * eta_r.max())
+    harm = lambda X, b, t: 0.5 * (X * X).sum(-1)
+    tot_r = ref.lin_eta_total(sp, U, lam, 0.5, "harmonic", c=0.5)
+    tot_p, _ = port.estimate_eta(U, lam, s, lo, hi, harm)
+    assert abs(tot_p - tot_r) <= 1e-10 * tot_r
