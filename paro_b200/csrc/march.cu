@@ -443,8 +443,9 @@ template <int MODE, bool VAR, int CB>
 __global__ void __launch_bounds__(kNT, CB <= 2 ? 3 : 2) stream_kernel(const MarchArgs a) {
   extern __shared__ __align__(16) double smem[];
   constexpr int NR = MODE == kK1 ? 2 : 3;
-  constexpr int NA = MODE == kK2 ? 2 : 1;
-  constexpr bool FMA = MODE != kApply;
+  constexpr bool SETUP = MODE == kSetupWarm || MODE == kSetupCold;
+  constexpr int NA = MODE == kK2 ? 2 : SETUP ? 3 : 1;
+  constexpr bool FMA = MODE == kK1 || MODE == kK2;
   __shared__ double red[kNT / 32][CB * NA];
 
   double* ring = smem;                    // [NR][CB][kHP]
@@ -471,6 +472,7 @@ __global__ void __launch_bounds__(kNT, CB <= 2 ? 3 : 2) stream_kernel(const Marc
         if (a.cols[c].first != 0) firstm |= 1u << j;
       }
       if (MODE == kK2) colA[j] = a.cols[c].alpha;
+      if (SETUP) colA[j] = a.scale[c];  // rhs scale lambda + sigma (paro.cpp:96-98)
     }
   }
   if (actm == 0) return;
@@ -607,10 +609,12 @@ __global__ void __launch_bounds__(kNT, CB <= 2 ? 3 : 2) stream_kernel(const Marc
   }
 
   double sC[CB], sN[CB], cCur[CB];  // row t partial, row t+1 partial, centre value of plane t
+  double mC[CB], mN[CB];            // setup: the same for the right-hand-side mass stencil
   double acc[CB][NA];
 #pragma unroll
   for (int j = 0; j < CB; ++j) {
     sC[j] = sN[j] = cCur[j] = 0.0;
+    mC[j] = mN[j] = 0.0;
 #pragma unroll
     for (int q = 0; q < NA; ++q) acc[j][q] = 0.0;
   }
@@ -652,9 +656,9 @@ __global__ void __launch_bounds__(kNT, CB <= 2 ? 3 : 2) stream_kernel(const Marc
       for (int i = 0; i < 4; ++i) cC[3 + i] = ldnc(cf + pt + offF[i]);
 #pragma unroll
       for (int i = 0; i < 4; ++i) cPp[i] = ldnc(cf + pm + offF[4 + i]);
-      if (MODE == kK2) invdP = ldnc(a.invd + pm);
+      if (MODE == kK2 || SETUP) invdP = ldnc(a.invd + pm);
     }
-    if (!VAR && MODE == kK2) invdP = a.op.invd_const;
+    if (!VAR && (MODE == kK2 || SETUP)) invdP = a.op.invd_const;
   };
   load_coefs(z0 - 1);
   for (int t = z0 - 1; t <= z1; ++t, s0 = s0 == 2 ? 0 : s0 + 1) {
@@ -714,6 +718,28 @@ __global__ void __launch_bounds__(kNT, CB <= 2 ? 3 : 2) stream_kernel(const Marc
             acc[j][0] += ctr * s;
           } else if (MODE == kK1) {
             acc[j][0] += ctr * s;  // p'q
+          } else if (SETUP) {
+            // b = (M f) * scale (paro.cpp:96-98; model.cpp:248-249) or an explicit b
+            double m = mC[j];
+            m = madd(m, a.mw[4], v00);
+            m = madd(m, a.mw[5], vp0);
+            m = madd(m, a.mw[6], v0p);
+            m = madd(m, a.mw[7], vpp);
+            const long long gw = a.ldw ? static_cast<long long>(c0 + j) * a.ldw + (u * S2 + own) : gi;
+            const double bb = a.rhs != nullptr ? a.rhs[gi] : __dmul_rn(m, colA[j]);
+            double rr;
+            if (MODE == kSetupWarm) {
+              rr = __dsub_rn(bb, s);  // r = b - A x0 (linalg.cpp:184-185)
+              a.x[gw] = ctr;          // x = x0
+            } else {
+              rr = bb;                // x0 = 0: A x0 = 0, r = b
+              a.x[gw] = 0.0;
+            }
+            a.dst[gw] = rr;
+            const double zz = __dmul_rn(invdP, rr);
+            acc[j][0] += bb * bb;
+            acc[j][1] += rr * zz;
+            acc[j][2] += rr * rr;
           } else {
             // x += alpha p ; r -= alpha q ; z = invd r  (linalg.cpp:202-206)
             const double al = colA[j];
@@ -749,6 +775,23 @@ __global__ void __launch_bounds__(kNT, CB <= 2 ? 3 : 2) stream_kernel(const Marc
         sC[j] = c;
         sN[j] = nx;
         cCur[j] = v00;
+        if (SETUP) {  // mass row sums: centre terms of row t, Pm terms of row t+1
+          double m = mN[j];
+          m = madd(m, a.mw[3], vmm);
+          m = madd(m, a.mw[2], v0m);
+          m = madd(m, a.mw[1], vm0);
+          m = madd(m, a.mw[0], v00);
+          m = madd(m, a.mw[1], vp0);
+          m = madd(m, a.mw[2], v0p);
+          m = madd(m, a.mw[3], vpp);
+          double mx = 0.0;
+          mx = madd(mx, a.mw[7], vmm);
+          mx = madd(mx, a.mw[6], v0m);
+          mx = madd(mx, a.mw[5], vm0);
+          mx = madd(mx, a.mw[4], v00);
+          mC[j] = m;
+          mN[j] = mx;
+        }
       }
     }
     if (MODE == kK1 && t + 1 <= z1) transform(t + 1, s1);
@@ -802,10 +845,10 @@ bool use_v2() {
 
 template <int MODE, bool VAR, int CB>
 void launch_t(const MarchArgs& a, cudaStream_t st) {
-  if constexpr (MODE == kApply || MODE == kK1 || MODE == kK2) {
-    // the streaming kernel takes a constant shift stencil; a variable one
-    // (inexact mesh spacing) stays on the v2 kernel
-    if (!use_v2() && a.op.mcoef == nullptr) {
+  {
+    // the streaming kernel takes constant shift / rhs-mass stencils; variable
+    // ones (inexact mesh spacing) stay on the v2 kernel
+    if (!use_v2() && a.op.mcoef == nullptr && a.mwcoef == nullptr) {
       if (VAR && a.op.sigma != 0.0) throw ParoError(kInvalidArgument, "march: shifted variable operator not preshifted");
       return launch_s<MODE, VAR, CB>(a, st);
     }
