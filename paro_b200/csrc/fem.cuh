@@ -36,14 +36,18 @@ struct Box {
   }
 };
 
-// corner offsets of tet p (cell-local, each component 0/1)
+// corner offsets of tet p (cell-local, each component 0/1). For p = (a,b,c):
+// corner 1 = e_a, corner 2 = e_a + e_b (every axis but c), corner 3 = (1,1,1);
+// computed in registers (no table lookup, no dynamically indexed array).
 __device__ __forceinline__ void tet_corners(int p, int (&t)[4][3]) {
-  t[0][0] = t[0][1] = t[0][2] = 0;
-  for (int m = 0; m < 3; ++m) {
-    t[m + 1][0] = t[m][0];
-    t[m + 1][1] = t[m][1];
-    t[m + 1][2] = t[m][2];
-    t[m + 1][kPerms[p][m]] += 1;
+  const int a = p >> 1;                 // kPerms[p][0]
+  const int c = (294 >> (2 * p)) & 3;   // kPerms[p][2]: 2,1,2,0,1,0
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    t[0][d] = 0;
+    t[1][d] = d == a ? 1 : 0;
+    t[2][d] = d == c ? 0 : 1;
+    t[3][d] = 1;
   }
 }
 
