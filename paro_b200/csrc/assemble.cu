@@ -86,9 +86,10 @@ __device__ double weight_at(const AsmArgs& a, const V3 (&P)[4], const int (&vtx)
   return eval_in_element(a.vh, a.box.s, vtx, bary) + l.v;
 }
 
-// w(x_q) of every (cell, Kuhn tet, quadrature point) of a 4-point rule, each
-// evaluated once (the dof gather below otherwise evaluates it for each of the
-// tet's 4 vertices); same floating-point operations as in the gather.
+// qw_q |e| w(x_q) of every (cell, Kuhn tet, quadrature point) of a 4-point
+// rule, each evaluated once (the dof gather below otherwise evaluates it for
+// each of the tet's 4 vertices, with the same floating-point operations), so
+// the gather of a weighted mass needs no element geometry at all.
 __global__ void __launch_bounds__(128) wtable_kernel(const AsmArgs a, double* wtab) {
   const int s = a.box.s;
   const long long ncell = static_cast<long long>(s) * s * s;
@@ -107,9 +108,13 @@ __global__ void __launch_bounds__(128) wtable_kernel(const AsmArgs a, double* wt
       vtx[i][2] = ck + tc[i][2];
       P[i] = V3{a.box.coord(vtx[i][0]), a.box.coord(vtx[i][1]), a.box.coord(vtx[i][2])};
     }
+    const double vol = tet_volume(P);
     for (int q = 0; q < a.nq; ++q) {
       const V3 x = quad_point(P, a.qp + 4 * q);
-      wtab[(cidx * 6 + p) * 4 + q] = weight_at(a, P, vtx, x);
+      const double wq = weight_at(a, P, vtx, x);
+      if (!isfinite(wq)) atomicOr(a.flags, 2);
+      // the gather's per-element factor qw[q] |e| w(x_q), same association
+      wtab[(cidx * 6 + p) * 4 + q] = a.qw[q] * vol * wq;
     }
   }
 }
@@ -139,6 +144,19 @@ __global__ void __launch_bounds__(128) assemble_kernel(const AsmArgs a) {
           for (int i = 0; i < 4; ++i)
             if (tc[i][0] == lv[0] && tc[i][1] == lv[1] && tc[i][2] == lv[2]) iv = i;
           if (iv < 0) continue;
+          double row[4] = {0.0, 0.0, 0.0, 0.0};  // local[max(iv,j)][min(iv,j)]
+          if (a.wtab) {  // weighted mass, 4-point rule: qw_q |e| w(x_q) from the table
+            const double* wt = a.wtab + ((((static_cast<long long>(ck) * s) + cj) * s + ci) * 6 + p) * 4;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const double ww = wt[q];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int hi = iv > j ? iv : j, lo = iv > j ? j : iv;
+                row[j] += ww * a.qp[4 * q + hi] * a.qp[4 * q + lo];
+              }
+            }
+          } else {
           int vtx[4][3];
           V3 P[4];
           for (int i = 0; i < 4; ++i) {
@@ -148,7 +166,6 @@ __global__ void __launch_bounds__(128) assemble_kernel(const AsmArgs a) {
             P[i] = V3{a.box.coord(vtx[i][0]), a.box.coord(vtx[i][1]), a.box.coord(vtx[i][2])};
           }
           const double vol = tet_volume(P);
-          double row[4] = {0.0, 0.0, 0.0, 0.0};  // local[max(iv,j)][min(iv,j)]
           if (a.kind == kAsmMass) {
             for (int j = 0; j < 4; ++j) row[j] = vol * (j == iv ? 2.0 : 1.0) / 20.0;
           } else if (a.kind == kAsmStiffness) {
@@ -203,9 +220,7 @@ __global__ void __launch_bounds__(128) assemble_kernel(const AsmArgs a) {
             }
             for (int q = 0; q < nq; ++q) {
               const V3 x = quad_point(P, qp + 4 * q);
-              const double wq =
-                  a.wtab ? a.wtab[((((static_cast<long long>(ck) * s) + cj) * s + ci) * 6 + p) * 4 + q]
-                         : weight_at(a, P, vtx, x);
+              const double wq = weight_at(a, P, vtx, x);
               if (!isfinite(wq)) atomicOr(a.flags, 2);
               const double ww = qw[q] * vol * wq;
               for (int j = 0; j < 4; ++j) {
@@ -213,6 +228,7 @@ __global__ void __launch_bounds__(128) assemble_kernel(const AsmArgs a) {
                 row[j] += ww * qp[4 * q + hi] * qp[4 * q + lo];
               }
             }
+          }
           }
           for (int j = 0; j < 4; ++j) {
             const int ox = tc[j][0] - tc[iv][0], oy = tc[j][1] - tc[iv][1], oz = tc[j][2] - tc[iv][2];
