@@ -119,6 +119,95 @@ __global__ void __launch_bounds__(128) wtable_kernel(const AsmArgs a, double* wt
   }
 }
 
+// Weighted-mass gather from the quadrature table with the cell / tet loops
+// unrolled at compile time: for the dof's corner lv = -(DI, DJ, DK) of cell
+// (I+DI, J+DJ, K+DK), tet P = (A, B, C) contains it as local vertex IV
+// (corners (0,0,0), e_A, (1,1,1) - e_C, (1,1,1)), so every index below is a
+// constant. Same operations and order as assemble_kernel's table branch.
+__host__ __device__ constexpr int kuhn_corner(int j, int p, int d) {
+  return j == 0 ? 0 : j == 3 ? 1 : j == 1 ? (d == (p >> 1) ? 1 : 0) : (d == ((294 >> (2 * p)) & 3) ? 0 : 1);
+}
+__host__ __device__ constexpr int kuhn_iv(int l0, int l1, int l2, int p) {
+  for (int j = 0; j < 4; ++j)
+    if (kuhn_corner(j, p, 0) == l0 && kuhn_corner(j, p, 1) == l1 && kuhn_corner(j, p, 2) == l2) return j;
+  return -1;
+}
+
+template <int DI, int DJ, int DK, int P>
+__device__ __forceinline__ void gather_tet(const AsmArgs& a, const double (&qp)[16], int I, int J, int K,
+                                           double (&acc)[kSlots]) {
+  constexpr int IV = kuhn_iv(-DI, -DJ, -DK, P);
+  if constexpr (IV >= 0) {
+    const int s = a.box.s;
+    const double* wt =
+        a.wtab + ((((static_cast<long long>(K + DK) * s) + (J + DJ)) * s + (I + DI)) * 6 + P) * 4;
+    double row[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double ww = wt[q];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int hi = IV > j ? IV : j, lo = IV > j ? j : IV;
+        row[j] += ww * qp[4 * q + hi] * qp[4 * q + lo];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int ox = kuhn_corner(j, P, 0) - kuhn_corner(IV, P, 0);
+      const int oy = kuhn_corner(j, P, 1) - kuhn_corner(IV, P, 1);
+      const int oz = kuhn_corner(j, P, 2) - kuhn_corner(IV, P, 2);
+      if (j == IV) acc[0] += row[j];
+      else if (ox >= 0 && oy >= 0 && oz >= 0) acc[ox + 2 * oy + 4 * oz] += row[j];
+    }
+  }
+}
+
+template <int DI, int DJ, int DK>
+__device__ __forceinline__ void gather_cell(const AsmArgs& a, const double (&qp)[16], int I, int J, int K,
+                                            double (&acc)[kSlots]) {
+  gather_tet<DI, DJ, DK, 0>(a, qp, I, J, K, acc);
+  gather_tet<DI, DJ, DK, 1>(a, qp, I, J, K, acc);
+  gather_tet<DI, DJ, DK, 2>(a, qp, I, J, K, acc);
+  gather_tet<DI, DJ, DK, 3>(a, qp, I, J, K, acc);
+  gather_tet<DI, DJ, DK, 4>(a, qp, I, J, K, acc);
+  gather_tet<DI, DJ, DK, 5>(a, qp, I, J, K, acc);
+}
+
+__global__ void __launch_bounds__(128) table_gather_kernel(const AsmArgs a) {
+  const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (t >= a.n) return;
+  const int s = a.box.s;
+  const long long S = s - 1;
+  const int I = static_cast<int>(t % S) + 1;
+  const int J = static_cast<int>((t / S) % S) + 1;
+  const int K = static_cast<int>(t / (S * S)) + 1;
+  double qp[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) qp[i] = __ldg(a.qp + i);
+  double acc[kSlots];
+#pragma unroll
+  for (int o = 0; o < kSlots; ++o) acc[o] = 0.0;
+  // cells in the reference's element order: (k, j, i) ascending
+  gather_cell<-1, -1, -1>(a, qp, I, J, K, acc);
+  gather_cell<0, -1, -1>(a, qp, I, J, K, acc);
+  gather_cell<-1, 0, -1>(a, qp, I, J, K, acc);
+  gather_cell<0, 0, -1>(a, qp, I, J, K, acc);
+  gather_cell<-1, -1, 0>(a, qp, I, J, K, acc);
+  gather_cell<0, -1, 0>(a, qp, I, J, K, acc);
+  gather_cell<-1, 0, 0>(a, qp, I, J, K, acc);
+  gather_cell<0, 0, 0>(a, qp, I, J, K, acc);
+#pragma unroll
+  for (int o = 0; o < kSlots; ++o) {
+    double v = acc[o];
+    if (a.kind == kAsmScf && a.vext_coef) {
+      // ks_form_matrix: a = kinetic; a += vext_mass; a += scf_mass
+      const double kin = a.kin_coef ? a.kin_coef[o * a.n + t] : a.kin_w[o];
+      v = (kin + a.vext_coef[o * a.n + t]) + v;
+    }
+    a.out[o * a.n + t] = v;
+  }
+}
+
 __global__ void __launch_bounds__(128) assemble_kernel(const AsmArgs a) {
   const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (t >= a.n) return;
@@ -340,7 +429,8 @@ void assemble(Ctx& ctx, const AssembleSpec& spec, Op& out) {
     a.wtab = wt;
   }
   const long long blocks = (g.n + 127) / 128;
-  assemble_kernel<<<static_cast<unsigned>(blocks), 128, 0, ctx.stream>>>(a);
+  if (a.wtab) table_gather_kernel<<<static_cast<unsigned>(blocks), 128, 0, ctx.stream>>>(a);
+  else assemble_kernel<<<static_cast<unsigned>(blocks), 128, 0, ctx.stream>>>(a);
   ++ctx.launches;
   PARO_CUDA(cudaGetLastError());
   int hflags = 0;
