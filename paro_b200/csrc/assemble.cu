@@ -45,6 +45,7 @@ struct AsmArgs {
   double* out = nullptr;
   int* flags = nullptr;      // bit0 singular point hit, bit1 non-finite weight
   const double* wtab = nullptr;  // 4-point rules: precomputed w(x_q) per (cell, tet, point)
+  unsigned long long* clamps = nullptr;  // Scf: count of rho(x_q) < 0
 };
 
 __device__ __forceinline__ double eval_in_element(const double* f, int s, const int (&vtx)[4][3],
@@ -57,8 +58,9 @@ __device__ __forceinline__ double eval_in_element(const double* f, int s, const 
   return v;
 }
 
-// weight function w(e, x) of the weighted-mass kinds
-__device__ double weight_at(const AsmArgs& a, const V3 (&P)[4], const int (&vtx)[4][3], V3 x) {
+// weight function w(e, x) of the weighted-mass kinds; *neg (Scf) is set when
+// the interpolated density is negative (lda_vxc clamps it, model.cpp:270-273)
+__device__ double weight_at(const AsmArgs& a, const V3 (&P)[4], const int (&vtx)[4][3], V3 x, bool* neg = nullptr) {
   if (a.kind == kAsmCoulomb) {  // external_potential, eps = 0 (model.cpp:150-162)
     double v = 0.0;
     for (int k = 0; k < a.nnuc; ++k) {
@@ -82,6 +84,7 @@ __device__ double weight_at(const AsmArgs& a, const V3 (&P)[4], const int (&vtx)
   double bary[4];
   barycentric(P, x, bary);
   const double rho_q = eval_in_element(a.rho, a.box.s, vtx, bary);
+  if (neg) *neg = rho_q < 0.0;
   const Lda l = lda_vxc(rho_q, a.exchange_only != 0, a.cx);
   return eval_in_element(a.vh, a.box.s, vtx, bary) + l.v;
 }
@@ -97,6 +100,10 @@ __global__ void __launch_bounds__(128) wtable_kernel(const AsmArgs a, double* wt
   if (cidx >= ncell) return;
   const int ci = static_cast<int>(cidx % s), cj = static_cast<int>((cidx / s) % s),
             ck = static_cast<int>(cidx / (static_cast<long long>(s) * s));
+  unsigned nneg = 0;
+  // the cell's corner coordinates, once (coord() divides by s)
+  const double x0c = a.box.coord(ci), x1c = a.box.coord(ci + 1), y0c = a.box.coord(cj), y1c = a.box.coord(cj + 1);
+  const double z0c = a.box.coord(ck), z1c = a.box.coord(ck + 1);
   for (int p = 0; p < 6; ++p) {
     int tc[4][3];
     tet_corners(p, tc);
@@ -106,17 +113,20 @@ __global__ void __launch_bounds__(128) wtable_kernel(const AsmArgs a, double* wt
       vtx[i][0] = ci + tc[i][0];
       vtx[i][1] = cj + tc[i][1];
       vtx[i][2] = ck + tc[i][2];
-      P[i] = V3{a.box.coord(vtx[i][0]), a.box.coord(vtx[i][1]), a.box.coord(vtx[i][2])};
+      P[i] = V3{tc[i][0] ? x1c : x0c, tc[i][1] ? y1c : y0c, tc[i][2] ? z1c : z0c};
     }
     const double vol = tet_volume(P);
     for (int q = 0; q < a.nq; ++q) {
       const V3 x = quad_point(P, a.qp + 4 * q);
-      const double wq = weight_at(a, P, vtx, x);
+      bool neg = false;
+      const double wq = weight_at(a, P, vtx, x, &neg);
+      nneg += neg ? 1 : 0;
       if (!isfinite(wq)) atomicOr(a.flags, 2);
       // the gather's per-element factor qw[q] |e| w(x_q), same association
       wtab[(cidx * 6 + p) * 4 + q] = a.qw[q] * vol * wq;
     }
   }
+  if (nneg && a.clamps) atomicAdd(a.clamps, static_cast<unsigned long long>(nneg));
 }
 
 // Weighted-mass gather from the quadrature table with the cell / tet loops
@@ -381,7 +391,7 @@ void assemble(Ctx& ctx, const AssembleSpec& spec, Op& out) {
   a.kind = spec.kind;
   a.scale = spec.scale;
   a.out = out.coef;
-  int* flags = flag_buf.get<int>(1);
+  int* flags = flag_buf.get<int>(4);  // [0] error bits, [2..3] clamp counter
   PARO_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), ctx.stream));
   a.flags = flags;
   const bool wmass = spec.kind != kAsmMass && spec.kind != kAsmStiffness;
@@ -421,6 +431,12 @@ void assemble(Ctx& ctx, const AssembleSpec& spec, Op& out) {
     a.vext_coef = spec.vext ? spec.vext->coef : nullptr;
     if (spec.vext && !spec.vext->var) throw ParoError(kInvalidArgument, "ks form: V_ext mass must be variable");
   }
+  unsigned long long* clamps = nullptr;
+  if (spec.kind == kAsmScf && spec.clamped) {
+    clamps = reinterpret_cast<unsigned long long*>(flags + 2);
+    PARO_CUDA(cudaMemsetAsync(clamps, 0, sizeof(unsigned long long), ctx.stream));
+    a.clamps = clamps;
+  }
   if (wmass && !singular && a.nq == 4) {
     const long long ncell = static_cast<long long>(g.s) * g.s * g.s;
     double* wt = ctx.wtab.get<double>(static_cast<size_t>(ncell) * 24);
@@ -434,8 +450,11 @@ void assemble(Ctx& ctx, const AssembleSpec& spec, Op& out) {
   ++ctx.launches;
   PARO_CUDA(cudaGetLastError());
   int hflags = 0;
+  unsigned long long hclamps = 0;
   PARO_CUDA(cudaMemcpyAsync(&hflags, flags, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  if (clamps) PARO_CUDA(cudaMemcpyAsync(&hclamps, clamps, sizeof(hclamps), cudaMemcpyDeviceToHost, ctx.stream));
   PARO_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (spec.clamped) *spec.clamped = static_cast<long long>(hclamps);
   if (hflags & 1) throw ParoError(kError, "external potential evaluated at a nucleus");
   if (hflags & 2) throw ParoError(kError, "weighted mass: non-finite coefficient");
 }

@@ -27,6 +27,7 @@ struct AssembleSpec {
   int exchange_only = 0;
   const Op* kinetic = nullptr;
   const Op* vext = nullptr;
+  long long* clamped = nullptr;  // Scf: (element, point) pairs with rho < 0 (the reference's clamp count)
 };
 
 void assemble(Ctx& ctx, const AssembleSpec& spec, Op& out);

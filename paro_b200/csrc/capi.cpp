@@ -513,8 +513,10 @@ int paro_ks_form(paro_ctx* ctx, const paro_op* kinetic, const paro_op* vext, con
     s.exchange_only = exchange_only;
     s.kinetic = &kinetic->o;
     s.vext = &vext->o;
+    long long cl = 0;
+    s.clamped = &cl;  // counted while the quadrature table is built
     assemble(ctx->c, s, out->o);
-    if (clamped) *clamped = static_cast<long long>(cell_reduce(ctx->c, kCellClamp, rho, nullptr, exchange_only));
+    if (clamped) *clamped = cl;
     return kOk;
   });
 }

@@ -88,6 +88,9 @@ __global__ void __launch_bounds__(kEstThreads) estimate_kernel(const EstArgs a) 
               ck = static_cast<int>(cidx / (static_cast<long long>(s) * s));
     // reaction at the 24 quadrature points (orbital independent)
     double react[6][4];
+    // the cell's corner coordinates, once (coord() divides by s)
+    const double x0c = a.box.coord(ci), x1c = a.box.coord(ci + 1), y0c = a.box.coord(cj), y1c = a.box.coord(cj + 1);
+    const double z0c = a.box.coord(ck), z1c = a.box.coord(ck + 1);
 #pragma unroll
     for (int p = 0; p < 6; ++p) {
       int tc[4][3];
@@ -98,7 +101,7 @@ __global__ void __launch_bounds__(kEstThreads) estimate_kernel(const EstArgs a) 
         vtx[i][0] = ci + tc[i][0];
         vtx[i][1] = cj + tc[i][1];
         vtx[i][2] = ck + tc[i][2];
-        P[i] = V3{a.box.coord(vtx[i][0]), a.box.coord(vtx[i][1]), a.box.coord(vtx[i][2])};
+        P[i] = V3{tc[i][0] ? x1c : x0c, tc[i][1] ? y1c : y0c, tc[i][2] ? z1c : z0c};
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {

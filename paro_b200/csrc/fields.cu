@@ -74,6 +74,9 @@ __global__ void __launch_bounds__(kRedThreads) cell_reduce_kernel(const CellArgs
   double acc = 0.0;
   if (c < ncell) {
     const int ci = static_cast<int>(c % s), cj = static_cast<int>((c / s) % s), ck = static_cast<int>(c / (static_cast<long long>(s) * s));
+    // the cell's corner coordinates, once (coord() divides by s)
+    const double x0c = a.box.coord(ci), x1c = a.box.coord(ci + 1), y0c = a.box.coord(cj), y1c = a.box.coord(cj + 1);
+    const double z0c = a.box.coord(ck), z1c = a.box.coord(ck + 1);
     for (int p = 0; p < 6; ++p) {
       int tc[4][3];
       tet_corners(p, tc);
@@ -84,7 +87,7 @@ __global__ void __launch_bounds__(kRedThreads) cell_reduce_kernel(const CellArgs
         vtx[i][0] = ci + tc[i][0];
         vtx[i][1] = cj + tc[i][1];
         vtx[i][2] = ck + tc[i][2];
-        P[i] = V3{a.box.coord(vtx[i][0]), a.box.coord(vtx[i][1]), a.box.coord(vtx[i][2])};
+        P[i] = V3{tc[i][0] ? x1c : x0c, tc[i][1] ? y1c : y0c, tc[i][2] ? z1c : z0c};
         fv[i] = vval(a.f, s, vtx[i][0], vtx[i][1], vtx[i][2]);
         gv[i] = a.g ? vval(a.g, s, vtx[i][0], vtx[i][1], vtx[i][2]) : 0.0;
       }
