@@ -141,3 +141,33 @@ def test_hartree_matches_reference(ref, gpu_ctx_factory):
     b = ks.op("mass").matvec(rho) * 4 * np.pi
     r = ks.op("poisson").matvec(vh) - b
     assert np.linalg.norm(r) <= 1e-12 * np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("s", [17, 20, 33])
+def test_source_step_even_and_odd_rows(ref, gpu_ctx_factory, s):
+    """Step 3 through every plane-staging path: even and odd interior row
+    length S = s - 1 (the bulk-copy K2 lays rows out with stride 38 / 37),
+    tiles that overhang the lattice in x and y, K >= 4 (bulk K2) and K = 2
+    (LDGSTS K2), against the reference at the solver tolerance."""
+    from paro_b200 import core
+
+    sp = ref.Space(s, -6.0, 6.0)
+    Z = np.array([1.0, 1.0])
+    R = np.array([[0.7, 0.0, 0.0], [-0.7, 0.0, 0.0]])
+    ks = ref.KsSystem(sp, Z, R, 2)
+    ctx = gpu_ctx_factory(sp.s, sp.lo, sp.hi)
+    mass = ks.op("mass")
+    a0 = ks.op("kinetic").copy().add_scaled(ks.op("vext"))
+    rng = np.random.default_rng(s)
+    G = rng.uniform(-1, 1, (6, sp.n))
+    lam, U, _, _ = ref.rayleigh_ritz(sp, G, a0, mass, 6)
+    ga = core.Operator.from_csr(ctx, *a0.csr())
+    gm = core.Operator.from_csr(ctx, *mass.csr())
+    tol = 1e-10
+    for k in (6, 2):
+        half, sigma = core.shifted_source_step(ga, gm, _dev(U[:k]), lam[:k], tol=tol)
+        half_ref, sigma_ref = ref.shifted_source(a0, mass, sp, U[:k], lam[:k], tol)
+        assert sigma == sigma_ref
+        h = half.cpu().numpy()
+        for c in range(k):
+            np.testing.assert_allclose(h[c], half_ref[c], rtol=0, atol=50 * tol * np.abs(half_ref[c]).max())
