@@ -1,0 +1,53 @@
+"""Run artifacts in the reference's formats, so a run of
+this driver can be diffed against `paro --config` output:
+
+  trace.csv        write_trace_csv   proj/src/runner.cpp:50-65
+                   header iter,dofs,lambda_1..N[,e_tot],eta_total,t_meshgen,t_source,t_project;
+                   values "%.12g", times "%.6f", missing values "nan"
+  eigenvalues.txt  proj/src/runner.cpp:97-101   "<i> <lambda_i %.15g>" per line
+"""
+from __future__ import annotations
+
+import math
+from pathlib import Path
+
+
+def _fmt(v, spec="%.12g") -> str:
+    """fmt (runner.cpp:15-19): C printf formatting of a double."""
+    if v is None:
+        return "nan"
+    v = float(v)
+    if math.isnan(v):
+        return "nan"
+    if math.isinf(v):
+        return "inf" if v > 0 else "-inf"
+    return spec % v
+
+
+def trace_csv(traces, n_lambdas: int, kohn_sham: bool) -> str:
+    head = "iter,dofs" + "".join(f",lambda_{i}" for i in range(1, n_lambdas + 1))
+    if kohn_sham:
+        head += ",e_tot"
+    lines = [head + ",eta_total,t_meshgen,t_source,t_project"]
+    for tr in traces:
+        row = [str(tr.iter), str(tr.dofs)]
+        row += [_fmt(tr.lambdas[i]) if i < len(tr.lambdas) else "nan" for i in range(n_lambdas)]
+        if kohn_sham:
+            row.append(_fmt(tr.e_tot))
+        # eta_total is 0 when Step 2 did not run (the reference always runs it)
+        row.append(_fmt(tr.eta_total if tr.eta_total is not None else 0.0))
+        row += [_fmt(tr.t_meshgen, "%.6f"), _fmt(tr.t_source, "%.6f"), _fmt(tr.t_project, "%.6f")]
+        lines.append(",".join(row))
+    return "\n".join(lines) + "\n"
+
+
+def eigenvalues_txt(lambdas) -> str:
+    return "".join(f"{i + 1} {_fmt(v, '%.15g')}\n" for i, v in enumerate(lambdas))
+
+
+def write_run(out_dir, traces, final_lambdas, n_lambdas: int, kohn_sham: bool) -> None:
+    """trace.csv + eigenvalues.txt under out_dir (run_experiment, runner.cpp:79-101)."""
+    d = Path(out_dir)
+    d.mkdir(parents=True, exist_ok=True)
+    (d / "trace.csv").write_text(trace_csv(traces, n_lambdas, kohn_sham))
+    (d / "eigenvalues.txt").write_text(eigenvalues_txt(final_lambdas))

@@ -195,6 +195,8 @@ class Trace:
     t_project: float
     t_total: float
     eta_total: float | None = None   # Step 2 (estimate=True): combine_max(estimate_eigen_residual).total()
+    t_meshgen: float = 0.0           # Step 2 wall time (the reference's t_meshgen column)
+    dofs: int = 0
 
 
 class ParoRun:
@@ -353,7 +355,9 @@ class ParoRun:
         t0 = time.perf_counter()
         vh_in = be.hartree(self.rho_in, out=self.vh)
         # Step 2 on a fixed mesh: the estimator only feeds eta_total (paro.cpp:521-538)
+        t2 = time.perf_counter()
         eta = be.estimate(self.orb[:N_], self.lambdas[:N_], self.rho_in, vh_in) if self.estimate else None
+        t_meshgen = time.perf_counter() - t2
         a_in, cl = be.ks_form(self.rho_in, vh_in, "in")
         self.clamped += cl
         ts = time.perf_counter()
@@ -379,7 +383,7 @@ class ParoRun:
         be.mix(self.rho_in, rho_out, w.mixing_alpha, out=self.rho_in)
         self._sync()
         return Trace(it + 1, lam[: w.n_orbitals], e_tot, res, sigma, defect, iters, t_source, t_project,
-                     time.perf_counter() - t0, eta)
+                     time.perf_counter() - t0, eta, t_meshgen, be.n)
 
     def _linear_step(self, it: int) -> Trace:
         """paro.cpp:340-354."""
@@ -387,6 +391,7 @@ class ParoRun:
         t0 = time.perf_counter()
         N_ = w.n_orbitals
         eta = be.estimate(self.orb[:N_], self.lambdas[:N_]) if self.estimate else None  # paro.cpp:306-315
+        t_meshgen = time.perf_counter() - t0
         sigma, iters = self.step3(be.form, it)
         self._sync()
         t_source = time.perf_counter() - t0
@@ -397,7 +402,7 @@ class ParoRun:
         self._sync()
         self.k, self.lambdas = orb.shape[0], lam
         return Trace(it + 1, lam[: w.n_orbitals], None, None, sigma, defect, iters, t_source,
-                     time.perf_counter() - tp, time.perf_counter() - t0, eta)
+                     time.perf_counter() - tp, time.perf_counter() - t0, eta, t_meshgen, be.n)
 
     def run(self, iterations: int | None = None):
         return [self.step(i) for i in range(iterations if iterations is not None else self.w.iterations)]
