@@ -90,7 +90,7 @@ constexpr size_t bulk_smem() {
 }
 
 template <int MODE, bool VAR, int CB, int RS>
-__global__ void __launch_bounds__(kNT, 2) bulk_kernel(const MarchArgs a) {
+__global__ void __launch_bounds__(kNT, kMinCtas) bulk_kernel(const MarchArgs a) {
   static_assert(MODE == kK1 || MODE == kK2, "bulk_kernel: PCG passes only");
   static_assert(RS == 37 || RS == 38, "row stride");
   extern __shared__ __align__(128) double smem[];

@@ -108,7 +108,7 @@ __device__ __forceinline__ void load_weights(const double* __restrict__ cf, long
 }
 
 template <int MODE, bool VAR, int CB>
-__global__ void __launch_bounds__(kNT, CB <= 2 ? 3 : 2) march_kernel(const MarchArgs a) {
+__global__ void __launch_bounds__(kNT, CB <= 2 && kMinCtas == 2 ? 3 : kMinCtas) march_kernel(const MarchArgs a) {
   extern __shared__ __align__(16) double smem[];
   constexpr int NA = Cfg<MODE>::NA;
   constexpr int NR = Cfg<MODE>::NR;
@@ -440,7 +440,7 @@ constexpr size_t stream_smem() {
 }
 
 template <int MODE, bool VAR, int CB>
-__global__ void __launch_bounds__(kNT, CB <= 2 ? 3 : 2) stream_kernel(const MarchArgs a) {
+__global__ void __launch_bounds__(kNT, CB <= 2 && kMinCtas == 2 ? 3 : kMinCtas) stream_kernel(const MarchArgs a) {
   extern __shared__ __align__(16) double smem[];
   constexpr int NR = MODE == kK1 ? 2 : 3;
   constexpr bool SETUP = MODE == kSetupWarm || MODE == kSetupCold;

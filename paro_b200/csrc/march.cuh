@@ -20,12 +20,17 @@
 namespace paro_b200 {
 
 constexpr int kTX = 32;
-constexpr int kTY = 8;
+#ifndef PARO_TILE_Y
+#define PARO_TILE_Y 8
+#endif
+constexpr int kTY = PARO_TILE_Y;
 constexpr int kNT = kTX * kTY;
 constexpr int kHX = kTX + 2;
 constexpr int kHY = kTY + 2;
 constexpr int kHP = kHX * kHY;              // halo'd plane, 340 points
 constexpr int kLoadsPerThread = (kHP + kNT - 1) / kNT;  // 2
+// resident CTAs per SM the kernels are compiled for (128 registers per thread)
+constexpr int kMinCtas = kNT >= 512 ? 1 : 2;
 
 enum MarchMode : int {
   kApply = 0,       // y = (A + sigma M) x                       [opt. x.y partial]
