@@ -242,17 +242,25 @@ __global__ void colmax_kernel(const double* V, long long ld, long long n, unsign
   if (threadIdx.x == 0 && m > 0.0) atomicMax(amax + c, static_cast<unsigned long long>(__double_as_longlong(m)));
 }
 
+// first index with |v| > 1e-12 max|v| (fix_sign, linalg.cpp:229-241): each
+// block scans one contiguous segment, low segments first, and stops as soon as
+// a lower index is already known (the pivot is usually in the first planes)
 __global__ void firstidx_kernel(const double* V, long long ld, long long n, const unsigned long long* amax,
                                 unsigned long long* first) {
+  __shared__ int stop;
   const int c = blockIdx.y;
   const double thr = 1e-12 * __longlong_as_double(static_cast<long long>(amax[c]));
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    if (static_cast<unsigned long long>(i) >= first[c]) return;
-    if (fabs(V[c * ld + i]) > thr) {
-      atomicMin(first + c, static_cast<unsigned long long>(i));
-      return;
-    }
+  const long long seg = (n + gridDim.x - 1) / gridDim.x;
+  const long long lo = blockIdx.x * seg, hi = min(n, lo + seg);
+  for (long long base = lo; base < hi; base += blockDim.x) {
+    if (threadIdx.x == 0) stop = *reinterpret_cast<volatile const unsigned long long*>(first + c) <
+                                 static_cast<unsigned long long>(base);
+    __syncthreads();
+    if (stop) return;
+    const long long i = base + threadIdx.x;
+    const bool hit = i < hi && fabs(V[c * ld + i]) > thr;
+    if (hit) atomicMin(first + c, static_cast<unsigned long long>(i));
+    if (__syncthreads_or(hit)) return;
   }
 }
 
