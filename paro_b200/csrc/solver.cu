@@ -12,6 +12,8 @@
 // the device; the host only polls an active-column count between CUDA-graph
 // chunks of iterations, keeping one chunk in flight ahead of the poll.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <vector>
@@ -237,10 +239,31 @@ void apply_op(Ctx& ctx, const Op& a, const Op* shift, double sigma, int K, const
 // Core batched PCG. On entry `cols` (host) holds tol/max_iter per column; the
 // setup pass computes r0 from either (M src)*scale (rhs == nullptr) or rhs.
 // warm: x0 = src (source solves) ; cold: x0 = 0 (Hartree).
+// PARO_PCG_TRACE=1: per-phase wall times of batched_pcg on stderr (synchronising)
+struct PhaseTrace {
+  bool on;
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t0;
+  explicit PhaseTrace(cudaStream_t s) : st(s) {
+    const char* e = std::getenv("PARO_PCG_TRACE");
+    on = e && e[0] == '1';
+    t0 = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[pcg] %-14s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
+
 void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* src, const double* rhs,
                  const double* scale_host, bool warm, double* x, long long ld, std::vector<CgColumn>& cols,
                  const Op* mass, bool abort_on_not_spd = false) {
+  PhaseTrace trace(ctx.stream);
   const OpDev op = preshift(ctx, op_in);
+  trace.mark("preshift");
   const Grid& g = ctx.grid;
   const long long n = g.n;
   cudaStream_t st = ctx.stream;
@@ -315,6 +338,7 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
   zero_marked_kernel<<<dim3(148, K), 256, 0, st>>>(dcols, K, xi, ldi, n);
   ctx.launches += 3;
   PARO_CUDA(cudaGetLastError());
+  trace.mark("setup");
 
   // iteration chunks captured once into a CUDA graph (PARO_NO_GRAPH=1 launches
   // them directly, e.g. for ncu)
@@ -361,6 +385,7 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
     PARO_CUDA(cudaGraphInstantiate(&exec, graph, 0));
     PARO_CUDA(cudaStreamDestroy(cap));
   }
+  trace.mark("graph");
   auto launch_chunk = [&] {
     if (no_graph) enqueue_chunk(st);
     else PARO_CUDA(cudaGraphLaunch(exec, st));
@@ -419,12 +444,17 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
   PARO_CUDA(cudaEventDestroy(ev[1]));
   if (exec) PARO_CUDA(cudaGraphExecDestroy(exec));
   if (graph) PARO_CUDA(cudaGraphDestroy(graph));
+  trace.mark("iterations");
   std::vector<CgColumn> before = cols;
   PARO_CUDA(cudaMemcpy(cols.data(), dcols, sizeof(CgColumn) * K, cudaMemcpyDeviceToHost));
-  for (int c = 0; c < K; ++c)
+  // an aborted batch (NotSpd: the sigma policy restarts the step) has no result to return
+  bool aborted = false;
+  for (int c = 0; c < K; ++c) aborted |= abort_on_not_spd && cols[c].status == kNotSpd;
+  for (int c = 0; c < K && !aborted; ++c)
     if (before[c].active)
       PARO_CUDA(cudaMemcpyAsync(x + c * ld, xi + c * ldi, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
   PARO_CUDA(cudaStreamSynchronize(st));
+  trace.mark("copy-out");
   double col_iters = 0.0, batch_iters = 0.0;
   for (int c = 0; c < K; ++c)
     if (before[c].active) {
