@@ -450,6 +450,9 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
   // an aborted batch (NotSpd: the sigma policy restarts the step) has no result to return
   bool aborted = false;
   for (int c = 0; c < K; ++c) aborted |= abort_on_not_spd && cols[c].status == kNotSpd;
+  if (trace.on)
+    for (int c = 0; c < K; ++c)
+      if (cols[c].status == kNotSpd) std::fprintf(stderr, "[pcg] NotSpd column %d at iteration %llu\n", c, cols[c].it);
   for (int c = 0; c < K && !aborted; ++c)
     if (before[c].active)
       PARO_CUDA(cudaMemcpyAsync(x + c * ld, xi + c * ldi, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
