@@ -413,6 +413,10 @@ __global__ void __launch_bounds__(kNT, kMinCtas) bulk_kernel(const MarchArgs a) 
       const double* st = slot_own(s0);
       const long long pdst = static_cast<long long>(c0) * ld + static_cast<long long>(t) * S2 + own;
       const int bo = bparO ^ zpar(t - 1);
+      const int so = ty * RS + tx + 1 + bo;
+      // row t-1 of column c0 in x and r; the columns follow at stride ld
+      double* xq = a.x + (pdst - S2);
+      double* rq = a.r + (pdst - S2);
 #pragma unroll
       for (int j = 0; j < CB; ++j) {
         if (!act(j)) continue;
@@ -431,13 +435,11 @@ __global__ void __launch_bounds__(kNT, kMinCtas) bulk_kernel(const MarchArgs a) 
             acc[j][0] += ctr * s;  // p'q
           } else {
             // x += alpha p ; r -= alpha q ; z = invd r  (linalg.cpp:202-206)
-            const long long gi = static_cast<long long>(c0 + j) * ld + (static_cast<long long>(t - 1) * S2 + own);
-            const int so = ty * RS + tx + 1 + bo;
             const double al = colA[j];
             const double xn = __dadd_rn(st[j * CO + so], __dmul_rn(al, ctr));
             const double rn = __dsub_rn(st[(CB + j) * CO + so], __dmul_rn(al, s));
-            a.x[gi] = xn;
-            a.r[gi] = rn;
+            xq[j * ld] = xn;
+            rq[j * ld] = rn;
             const double zz = __dmul_rn(invdP, rn);
             acc[j][0] += rn * zz;
             acc[j][1] += rn * rn;
