@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(kNT, CB <= 2 && kMinCtas == 2 ? 3 : kMinCtas) 
     double ow[kSlots], bk[kSlots], invd = 0.0;
     if (VAR && inside) load_weights(a.op.coef, n, idx, gx, gy, z, S, S2, ow, bk);
     if ((MODE == kK2 || MODE == kSetupWarm || MODE == kSetupCold) && inside)
-      invd = VAR ? __ldg(a.invd + idx) : a.op.invd_const;
+      invd = VAR ? __ldg(a.invd + (a.P ? (static_cast<long long>(z) * S + gy) * a.P + gx : idx)) : a.op.invd_const;
     cp_wait<1>();
     __syncthreads();
     if (MODE == kK1) {
@@ -378,7 +378,9 @@ __global__ void __launch_bounds__(kNT, CB <= 2 && kMinCtas == 2 ? 3 : kMinCtas) 
           }
           double rr;
           // x, r may live in the solver's padded buffers (stride ldw)
-          const long long gw = a.ldw ? static_cast<long long>(c0 + j) * a.ldw + idx : gi;
+          const long long gw =
+              a.ldw ? static_cast<long long>(c0 + j) * a.ldw + (a.P ? (static_cast<long long>(z) * S + gy) * a.P + gx : idx)
+                    : gi;
           if (MODE == kSetupWarm) {
             rr = __dsub_rn(bb, s);  // r = b - A x0 (linalg.cpp:184-185)
             a.x[gw] = ctr;          // x = x0
@@ -656,7 +658,11 @@ __global__ void __launch_bounds__(kNT, CB <= 2 && kMinCtas == 2 ? 3 : kMinCtas) 
       for (int i = 0; i < 4; ++i) cC[3 + i] = ldnc(cf + pt + offF[i]);
 #pragma unroll
       for (int i = 0; i < 4; ++i) cPp[i] = ldnc(cf + pm + offF[4 + i]);
-      if (MODE == kK2 || SETUP) invdP = ldnc(a.invd + pm);
+      // the solver's inverse diagonal may be in the row-padded layout (a.P)
+      if (MODE == kK2 || SETUP)
+        invdP = ldnc(a.invd + (a.P ? (static_cast<long long>(min(max(t - 1, 0), S - 1)) * S + (inside ? gy : 0)) * a.P +
+                                         (inside ? gx : 0)
+                                   : pm));
     }
     if (!VAR && (MODE == kK2 || SETUP)) invdP = a.op.invd_const;
   };
@@ -725,7 +731,10 @@ __global__ void __launch_bounds__(kNT, CB <= 2 && kMinCtas == 2 ? 3 : kMinCtas) 
             m = madd(m, a.mw[5], vp0);
             m = madd(m, a.mw[6], v0p);
             m = madd(m, a.mw[7], vpp);
-            const long long gw = a.ldw ? static_cast<long long>(c0 + j) * a.ldw + (u * S2 + own) : gi;
+            const long long gw =
+                a.ldw ? static_cast<long long>(c0 + j) * a.ldw +
+                            (a.P ? (static_cast<long long>(u) * S + gy) * a.P + gx : static_cast<long long>(u) * S2 + own)
+                      : gi;
             const double bb = a.rhs != nullptr ? a.rhs[gi] : __dmul_rn(m, colA[j]);
             double rr;
             if (MODE == kSetupWarm) {

@@ -15,6 +15,8 @@
 // is bit-identical to the reference CSR matvec on the same coefficients.
 #pragma once
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace paro_b200 {
@@ -76,7 +78,26 @@ struct MarchArgs {
   int with_dot = 0;              // Apply: accumulate x.y
   long long ldw = 0;             // Setup: stride of the x, r outputs (0: ld)
   int bulk = 0;                  // K1/K2: operands in padded solver buffers -> bulk-copy kernel
+  int P = 0;                     // row length of the row-padded solver layout (0: dense S);
+                                 // Setup writes x, r there, the TMA passes read/write it
 };
+
+// Row-padded solver layout (tma.cu): element (x, y, z) of a column at
+// (z*S + y)*P + x with P = S rounded up to even, so every row starts 16-byte
+// aligned and the PCG operands can be described by TMA tensor maps
+// (4-D: x, y, z, column). Points outside the lattice come back as zeros from
+// the TMA engine's out-of-bounds fill (the Dirichlet elimination).
+inline int padded_row(int S) { return S + (S & 1); }
+
+// Tensor maps of one batched PCG call's buffers (encoded once per call).
+struct PcgTma {
+  alignas(64) CUtensorMap r_halo, p0_halo, p1_halo, invd_halo, x_own, r_own;
+};
+void tma_plan(PcgTma& t, int S, long long ldi, int K, const double* r, const double* p0, const double* p1,
+              const double* x, const double* invd);
+// K1 (p_new -> a.dst; its p_old is p0 when p_is_p0) or K2 (its stencil source p is p0
+// when p_is_p0), both on the row-padded layout described by t.
+void launch_tma(int mode, bool var, int cb, const MarchArgs& a, const PcgTma& t, bool p_is_p0, cudaStream_t st);
 
 void launch_march(int mode, bool var, int cb, const MarchArgs& a, cudaStream_t st);
 // K1/K2 on padded solver buffers (bulk.cu): every vector operand is 16-byte

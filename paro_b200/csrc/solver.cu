@@ -147,13 +147,15 @@ __global__ void zero_marked_kernel(const CgColumn* cols, int K, double* x, long 
 }
 
 // inv_diag = 1 / fl(c0 + fl(sigma*m0)); flags a non-positive diagonal.
+// P > 0: written in the row-padded layout (rows of S points at stride P).
 __global__ void invd_kernel(const double* c0, double sigma, double m0, const double* m0v, long long n, double* invd,
-                            int* bad) {
+                            int* bad, int S, int P) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const double d = __dadd_rn(c0[i], __dmul_rn(sigma, m0v ? m0v[i] : m0));
     if (d <= 0.0) *bad = 1;
-    invd[i] = 1.0 / d;
+    const long long o = P > 0 ? (i / S) * P + i % S : i;
+    invd[o] = 1.0 / d;
   }
 }
 
@@ -278,14 +280,22 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
   }
   if (!var && op.mcoef) throw ParoError(kInvalidArgument, "pcg: a variable shift needs a variable operator");
   const int cb = pick_cb(K);
+  // TMA-tensor passes (tma.cu) unless the shift stencil varies per point
+  static const bool no_tma = [] {
+    const char* e = std::getenv("PARO_NO_TMA");  // experiment knob: previous (bulk/LDGSTS) passes
+    return e && e[0] == '1';
+  }();
+  const bool use_tma = !no_tma && op.mcoef == nullptr;
+  const int P = use_tma ? padded_row(g.S) : g.S;
+  const long long np = static_cast<long long>(g.S) * g.S * P;  // elements per column in the solver layout
 
   CgColumn* dcols = ctx.cols.get<CgColumn>(K);
   double* dscale = ctx.scale.get<double>(K);
   double* partials = ctx.partials.get<double>(static_cast<size_t>(K) * 3 * m.nblk);
   // the iteration vectors live in padded solver buffers (even stride ldi,
-  // kBulkPad readable margins) that the bulk-copy PCG kernels require; x is
-  // copied back to the caller's layout at the end
-  const long long ldi = ((n + 2 * kBulkPad + 31) / 32) * 32;
+  // kBulkPad readable margins; rows padded to even length on the TMA path);
+  // x is copied back to the caller's layout at the end
+  const long long ldi = ((np + 2 * kBulkPad + 31) / 32) * 32;
   auto padded = [&](DevBuf& buf, int cols) {
     return buf.get<double>(static_cast<size_t>(cols) * ldi + 2 * kBulkPad) + kBulkPad;
   };
@@ -300,7 +310,7 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
     PARO_CUDA(cudaMemset2DAsync(v + len, sizeof(double) * ldi, 0, sizeof(double) * (ldi - len), cols, st));
     PARO_CUDA(cudaMemsetAsync(v + static_cast<long long>(cols) * ldi, 0, sizeof(double) * kBulkPad, st));
   };
-  for (double* v : {r, p0, p1, xi}) zero_margins(v, K, n);
+  for (double* v : {r, p0, p1, xi}) zero_margins(v, K, np);
   int* flag = ctx.flag.get<int>(3);
 
   PARO_CUDA(cudaMemcpyAsync(dcols, cols.data(), sizeof(CgColumn) * K, cudaMemcpyHostToDevice, st));
@@ -314,8 +324,9 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
   double* invd = nullptr;
   if (var) {
     invd = padded(ctx.invd, 1);
-    zero_margins(invd, 1, n);
-    invd_kernel<<<148 * 8, 256, 0, st>>>(op.coef, op.sigma, op.m[0], op.mcoef, n, invd, flag);
+    zero_margins(invd, 1, np);
+    invd_kernel<<<148 * 8, 256, 0, st>>>(op.coef, op.sigma, op.m[0], op.mcoef, n, invd, flag, g.S,
+                                         use_tma ? P : 0);
     ++ctx.launches;
   } else {
     const double d = op.w[0] + op.sigma * op.m[0];
@@ -331,11 +342,12 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
   m.dst = r;
   m.x = xi;
   m.ldw = ldi;
+  m.P = use_tma ? P : 0;
   m.scale = dscale;
   m.rhs = rhs;
   launch_march(warm ? kSetupWarm : kSetupCold, var, cb, m, st);
   fin_kernel<<<K, kFinThreads, 0, st>>>(kFinSetup, dcols, partials, m.nblk, flag);
-  zero_marked_kernel<<<dim3(148, K), 256, 0, st>>>(dcols, K, xi, ldi, n);
+  zero_marked_kernel<<<dim3(148, K), 256, 0, st>>>(dcols, K, xi, ldi, np);
   ctx.launches += 3;
   PARO_CUDA(cudaGetLastError());
   trace.mark("setup");
@@ -347,6 +359,8 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
     const char* e = std::getenv("PARO_K1_BULK");  // experiment knob
     return e && e[0] == '1';
   }();
+  PcgTma tmaps;
+  if (use_tma) tma_plan(tmaps, g.S, ldi, K, r, p0, p1, xi, invd);
   auto enqueue_chunk = [&](cudaStream_t s) {
     for (int it = 0; it < chunk; ++it) {
       MarchArgs k1 = m;
@@ -354,9 +368,10 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
       k1.pold = (it & 1) ? p1 : p0;
       k1.dst = (it & 1) ? p0 : p1;
       k1.r = r;
-      // K1 stays on the LDGSTS streaming kernel (faster than its bulk-copy
-      // variant, profiles/r01b); K2 takes the bulk-copy kernel
-      if (op.mcoef || !k1_bulk) launch_march(kK1, var, cb, k1, s);
+      // previous generation (PARO_NO_TMA=1): K1 on the LDGSTS streaming
+      // kernel, K2 on the bulk-copy kernel
+      if (use_tma) launch_tma(kK1, var, cb, k1, tmaps, (it & 1) == 0, s);
+      else if (op.mcoef || !k1_bulk) launch_march(kK1, var, cb, k1, s);
       else launch_bulk(kK1, var, cb, k1, s);
       fin_kernel<<<K, kFinThreads, 0, s>>>(kFinK1, dcols, partials, m.nblk, flag);
       MarchArgs k2 = m;
@@ -364,7 +379,8 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
       k2.src = k1.dst;
       k2.x = xi;
       k2.r = r;
-      if (op.mcoef || K < 4) launch_march(kK2, var, cb, k2, s);  // narrow batches: LDGSTS kernel
+      if (use_tma) launch_tma(kK2, var, cb, k2, tmaps, (it & 1) != 0, s);
+      else if (op.mcoef || K < 4) launch_march(kK2, var, cb, k2, s);  // narrow batches: LDGSTS kernel
       else launch_bulk(kK2, var, cb, k2, s);
       fin_kernel<<<K, kFinThreads, 0, s>>>(kFinK2, dcols, partials, m.nblk, flag);
     }
@@ -454,8 +470,14 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
     for (int c = 0; c < K; ++c)
       if (cols[c].status == kNotSpd) std::fprintf(stderr, "[pcg] NotSpd column %d at iteration %llu\n", c, cols[c].it);
   for (int c = 0; c < K && !aborted; ++c)
-    if (before[c].active)
-      PARO_CUDA(cudaMemcpyAsync(x + c * ld, xi + c * ldi, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    if (before[c].active) {
+      if (P == g.S)
+        PARO_CUDA(cudaMemcpyAsync(x + c * ld, xi + c * ldi, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+      else  // row-padded -> dense
+        PARO_CUDA(cudaMemcpy2DAsync(x + c * ld, sizeof(double) * g.S, xi + c * ldi, sizeof(double) * P,
+                                    sizeof(double) * g.S, static_cast<size_t>(g.S) * g.S, cudaMemcpyDeviceToDevice,
+                                    st));
+    }
   PARO_CUDA(cudaStreamSynchronize(st));
   trace.mark("copy-out");
   double col_iters = 0.0, batch_iters = 0.0;

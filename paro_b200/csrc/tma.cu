@@ -1,0 +1,535 @@
+// TMA-tensor variant of the two fused Jacobi-PCG stencil passes (K1, K2) on
+// the row-padded solver layout (march.cuh: padded_row).
+//
+// Same streaming row sums as stream_kernel / bulk_kernel, but every operand
+// plane is moved by the TMA engine from a 4-D tensor map (x, y, z, column):
+// one elected thread issues one cp.async.bulk.tensor per (array, column) and
+// plane, completion is counted on an mbarrier per ring slot, and the engine's
+// out-of-bounds zero fill supplies the Dirichlet halo (fem.cpp:21-28), so no
+// thread spends issue slots on per-row copies, edge fix-ups or zero planes
+// (the per-thread bulk copies of bulk_kernel compiled to a uniform-register
+// waterfall on 4 of the 8 warps, which then gated every barrier).
+//
+// K2 also writes x and r back with TMA tensor stores: the own-point rows of
+// x and r land in a 4-slot ring, are updated in place, fenced to the async
+// proxy and stored by the elected thread one step later.
+//
+// Arithmetic is identical to bulk_kernel (same FMA row sums, same update
+// formulas, linalg.cpp:179, 202-210), so results do not depend on the variant.
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <mutex>
+
+#include "march.cuh"
+
+namespace paro_b200 {
+
+namespace {
+
+__device__ __forceinline__ unsigned su32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT%=;\n"
+      "}\n" ::"r"(su32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// global -> shared tile of a 4-D tensor map; completes tx bytes on bar
+__device__ __forceinline__ void tma_load(double* dst, const CUtensorMap* map, int x, int y, int z, int c,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];\n" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(z), "r"(c), "r"(su32(bar))
+      : "memory");
+}
+// shared -> global tile (out-of-bounds elements are not written)
+__device__ __forceinline__ void tma_store(const CUtensorMap* map, int x, int y, int z, int c, const double* src) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];\n" ::"l"(
+                   reinterpret_cast<unsigned long long>(map)),
+               "r"(x), "r"(y), "r"(z), "r"(c), "r"(su32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ double ldnc(const double* p) {
+  double v;
+  asm volatile("ld.global.f64 %0, [%1];\n" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// The inner (x) start of a tensor box must be 16-byte aligned (an odd
+// double offset faults with an illegal instruction), so the halo'd box is
+// 36 x 10 from (x0 - 2, y0 - 1): element x = x0 - 1 + hx of halo row hy sits
+// at hy * kRW + hx + 1.
+constexpr int kRW = 36;                          // halo'd box row width
+constexpr int kHR = kRW * kHY;                   // 360 doubles per halo'd box
+constexpr int kHB = 368;                         // slot stride (128-byte aligned)
+constexpr unsigned kHaloBytes = kHR * 8;
+constexpr unsigned kOwnBytes = kNT * 8;          // 32 x 8 box
+constexpr int kNP = 3;                           // halo'd plane ring
+constexpr int kNX = 4;                           // K2 own-row ring (in-place update + store)
+
+// Each tensor map is its own __grid_constant__ parameter (wrapped in a struct
+// the descriptors faulted with an illegal instruction on this driver).
+// K1: ma = r, mb = p_old, mc = invd (halo'd boxes); K2: ma = p (halo'd box),
+// mb = x, mc = r (own-row boxes).
+
+// doubles of operand data (planes + own rows / p_new ring)
+template <int MODE, int CB>
+constexpr int tma_data() {
+  if (MODE == kK2) return kNP * CB * kHB + kNX * 2 * CB * kNT;
+  return kNP * (2 * CB + 1) * kHB + 2 * CB * kHR;
+}
+// bytes: alignment slack + data + mbarriers + block-reduction scratch
+template <int MODE, int CB>
+constexpr size_t tma_smem() {
+  return 128 + sizeof(double) * (tma_data<MODE, CB>() + kNP + kNX + (kNT / 32) * CB * (MODE == kK2 ? 2 : 1));
+}
+
+template <int MODE, bool VAR, int CB>
+__global__ void __launch_bounds__(kNT, kMinCtas) tma_kernel(const MarchArgs a, const __grid_constant__ CUtensorMap ma,
+                                                                const __grid_constant__ CUtensorMap mb,
+                                                                const __grid_constant__ CUtensorMap mc) {
+  static_assert(MODE == kK1 || MODE == kK2, "tma_kernel: PCG passes only");
+  static_assert(kTX == 32 && kTY == 8, "tma_kernel: 32x8 tiles");
+  // everything in dynamic shared memory, base rounded up to the 128 bytes the
+  // tensor copies need (tma_smem() reserves the slack)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  constexpr int NA = MODE == kK2 ? 2 : 1;
+  constexpr int NARR = MODE == kK1 ? 2 * CB + 1 : CB;  // halo'd arrays per plane slot
+  unsigned long long* barP = reinterpret_cast<unsigned long long*>(smem + tma_data<MODE, CB>());
+  unsigned long long* barX = barP + kNP;
+  double(*red)[CB * NA] = reinterpret_cast<double(*)[CB * NA]>(barX + kNX);
+
+  double* planes = smem;                       // [kNP][NARR][kHB]
+  double* extra = planes + kNP * NARR * kHB;   // K2: own rows [kNX][2][CB][kNT]; K1: p_new ring [2][CB][kHR]
+
+  const int S = a.S;
+  const int S2 = S * S;
+  const int P = a.P;
+  const long long n = a.n;
+  const long long ld = a.ld;
+  const int tid = threadIdx.x;
+  const int blk = blockIdx.y;
+  const int c0 = blockIdx.x * CB;
+
+  unsigned actm = 0, firstm = 0;
+  int nact = 0, nnf = 0;
+  double colA[CB], colB[CB];
+#pragma unroll
+  for (int j = 0; j < CB; ++j) {
+    const int c = c0 + j;
+    const bool on = c < a.K && a.cols[c].active != 0;
+    colA[j] = colB[j] = 0.0;
+    if (on) {
+      actm |= 1u << j;
+      ++nact;
+      bool f = false;
+      if (MODE == kK1) {
+        colB[j] = a.cols[c].beta;
+        f = a.cols[c].first != 0;
+        if (f) firstm |= 1u << j;
+      }
+      if (!f) ++nnf;
+      if (MODE == kK2) colA[j] = a.cols[c].alpha;
+    }
+  }
+  if (actm == 0) return;
+  auto act = [&](int j) { return (actm >> j) & 1u; };
+  auto first = [&](int j) { return (firstm >> j) & 1u; };
+
+  const int bx = blk % a.nTX;
+  const int by = (blk / a.nTX) % a.nTY;
+  const int bz = blk / (a.nTX * a.nTY);
+  const int x0 = bx * kTX, y0 = by * kTY;
+  const int z0 = bz * a.ZC;
+  const int z1 = min(S, z0 + a.ZC);
+  const int tx = tid % kTX, ty = tid / kTX;
+  const int gx = x0 + tx, gy = y0 + ty;
+  const bool inside = gx < S && gy < S;
+
+  if (tid == 0) {
+    for (int s = 0; s < kNP; ++s) mbar_init(&barP[s], 1);
+    if (MODE == kK2)
+      for (int s = 0; s < kNX; ++s) mbar_init(&barX[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto slot_planes = [&](int s) { return planes + s * NARR * kHB; };
+  auto slot_own = [&](int s) { return extra + s * 2 * CB * kNT; };  // K2: [2][CB][kNT]
+  // elected thread: halo'd plane z (zero-filled outside the lattice) into slot s
+  auto issue_halo = [&](int s, int z) {
+    const unsigned arrays = MODE == kK1 ? nact + nnf + (VAR ? 1 : 0) : nact;
+    mbar_arm(&barP[s], arrays * kHaloBytes);
+    double* d = slot_planes(s);
+#pragma unroll
+    for (int j = 0; j < CB; ++j) {
+      if (!act(j)) continue;
+      tma_load(d + j * kHB, &ma, x0 - 2, y0 - 1, z, c0 + j, &barP[s]);
+      if (MODE == kK1 && !first(j)) tma_load(d + (CB + j) * kHB, &mb, x0 - 2, y0 - 1, z, c0 + j, &barP[s]);
+    }
+    if (MODE == kK1 && VAR) tma_load(d + 2 * CB * kHB, &mc, x0 - 2, y0 - 1, z, 0, &barP[s]);
+  };
+  // K2 elected thread: own rows of x and r on plane z into own slot s
+  auto issue_own = [&](int s, int z) {
+    mbar_arm(&barX[s], 2u * nact * kOwnBytes);
+    double* d = slot_own(s);
+#pragma unroll
+    for (int j = 0; j < CB; ++j) {
+      if (!act(j)) continue;
+      tma_load(d + j * kNT, &mb, x0, y0, z, c0 + j, &barX[s]);
+      tma_load(d + (CB + j) * kNT, &mc, x0, y0, z, c0 + j, &barX[s]);
+    }
+  };
+  auto store_own = [&](int s, int z) {
+    const double* d = slot_own(s);
+#pragma unroll
+    for (int j = 0; j < CB; ++j) {
+      if (!act(j)) continue;
+      tma_store(&mb, x0, y0, z, c0 + j, d + j * kNT);
+      tma_store(&mc, x0, y0, z, c0 + j, d + (CB + j) * kNT);
+    }
+    bulk_commit();
+  };
+
+  // K1: raw plane slot s (plane z) -> p_new = z + beta p_old into ring slot rg
+  int hpos[kLoadsPerThread];  // box offset of the halo'd positions this thread transforms (-1: none)
+#pragma unroll
+  for (int l = 0; l < kLoadsPerThread; ++l) {
+    const int i = tid + l * kNT;
+    hpos[l] = i < kHP ? (i / kHX) * kRW + i % kHX + 1 : -1;
+  }
+  auto transform = [&](int s, int rg) {
+    const double* rw = slot_planes(s);
+    double* ring = extra + rg * CB * kHR;
+#pragma unroll
+    for (int l = 0; l < kLoadsPerThread; ++l) {
+      const int i = hpos[l];
+      if (i < 0) continue;
+      const double d = VAR ? rw[2 * CB * kHB + i] : a.op.invd_const;
+#pragma unroll
+      for (int j = 0; j < CB; ++j) {
+        // z = inv_diag * r ; p = z + beta * p   (linalg.cpp:179, 210); zero outside the lattice
+        const double zz = __dmul_rn(d, rw[j * kHB + i]);
+        ring[j * kHR + i] = first(j) ? zz : __dadd_rn(zz, __dmul_rn(colB[j], rw[(CB + j) * kHB + i]));
+      }
+    }
+  };
+
+  // coefficient offsets (dense layout, see stream_kernel)
+  long long offB[kSlots], offF[kSlots];
+#pragma unroll
+  for (int o = 0; o < kSlots; ++o) {
+    offF[o] = o * n;
+    offB[o] = o * n - (o & 1) - ((o >> 1) & 1) * S;
+  }
+  const int ownc = inside ? gy * S + gx : 0;
+  const int ownp = inside ? gy * P + gx : 0;
+  double cN[4], cC[7], cPp[4], invdP = 0.0;
+  auto load_coefs = [&](int t) {
+    if (VAR) {
+      const int tc = min(max(t, 0), S - 1), tm1 = min(max(t - 1, 0), S - 1);
+      const long long pt = static_cast<long long>(tc) * S2 + ownc;
+      const long long pm = static_cast<long long>(tm1) * S2 + ownc;
+      const double* cf = a.op.coef;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cN[i] = ldnc(cf + pt + offB[4 + i]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) cC[i] = ldnc(cf + pt + offB[1 + i]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cC[3 + i] = ldnc(cf + pt + offF[i]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cPp[i] = ldnc(cf + pm + offF[4 + i]);
+      if (MODE == kK2) invdP = ldnc(a.invd + static_cast<long long>(tm1) * S * P + ownp);
+    } else {  // constant operator: fl(w + fl(sigma m)) from the host
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cN[i] = a.op.wc[4 + i];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) cC[i] = a.op.wc[1 + i];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cC[3 + i] = a.op.wc[i];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cPp[i] = a.op.wc[4 + i];
+      if (MODE == kK2) invdP = a.op.invd_const;
+    }
+  };
+
+  double sC[CB], sN[CB], cCur[CB];
+  double acc[CB][NA];
+#pragma unroll
+  for (int j = 0; j < CB; ++j) {
+    sC[j] = sN[j] = cCur[j] = 0.0;
+#pragma unroll
+    for (int q = 0; q < NA; ++q) acc[j][q] = 0.0;
+  }
+  unsigned phP = 0, phX = 0;  // bit s: parity of the next completion of barP[s] / barX[s]
+  auto waitP = [&](int s) {
+    mbar_wait(&barP[s], (phP >> s) & 1u);
+    phP ^= 1u << s;
+  };
+  auto waitX = [&](int s) {
+    mbar_wait(&barX[s], (phX >> s) & 1u);
+    phX ^= 1u << s;
+  };
+  // ring slots: halo'd plane t -> (t - z0 + 1) % kNP; own row u -> (u - z0) % kNX; p_new ring (K1) -> (t - z0 + 1) & 1
+  auto sp = [&](int t) { return (t - z0 + 1) % kNP; };
+  auto sx = [&](int u) { return (u - z0) & (kNX - 1); };
+
+  // ---- prologue
+  if (MODE == kK1) {
+    if (tid == 0) {
+      issue_halo(0, z0 - 1);
+      issue_halo(1, z0);
+      issue_halo(2, z0 + 1);
+    }
+    waitP(0);
+    transform(0, 0);
+  } else {
+    if (tid == 0) {
+      issue_halo(0, z0 - 1);
+      issue_halo(1, z0);
+    }
+  }
+  load_coefs(z0 - 1);
+
+  const int ib = ty * kRW + tx + 1;  // top-left of the 3x3 window in a halo'd box
+  for (int t = z0 - 1; t <= z1; ++t) {
+    const bool rowP = t - 1 >= z0;  // row t-1 completes at this step
+    if (MODE == kK1) {
+      if (t + 1 <= z1) waitP(sp(t + 1));  // raw plane t+1 landed
+    } else {
+      waitP(sp(t));                        // halo'd p plane t landed
+      if (rowP) waitX(sx(t - 1));          // own rows x, r of row t-1 landed
+    }
+    __syncthreads();  // every thread is done with step t-1 (its slots may be refilled / stored)
+    if (tid == 0) {
+      if (MODE == kK1) {
+        if (t + 3 <= z1) issue_halo(sp(t), t + 3);  // sp(t+3) == sp(t)
+      } else {
+        if (t - 2 >= z0) store_own(sx(t - 2), t - 2);  // row t-2, updated at step t-1
+        if (t + 1 < z1) {
+          if (t + 1 - kNX >= z0) bulk_wait_read<1>();   // the slot's previous row has been stored
+          issue_own(sx(t + 1), t + 1);
+        }
+        if (t + 2 <= z1) issue_halo(sp(t + 2), t + 2);  // sp(t+2) == sp(t-1)
+      }
+    }
+
+    if (inside) {
+      const double* Pl = MODE == kK1 ? extra + ((t - z0 + 1) & 1) * CB * kHR : slot_planes(sp(t));
+      constexpr int PS = MODE == kK1 ? kHR : kHB;  // per-column stride of the stencil source
+      constexpr int R = kRW;
+      double* st = MODE == kK2 ? slot_own(sx(t - 1 >= z0 ? t - 1 : z0)) : nullptr;
+      // p_new rows of plane t go to global (K1)
+      const long long pdst = static_cast<long long>(c0) * ld + (static_cast<long long>(t) * S + gy) * P + gx;
+#pragma unroll
+      for (int j = 0; j < CB; ++j) {
+        const double* Pj = Pl + j * PS + ib;
+        const double vmm = Pj[0], v0m = Pj[1], vm0 = Pj[R], v00 = Pj[R + 1];
+        const double vp0 = Pj[R + 2], v0p = Pj[2 * R + 1], vpp = Pj[2 * R + 2];
+        if (MODE == kK1 && t >= z0 && t < z1 && act(j)) a.dst[pdst + static_cast<long long>(j) * ld] = v00;
+        if (rowP) {  // Pp terms of row t-1: A[v, v+o], o = 4..7
+          double s = sC[j];
+          s = fma(cPp[0], v00, s);
+          s = fma(cPp[1], vp0, s);
+          s = fma(cPp[2], v0p, s);
+          s = fma(cPp[3], vpp, s);
+          const double ctr = cCur[j];
+          if (MODE == kK1) {
+            acc[j][0] = fma(ctr, s, acc[j][0]);  // p'q
+          } else {
+            // x += alpha p ; r -= alpha q ; z = invd r  (linalg.cpp:202-206)
+            const double al = colA[j];
+            double* xs = st + j * kNT + tid;
+            double* rs = st + (CB + j) * kNT + tid;
+            const double xn = __dadd_rn(*xs, __dmul_rn(al, ctr));
+            const double rn = __dsub_rn(*rs, __dmul_rn(al, s));
+            *xs = xn;
+            *rs = rn;
+            const double zz = __dmul_rn(invdP, rn);
+            acc[j][0] = fma(rn, zz, acc[j][0]);
+            acc[j][1] = fma(rn, rn, acc[j][1]);
+          }
+        }
+        // centre terms of row t, Pm terms of row t+1 (see stream_kernel)
+        double c = sN[j];
+        c = fma(cC[2], vmm, c);
+        c = fma(cC[1], v0m, c);
+        c = fma(cC[0], vm0, c);
+        c = fma(cC[3], v00, c);
+        c = fma(cC[4], vp0, c);
+        c = fma(cC[5], v0p, c);
+        c = fma(cC[6], vpp, c);
+        double nx = 0.0;
+        nx = fma(cN[3], vmm, nx);
+        nx = fma(cN[2], v0m, nx);
+        nx = fma(cN[1], vm0, nx);
+        nx = fma(cN[0], v00, nx);
+        sC[j] = c;
+        sN[j] = nx;
+        cCur[j] = v00;
+      }
+    }
+    // generic-proxy writes of the own rows must be visible to the TMA store
+    if (MODE == kK2 && rowP) fence_async_smem();
+    if (MODE == kK1 && t + 1 <= z1) transform(sp(t + 1), (t - z0 + 2) & 1);
+    if (t < z1) load_coefs(t + 1);
+  }
+  if (MODE == kK2) {
+    __syncthreads();
+    if (tid == 0) {
+      store_own(sx(z1 - 1), z1 - 1);
+      bulk_wait<0>();
+    }
+  }
+
+  const int warp = tid >> 5, lane = tid & 31;
+#pragma unroll
+  for (int j = 0; j < CB; ++j)
+#pragma unroll
+    for (int q = 0; q < NA; ++q) {
+      const double v = warp_sum(acc[j][q]);
+      if (lane == 0) red[warp][j * NA + q] = v;
+    }
+  __syncthreads();
+  if (tid < CB * NA) {
+    const int j = tid / NA, q = tid % NA;
+    if (act(j)) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kNT / 32; ++w) s += red[w][tid];
+      a.partials[(static_cast<long long>(c0 + j) * 3 + q) * a.nblk + blk] = s;
+    }
+  }
+}
+
+struct Maps {
+  CUtensorMap a, b, c;
+};
+
+template <int MODE, bool VAR, int CB>
+void launch_k(const MarchArgs& a, const Maps& m, cudaStream_t st) {
+  const int groups = (a.K + CB - 1) / CB;
+  constexpr size_t sm = tma_smem<MODE, CB>();
+  static std::once_flag once;
+  std::call_once(once, [] {
+    PARO_CUDA(cudaFuncSetAttribute(tma_kernel<MODE, VAR, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(sm)));
+  });
+  dim3 grid(groups, a.nblk);
+  tma_kernel<MODE, VAR, CB><<<grid, kNT, sm, st>>>(a, m.a, m.b, m.c);
+  PARO_CUDA(cudaGetLastError());
+}
+
+template <int MODE, bool VAR>
+void launch_cb(int cb, const MarchArgs& a, const Maps& m, cudaStream_t st) {
+  static const int forced = [] {
+    const char* e = std::getenv("PARO_MARCH_CB");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced > 0 && cb > forced) cb = forced;
+  switch (cb) {
+    case 1: launch_k<MODE, VAR, 1>(a, m, st); break;
+    case 2: launch_k<MODE, VAR, 2>(a, m, st); break;
+    default: launch_k<MODE, VAR, 4>(a, m, st); break;
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    PARO_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    if (f == nullptr || q != cudaDriverEntryPointSuccess)
+      throw ParoError(kCuda, "tma: cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// 4-D map (x, y, z, column) of a row-padded buffer with box (bx, by, 1, 1)
+void encode(CUtensorMap& m, const double* base, int S, long long ldi, int cols, int bx, int by) {
+  const int P = padded_row(S);
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(S),
+                              static_cast<cuuint64_t>(cols)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(P) * 8, static_cast<cuuint64_t>(S) * P * 8,
+                                 static_cast<cuuint64_t>(ldi) * 8};
+  const cuuint32_t box[4] = {static_cast<cuuint32_t>(bx), static_cast<cuuint32_t>(by), 1, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides, box,
+                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw ParoError(kCuda, "tma: cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+}
+
+}  // namespace
+
+void tma_plan(PcgTma& t, int S, long long ldi, int K, const double* r, const double* p0, const double* p1,
+              const double* x, const double* invd) {
+  if ((ldi & 1) != 0) throw ParoError(kInvalidArgument, "tma: column stride must be even");
+  encode(t.r_halo, r, S, ldi, K, kRW, kHY);
+  encode(t.p0_halo, p0, S, ldi, K, kRW, kHY);
+  encode(t.p1_halo, p1, S, ldi, K, kRW, kHY);
+  encode(t.x_own, x, S, ldi, K, kTX, kTY);
+  encode(t.r_own, r, S, ldi, K, kTX, kTY);
+  if (invd) encode(t.invd_halo, invd, S, ldi, 1, kRW, kHY);
+  else t.invd_halo = t.r_halo;
+}
+
+void launch_tma(int mode, bool var, int cb, const MarchArgs& a, const PcgTma& t, bool p_is_p0, cudaStream_t st) {
+  if (a.n > (1ll << 31) - 1) throw ParoError(kCapacity, "tma: more than 2^31 interior dofs per column");
+  if (a.P != padded_row(a.S)) throw ParoError(kInvalidArgument, "tma: operands must use the row-padded layout");
+  if (var && a.op.sigma != 0.0) throw ParoError(kInvalidArgument, "tma: shifted variable operator not preshifted");
+  if (a.op.mcoef != nullptr) throw ParoError(kInvalidArgument, "tma: variable shift stencil unsupported");
+  Maps m;
+  if (mode == kK1) {
+    m.a = t.r_halo;
+    m.b = p_is_p0 ? t.p0_halo : t.p1_halo;
+    m.c = t.invd_halo;
+    if (var) launch_cb<kK1, true>(cb, a, m, st);
+    else launch_cb<kK1, false>(cb, a, m, st);
+  } else if (mode == kK2) {
+    m.a = p_is_p0 ? t.p0_halo : t.p1_halo;
+    m.b = t.x_own;
+    m.c = t.r_own;
+    if (var) launch_cb<kK2, true>(cb, a, m, st);
+    else launch_cb<kK2, false>(cb, a, m, st);
+  } else {
+    throw ParoError(kInvalidArgument, "tma: mode must be K1 or K2");
+  }
+}
+
+}  // namespace paro_b200
