@@ -80,7 +80,7 @@ int paro_ctx_destroy(paro_ctx* ctx) {
   cudaStreamSynchronize(ctx->c.stream);
   for (DevBuf* b : {&ctx->c.partials, &ctx->c.cols, &ctx->c.scale, &ctx->c.invd, &ctx->c.pbuf0, &ctx->c.pbuf1,
                     &ctx->c.flag, &ctx->c.ws_a, &ctx->c.ws_b, &ctx->c.ws_c, &ctx->c.ws_d, &ctx->c.ws_e,
-                    &ctx->c.ws_small, &ctx->c.ws_small2, &ctx->c.dst_tab, &ctx->c.wtab, &ctx->c.shifted, &ctx->c.pcg_x, &ctx->c.ws_gram,
+                    &ctx->c.ws_small, &ctx->c.ws_small2, &ctx->c.dst_tab, &ctx->c.wtab, &ctx->c.shifted, &ctx->c.coefp, &ctx->c.pcg_x, &ctx->c.ws_gram,
                     &ctx->c.ws_small3})
     b->release();
   if (ctx->c.cublas) cublasDestroy(ctx->c.cublas);

@@ -64,6 +64,7 @@ struct Ctx {
   DevBuf ws_gram;                    // split-K partial Grams
   DevBuf pcg_x;                      // PCG iterate in the padded solver layout
   DevBuf shifted;                    // (A + sigma M) coefficients of the current shifted solve
+  DevBuf coefp;                      // the same in the row-padded layout (TMA staging in the PCG passes)
   int* pinned_count = nullptr;       // mapped host memory for the active-column poll
   int* pinned_count_dev = nullptr;
 

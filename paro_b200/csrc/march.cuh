@@ -91,10 +91,14 @@ inline int padded_row(int S) { return S + (S & 1); }
 
 // Tensor maps of one batched PCG call's buffers (encoded once per call).
 struct PcgTma {
-  alignas(64) CUtensorMap r_halo, p0_halo, p1_halo, invd_halo, x_own, r_own;
+  alignas(64) CUtensorMap r_halo, p0_halo, p1_halo, invd_halo, invd_own, x_own, r_own, coef_box;
+  CUtensorMap r_fwd, p0_fwd, p1_fwd, invd_fwd, coef_own;  // one-sided (forward) boxes of K1 (k1f_kernel)
+  bool has_coef = false;  // coef_box: the operator's 8 coefficient slots in the row-padded layout
 };
+// coefp (optional): the 8 coefficient slots of a variable operator in the
+// row-padded layout at stride ldi (K2 then stages them by TMA, k2c_kernel)
 void tma_plan(PcgTma& t, int S, long long ldi, int K, const double* r, const double* p0, const double* p1,
-              const double* x, const double* invd);
+              const double* x, const double* invd, const double* coefp);
 // K1 (p_new -> a.dst; its p_old is p0 when p_is_p0) or K2 (its stencil source p is p0
 // when p_is_p0), both on the row-padded layout described by t.
 void launch_tma(int mode, bool var, int cb, const MarchArgs& a, const PcgTma& t, bool p_is_p0, cudaStream_t st);

@@ -161,6 +161,17 @@ __global__ void invd_kernel(const double* c0, double sigma, double m0, const dou
 
 __global__ void set_flag_kernel(int* flag, int v) { *flag = v; }
 
+// 8 coefficient slots (dense, slot o at o*n) -> row-padded layout, slot o at o*ldi
+__global__ void pad_coef_kernel(const double* __restrict__ coef, long long n, int S, int P, long long ldi,
+                                double* __restrict__ out) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long o = (i / S) * P + i % S;
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) out[k * ldi + o] = coef[k * n + i];
+  }
+}
+
 struct Slots8 {
   double v[kSlots];
 };
@@ -360,7 +371,16 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
     return e && e[0] == '1';
   }();
   PcgTma tmaps;
-  if (use_tma) tma_plan(tmaps, g.S, ldi, K, r, p0, p1, xi, invd);
+  if (use_tma) {
+    double* coefp = nullptr;
+    if (var) {  // the operator's coefficients in the row-padded layout for K2's TMA staging
+      coefp = ctx.coefp.get<double>(static_cast<size_t>(kSlots) * ldi);
+      pad_coef_kernel<<<148 * 8, 256, 0, st>>>(op.coef, n, g.S, P, ldi, coefp);
+      PARO_CUDA(cudaGetLastError());
+      ++ctx.launches;
+    }
+    tma_plan(tmaps, g.S, ldi, K, r, p0, p1, xi, invd, coefp);
+  }
   auto enqueue_chunk = [&](cudaStream_t s) {
     for (int it = 0; it < chunk; ++it) {
       MarchArgs k1 = m;

@@ -436,6 +436,411 @@ __global__ void __launch_bounds__(kNT, kMinCtas) tma_kernel(const MarchArgs a, c
   }
 }
 
+// ---------------------------------------------------------------------------
+// K2 for a variable operator with the coefficients staged by TMA as well
+// (k2c). The 16 per-thread coefficient loads per plane of tma_kernel were
+// the largest cost of the PCG iteration (a constant-coefficient operator,
+// same kernels otherwise, runs 27 % faster): here one box per plane brings
+// the 8 slots of the (A + sigma M) coefficients with their (-1,-1) halo and
+// one box the inverse diagonal, all into the ring slot of the p plane, so
+// the thread reads them from shared memory. x and r stay in registers: the
+// own rows of row t are loaded at step t and updated at step t+1.
+constexpr int kCS = kSlots * kHR + kNT;  // coefficient slot: [8][10][36] boxes + inverse-diagonal own box [8][32]
+
+template <int CB>
+constexpr int k2c_data() {
+  return kNP * CB * kHB + kNP * kCS;
+}
+template <int CB>
+constexpr size_t k2c_smem() {
+  return 128 + sizeof(double) * (k2c_data<CB>() + kNP + (kNT / 32) * CB * 2);
+}
+
+template <int CB>
+__global__ void __launch_bounds__(kNT, kMinCtas)
+    k2c_kernel(const MarchArgs a, const __grid_constant__ CUtensorMap mp, const __grid_constant__ CUtensorMap mcoef,
+               const __grid_constant__ CUtensorMap minvd) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* smem = reinterpret_cast<double*>(smem_raw + ((128u - (su32(smem_raw) & 127u)) & 127u));
+  double* planes = smem;                       // [kNP][CB][kHB]
+  double* coefs = planes + kNP * CB * kHB;     // [kNP][kCS]
+  unsigned long long* barP = reinterpret_cast<unsigned long long*>(smem + k2c_data<CB>());
+  double(*red)[CB * 2] = reinterpret_cast<double(*)[CB * 2]>(barP + kNP);
+
+  const int S = a.S;
+  const int P = a.P;
+  const long long ld = a.ld;
+  const int tid = threadIdx.x;
+  const int blk = blockIdx.y;
+  const int c0 = blockIdx.x * CB;
+
+  unsigned actm = 0;
+  int nact = 0;
+  double colA[CB];
+#pragma unroll
+  for (int j = 0; j < CB; ++j) {
+    const int c = c0 + j;
+    const bool on = c < a.K && a.cols[c].active != 0;
+    colA[j] = 0.0;
+    if (on) {
+      actm |= 1u << j;
+      ++nact;
+      colA[j] = a.cols[c].alpha;
+    }
+  }
+  if (actm == 0) return;
+  auto act = [&](int j) { return (actm >> j) & 1u; };
+
+  const int bx = blk % a.nTX;
+  const int by = (blk / a.nTX) % a.nTY;
+  const int bz = blk / (a.nTX * a.nTY);
+  const int x0 = bx * kTX, y0 = by * kTY;
+  const int z0 = bz * a.ZC;
+  const int z1 = min(S, z0 + a.ZC);
+  const int tx = tid % kTX, ty = tid / kTX;
+  const int gx = x0 + tx, gy = y0 + ty;
+  const bool inside = gx < S && gy < S;
+
+  if (tid == 0) {
+    for (int s = 0; s < kNP; ++s) mbar_init(&barP[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](int s, int z) {  // thread 0: p, coefficient and inverse-diagonal planes z into slot s
+    mbar_arm(&barP[s], nact * kHaloBytes + (kSlots * kHR + kNT) * 8u);
+    double* d = planes + s * CB * kHB;
+#pragma unroll
+    for (int j = 0; j < CB; ++j)
+      if (act(j)) tma_load(d + j * kHB, &mp, x0 - 2, y0 - 1, z, c0 + j, &barP[s]);
+    double* cf = coefs + s * kCS;
+    tma_load(cf, &mcoef, x0 - 2, y0 - 1, z, 0, &barP[s]);
+    tma_load(cf + kSlots * kHR, &minvd, x0, y0, z, 0, &barP[s]);
+  };
+  unsigned phP = 0;
+  auto waitP = [&](int s) {
+    mbar_wait(&barP[s], (phP >> s) & 1u);
+    phP ^= 1u << s;
+  };
+  auto sp = [&](int t) { return (t - z0 + 1) % kNP; };
+
+  if (tid == 0) {
+    issue(0, z0 - 1);
+    issue(1, z0);
+  }
+
+  double sC[CB], sN[CB], cCur[CB], acc[CB][2];
+  double xc[CB], rc[CB];  // own x, r of row t-1
+#pragma unroll
+  for (int j = 0; j < CB; ++j) {
+    sC[j] = sN[j] = cCur[j] = 0.0;
+    acc[j][0] = acc[j][1] = 0.0;
+    xc[j] = rc[j] = 0.0;
+  }
+  double cPp[4] = {0.0, 0.0, 0.0, 0.0}, invdP = 0.0;  // own slots 4..7 and 1/diag of plane t-1
+  const int o0 = (ty + 1) * kRW + tx + 2;               // own point in a coefficient box
+  const int ib = ty * kRW + tx + 1;                      // top-left of the 3x3 window in a p box
+  const long long own0 = static_cast<long long>(c0) * ld + static_cast<long long>(gy) * P + gx;
+
+  for (int t = z0 - 1; t <= z1; ++t) {
+    const bool rowP = t - 1 >= z0;
+    // own x, r of row t-1, issued ahead of the plane wait and barrier so
+    // their latency overlaps them
+    if (inside && rowP) {
+      const long long o = own0 + static_cast<long long>(t - 1) * S * P;
+#pragma unroll
+      for (int j = 0; j < CB; ++j)
+        if (act(j)) {
+          xc[j] = ldnc(a.x + o + j * ld);
+          rc[j] = ldnc(a.r + o + j * ld);
+        }
+    }
+    waitP(sp(t));
+    __syncthreads();  // slot sp(t-1) (read at step t-1) may be refilled
+    if (tid == 0 && t + 2 <= z1) issue(sp(t + 2), t + 2);
+
+    if (inside) {
+      const double* Pl = planes + sp(t) * CB * kHB;
+      const double* Cp = coefs + sp(t) * kCS;
+      double cN[4], cC[7];
+      cC[0] = Cp[1 * kHR + o0 - 1];        // slot 1 at (-1, 0)
+      cC[1] = Cp[2 * kHR + o0 - kRW];      // slot 2 at (0, -1)
+      cC[2] = Cp[3 * kHR + o0 - kRW - 1];  // slot 3 at (-1, -1)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cC[3 + i] = Cp[i * kHR + o0];  // own slots 0..3
+      cN[0] = Cp[4 * kHR + o0];
+      cN[1] = Cp[5 * kHR + o0 - 1];
+      cN[2] = Cp[6 * kHR + o0 - kRW];
+      cN[3] = Cp[7 * kHR + o0 - kRW - 1];
+      const long long orow = own0 + static_cast<long long>(t - 1) * S * P;  // row t-1
+#pragma unroll
+      for (int j = 0; j < CB; ++j) {
+        const double* Pj = Pl + j * kHB + ib;
+        const double vmm = Pj[0], v0m = Pj[1], vm0 = Pj[kRW], v00 = Pj[kRW + 1];
+        const double vp0 = Pj[kRW + 2], v0p = Pj[2 * kRW + 1], vpp = Pj[2 * kRW + 2];
+        if (rowP) {  // Pp terms of row t-1: A[v, v+o], o = 4..7
+          double s = sC[j];
+          s = fma(cPp[0], v00, s);
+          s = fma(cPp[1], vp0, s);
+          s = fma(cPp[2], v0p, s);
+          s = fma(cPp[3], vpp, s);
+          // x += alpha p ; r -= alpha q ; z = invd r  (linalg.cpp:202-206)
+          const double xv = __dadd_rn(xc[j], __dmul_rn(colA[j], cCur[j]));
+          const double rv = __dsub_rn(rc[j], __dmul_rn(colA[j], s));
+          if (act(j)) {
+            a.x[orow + j * ld] = xv;
+            a.r[orow + j * ld] = rv;
+          }
+          const double zz = __dmul_rn(invdP, rv);
+          acc[j][0] = fma(rv, zz, acc[j][0]);
+          acc[j][1] = fma(rv, rv, acc[j][1]);
+        }
+        // centre terms of row t, Pm terms of row t+1 (see stream_kernel)
+        double c = sN[j];
+        c = fma(cC[2], vmm, c);
+        c = fma(cC[1], v0m, c);
+        c = fma(cC[0], vm0, c);
+        c = fma(cC[3], v00, c);
+        c = fma(cC[4], vp0, c);
+        c = fma(cC[5], v0p, c);
+        c = fma(cC[6], vpp, c);
+        double nx = 0.0;
+        nx = fma(cN[3], vmm, nx);
+        nx = fma(cN[2], v0m, nx);
+        nx = fma(cN[1], vm0, nx);
+        nx = fma(cN[0], v00, nx);
+        sC[j] = c;
+        sN[j] = nx;
+        cCur[j] = v00;
+      }
+      // plane t's own slots 4..7 and 1/diag serve row t at the next step
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cPp[i] = Cp[(4 + i) * kHR + o0];
+      invdP = Cp[kSlots * kHR + tid];
+    }
+  }
+
+  const int warp = tid >> 5, lane = tid & 31;
+#pragma unroll
+  for (int j = 0; j < CB; ++j)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const double v = warp_sum(acc[j][q]);
+      if (lane == 0) red[warp][j * 2 + q] = v;
+    }
+  __syncthreads();
+  if (tid < CB * 2) {
+    const int j = tid / 2, q = tid % 2;
+    if (act(j)) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kNT / 32; ++w) s += red[w][tid];
+      a.partials[(static_cast<long long>(c0 + j) * 3 + q) * a.nblk + blk] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1 on the symmetric form of p'Ap (k1f): with A symmetric,
+//   p'Ap = sum_v p_v (A_vv p_v + 2 sum_{o forward} A[v, v+o] p_{v+o}),
+// so a point needs only its own 8 coefficient slots (no back weights from
+// neighbours) and p_new at its forward neighbours (+x, +y, +z combinations):
+// half the stencil FMAs of the full row sum, a one-sided halo (34 x 9 boxes
+// from (x0, y0)) and one TMA box per plane for the 8 slots. The reduction
+// order differs from the row-sum form by rounding only.
+constexpr int kFW = 34;             // forward box row width (x0 .. x0+33; 16-byte aligned start)
+constexpr int kFR = kFW * 9;        // 306 doubles per forward box (rows y0 .. y0+8)
+constexpr int kFB = 320;            // slot stride (128-byte aligned)
+constexpr int kCO = kSlots * kNT;   // own coefficient box [8][8][32]
+
+template <bool VAR, int CB>
+constexpr int k1f_data() {
+  return 2 * (2 * CB + (VAR ? 1 : 0)) * kFB + 3 * CB * kFB + (VAR ? 2 * kCO : 0);
+}
+template <bool VAR, int CB>
+constexpr size_t k1f_smem() {
+  return 128 + sizeof(double) * (k1f_data<VAR, CB>() + 4 + (kNT / 32) * CB);
+}
+
+template <bool VAR, int CB>
+__global__ void __launch_bounds__(kNT, kMinCtas)
+    k1f_kernel(const MarchArgs a, const __grid_constant__ CUtensorMap mr, const __grid_constant__ CUtensorMap mpo,
+               const __grid_constant__ CUtensorMap minv, const __grid_constant__ CUtensorMap mcoef) {
+  constexpr int NARR = 2 * CB + (VAR ? 1 : 0);  // raw arrays: r, p_old (per column), inverse diagonal
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* smem = reinterpret_cast<double*>(smem_raw + ((128u - (su32(smem_raw) & 127u)) & 127u));
+  double* raw = smem;                         // [2][NARR][kFB]
+  double* ring = raw + 2 * NARR * kFB;        // p_new [3][CB][kFB]
+  double* coefs = ring + 3 * CB * kFB;        // [2][8][kNT] (VAR)
+  unsigned long long* barR = reinterpret_cast<unsigned long long*>(smem + k1f_data<VAR, CB>());
+  unsigned long long* barC = barR + 2;
+  double(*red)[CB] = reinterpret_cast<double(*)[CB]>(barC + 2);
+
+  const int S = a.S;
+  const int P = a.P;
+  const long long ld = a.ld;
+  const int tid = threadIdx.x;
+  const int blk = blockIdx.y;
+  const int c0 = blockIdx.x * CB;
+
+  unsigned actm = 0, firstm = 0;
+  int nact = 0, nnf = 0;
+  double colB[CB];
+#pragma unroll
+  for (int j = 0; j < CB; ++j) {
+    const int c = c0 + j;
+    const bool on = c < a.K && a.cols[c].active != 0;
+    colB[j] = 0.0;
+    if (on) {
+      actm |= 1u << j;
+      ++nact;
+      colB[j] = a.cols[c].beta;
+      if (a.cols[c].first != 0) firstm |= 1u << j;
+      else ++nnf;
+    }
+  }
+  if (actm == 0) return;
+  auto act = [&](int j) { return (actm >> j) & 1u; };
+  auto first = [&](int j) { return (firstm >> j) & 1u; };
+
+  const int bx = blk % a.nTX;
+  const int by = (blk / a.nTX) % a.nTY;
+  const int bz = blk / (a.nTX * a.nTY);
+  const int x0 = bx * kTX, y0 = by * kTY;
+  const int z0 = bz * a.ZC;
+  const int z1 = min(S, z0 + a.ZC);
+  const int tx = tid % kTX, ty = tid / kTX;
+  const int gx = x0 + tx, gy = y0 + ty;
+  const bool inside = gx < S && gy < S;
+
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&barR[i], 1);
+      mbar_init(&barC[i], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // thread 0: raw plane z (r, p_old, 1/diag over x0..x0+33, y0..y0+8) into raw slot s
+  auto issue_raw = [&](int s, int z) {
+    mbar_arm(&barR[s], (nact + nnf + (VAR ? 1 : 0)) * static_cast<unsigned>(kFR * 8));
+    double* d = raw + s * NARR * kFB;
+#pragma unroll
+    for (int j = 0; j < CB; ++j) {
+      if (!act(j)) continue;
+      tma_load(d + j * kFB, &mr, x0, y0, z, c0 + j, &barR[s]);
+      if (!first(j)) tma_load(d + (CB + j) * kFB, &mpo, x0, y0, z, c0 + j, &barR[s]);
+    }
+    if (VAR) tma_load(d + 2 * CB * kFB, &minv, x0, y0, z, 0, &barR[s]);
+  };
+  auto issue_coef = [&](int s, int z) {
+    mbar_arm(&barC[s], kCO * 8u);
+    tma_load(coefs + s * kCO, &mcoef, x0, y0, z, 0, &barC[s]);
+  };
+  unsigned phR = 0, phC = 0;
+  auto waitR = [&](int s) {
+    mbar_wait(&barR[s], (phR >> s) & 1u);
+    phR ^= 1u << s;
+  };
+  auto waitC = [&](int s) {
+    mbar_wait(&barC[s], (phC >> s) & 1u);
+    phC ^= 1u << s;
+  };
+  // raw plane z (slot s) -> p_new = z + beta p_old into ring slot q (linalg.cpp:179, 210)
+  auto transform = [&](int s, int q) {
+    const double* rw = raw + s * NARR * kFB;
+    double* pr = ring + q * CB * kFB;
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      const int i = tid + l * kNT;
+      if (i >= kFR) continue;
+      const double d = VAR ? rw[2 * CB * kFB + i] : a.op.invd_const;
+#pragma unroll
+      for (int j = 0; j < CB; ++j) {
+        const double zz = __dmul_rn(d, rw[j * kFB + i]);
+        pr[j * kFB + i] = first(j) ? zz : __dadd_rn(zz, __dmul_rn(colB[j], rw[(CB + j) * kFB + i]));
+      }
+    }
+  };
+
+  // ---- prologue: p_new planes z0, z0+1 in the ring, raw z0+2 and coefficients of z0 (and z0+1) in flight
+  if (tid == 0) {
+    issue_raw(0, z0);
+    issue_raw(1, z0 + 1);
+    if (VAR) issue_coef(0, z0);
+  }
+  waitR(0);
+  transform(0, 0);
+  waitR(1);
+  transform(1, 1);
+  __syncthreads();
+  if (tid == 0) {
+    if (z0 + 2 <= z1) issue_raw(0, z0 + 2);
+    if (VAR && z0 + 1 < z1) issue_coef(1, z0 + 1);
+  }
+
+  double acc[CB];
+#pragma unroll
+  for (int j = 0; j < CB; ++j) acc[j] = 0.0;
+  const int io = ty * kFW + tx;  // own point in a forward box
+  const long long own0 = static_cast<long long>(c0) * ld + static_cast<long long>(gy) * P + gx;
+  for (int t = z0; t < z1; ++t) {
+    const int q0 = (t - z0) % 3, q1 = (t + 1 - z0) % 3;
+    if (VAR) waitC((t - z0) & 1);
+    if (inside) {
+      double w[kSlots];
+      if (VAR) {
+        const double* cf = coefs + ((t - z0) & 1) * kCO + tid;
+#pragma unroll
+        for (int o = 0; o < kSlots; ++o) w[o] = cf[o * kNT];
+      } else {
+#pragma unroll
+        for (int o = 0; o < kSlots; ++o) w[o] = a.op.wc[o];
+      }
+      const long long orow = own0 + static_cast<long long>(t) * S * P;
+#pragma unroll
+      for (int j = 0; j < CB; ++j) {
+        const double* A0 = ring + q0 * CB * kFB + j * kFB + io;  // plane t
+        const double* A1 = ring + q1 * CB * kFB + j * kFB + io;  // plane t+1
+        const double pv = A0[0];
+        double s = w[1] * A0[1];
+        s = fma(w[2], A0[kFW], s);
+        s = fma(w[3], A0[kFW + 1], s);
+        s = fma(w[4], A1[0], s);
+        s = fma(w[5], A1[1], s);
+        s = fma(w[6], A1[kFW], s);
+        s = fma(w[7], A1[kFW + 1], s);
+        acc[j] = fma(pv, fma(2.0, s, w[0] * pv), acc[j]);  // p_v (A p)_v over the symmetric pairs
+        if (act(j)) a.dst[orow + j * ld] = pv;            // p_new (own points of plane t)
+      }
+    }
+    if (t + 2 <= z1) {
+      waitR((t - z0) & 1);                      // raw plane t+2 landed
+      transform((t - z0) & 1, (t + 2 - z0) % 3);  // ring slot of plane t-1 (read at step t-1)
+    }
+    __syncthreads();  // p_new(t+2) visible; raw slot of t+2 and coefficient slot of t consumed
+    if (tid == 0) {
+      if (t + 3 <= z1) issue_raw((t - z0 + 1) & 1, t + 3);    // raw slot of t+1 (transformed at step t-1)
+      if (VAR && t + 2 < z1) issue_coef((t - z0) & 1, t + 2);
+    }
+  }
+
+  const int warp = tid >> 5, lane = tid & 31;
+#pragma unroll
+  for (int j = 0; j < CB; ++j) {
+    const double v = warp_sum(acc[j]);
+    if (lane == 0) red[warp][j] = v;
+  }
+  __syncthreads();
+  if (tid < CB && act(tid)) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kNT / 32; ++w) s += red[w][tid];
+    a.partials[(static_cast<long long>(c0 + tid) * 3 + 0) * a.nblk + blk] = s;
+  }
+}
+
 struct Maps {
   CUtensorMap a, b, c;
 };
@@ -468,6 +873,34 @@ void launch_cb(int cb, const MarchArgs& a, const Maps& m, cudaStream_t st) {
   }
 }
 
+template <bool VAR, int CB>
+void launch_k1f(const MarchArgs& a, const CUtensorMap& mr, const CUtensorMap& mpo, const CUtensorMap& minv,
+                const CUtensorMap& mcoef, cudaStream_t st) {
+  const int groups = (a.K + CB - 1) / CB;
+  constexpr size_t sm = k1f_smem<VAR, CB>();
+  static std::once_flag once;
+  std::call_once(once, [] {
+    PARO_CUDA(cudaFuncSetAttribute(k1f_kernel<VAR, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(sm)));
+  });
+  dim3 grid(groups, a.nblk);
+  k1f_kernel<VAR, CB><<<grid, kNT, sm, st>>>(a, mr, mpo, minv, mcoef);
+  PARO_CUDA(cudaGetLastError());
+}
+
+template <int CB>
+void launch_k2c(const MarchArgs& a, const Maps& m, cudaStream_t st) {
+  const int groups = (a.K + CB - 1) / CB;
+  constexpr size_t sm = k2c_smem<CB>();
+  static std::once_flag once;
+  std::call_once(once, [] {
+    PARO_CUDA(cudaFuncSetAttribute(k2c_kernel<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+  });
+  dim3 grid(groups, a.nblk);
+  k2c_kernel<CB><<<grid, kNT, sm, st>>>(a, m.a, m.b, m.c);
+  PARO_CUDA(cudaGetLastError());
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* f = nullptr;
@@ -480,14 +913,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   return fn;
 }
 
-// 4-D map (x, y, z, column) of a row-padded buffer with box (bx, by, 1, 1)
-void encode(CUtensorMap& m, const double* base, int S, long long ldi, int cols, int bx, int by) {
+// 4-D map (x, y, z, column) of a row-padded buffer with box (bx, by, 1, bc)
+void encode(CUtensorMap& m, const double* base, int S, long long ldi, int cols, int bx, int by, int bc = 1) {
   const int P = padded_row(S);
   const cuuint64_t dims[4] = {static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(S),
                               static_cast<cuuint64_t>(cols)};
   const cuuint64_t strides[3] = {static_cast<cuuint64_t>(P) * 8, static_cast<cuuint64_t>(S) * P * 8,
                                  static_cast<cuuint64_t>(ldi) * 8};
-  const cuuint32_t box[4] = {static_cast<cuuint32_t>(bx), static_cast<cuuint32_t>(by), 1, 1};
+  const cuuint32_t box[4] = {static_cast<cuuint32_t>(bx), static_cast<cuuint32_t>(by), 1, static_cast<cuuint32_t>(bc)};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   const CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides, box,
                                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -498,15 +931,31 @@ void encode(CUtensorMap& m, const double* base, int S, long long ldi, int cols, 
 }  // namespace
 
 void tma_plan(PcgTma& t, int S, long long ldi, int K, const double* r, const double* p0, const double* p1,
-              const double* x, const double* invd) {
+              const double* x, const double* invd, const double* coefp) {
   if ((ldi & 1) != 0) throw ParoError(kInvalidArgument, "tma: column stride must be even");
   encode(t.r_halo, r, S, ldi, K, kRW, kHY);
   encode(t.p0_halo, p0, S, ldi, K, kRW, kHY);
   encode(t.p1_halo, p1, S, ldi, K, kRW, kHY);
   encode(t.x_own, x, S, ldi, K, kTX, kTY);
   encode(t.r_own, r, S, ldi, K, kTX, kTY);
-  if (invd) encode(t.invd_halo, invd, S, ldi, 1, kRW, kHY);
-  else t.invd_halo = t.r_halo;
+  if (invd) {
+    encode(t.invd_halo, invd, S, ldi, 1, kRW, kHY);
+    encode(t.invd_own, invd, S, ldi, 1, kTX, kTY);
+  } else {
+    t.invd_halo = t.invd_own = t.r_halo;
+  }
+  encode(t.r_fwd, r, S, ldi, K, kFW, 9);
+  encode(t.p0_fwd, p0, S, ldi, K, kFW, 9);
+  encode(t.p1_fwd, p1, S, ldi, K, kFW, 9);
+  if (invd) encode(t.invd_fwd, invd, S, ldi, 1, kFW, 9);
+  else t.invd_fwd = t.r_fwd;
+  t.has_coef = coefp != nullptr;
+  if (coefp) {  // the 8 slots at stride ldi
+    encode(t.coef_box, coefp, S, ldi, kSlots, kRW, kHY, kSlots);
+    encode(t.coef_own, coefp, S, ldi, kSlots, kTX, kTY, kSlots);
+  } else {
+    t.coef_box = t.coef_own = t.r_halo;
+  }
 }
 
 void launch_tma(int mode, bool var, int cb, const MarchArgs& a, const PcgTma& t, bool p_is_p0, cudaStream_t st) {
@@ -515,7 +964,27 @@ void launch_tma(int mode, bool var, int cb, const MarchArgs& a, const PcgTma& t,
   if (var && a.op.sigma != 0.0) throw ParoError(kInvalidArgument, "tma: shifted variable operator not preshifted");
   if (a.op.mcoef != nullptr) throw ParoError(kInvalidArgument, "tma: variable shift stencil unsupported");
   Maps m;
-  if (mode == kK1) {
+  static const bool no_k1f = [] {
+    const char* e = std::getenv("PARO_NO_K1F");  // experiment knob: K1 on the full row-sum kernel
+    return e && e[0] == '1';
+  }();
+  if (mode == kK1 && !no_k1f && (!var || t.has_coef)) {
+    static const int forced = [] {
+      const char* e = std::getenv("PARO_MARCH_CB");
+      return e ? std::atoi(e) : 0;
+    }();
+    const int c = forced > 0 && cb > forced ? forced : cb;
+    const CUtensorMap& po = p_is_p0 ? t.p0_fwd : t.p1_fwd;
+    if (var) {
+      if (c == 1) launch_k1f<true, 1>(a, t.r_fwd, po, t.invd_fwd, t.coef_own, st);
+      else if (c == 2) launch_k1f<true, 2>(a, t.r_fwd, po, t.invd_fwd, t.coef_own, st);
+      else launch_k1f<true, 4>(a, t.r_fwd, po, t.invd_fwd, t.coef_own, st);
+    } else {
+      if (c == 1) launch_k1f<false, 1>(a, t.r_fwd, po, t.invd_fwd, t.r_fwd, st);
+      else if (c == 2) launch_k1f<false, 2>(a, t.r_fwd, po, t.invd_fwd, t.r_fwd, st);
+      else launch_k1f<false, 4>(a, t.r_fwd, po, t.invd_fwd, t.r_fwd, st);
+    }
+  } else if (mode == kK1) {
     m.a = t.r_halo;
     m.b = p_is_p0 ? t.p0_halo : t.p1_halo;
     m.c = t.invd_halo;
@@ -525,7 +994,22 @@ void launch_tma(int mode, bool var, int cb, const MarchArgs& a, const PcgTma& t,
     m.a = p_is_p0 ? t.p0_halo : t.p1_halo;
     m.b = t.x_own;
     m.c = t.r_own;
-    if (var) launch_cb<kK2, true>(cb, a, m, st);
+    static const bool no_k2c = [] {
+      const char* e = std::getenv("PARO_NO_K2C");  // experiment knob: coefficients by per-thread loads
+      return e && e[0] == '1';
+    }();
+    if (var && t.has_coef && !no_k2c) {
+      m.b = t.coef_box;
+      m.c = t.invd_own;
+      static const int forced = [] {
+        const char* e = std::getenv("PARO_MARCH_CB");
+        return e ? std::atoi(e) : 0;
+      }();
+      const int c = forced > 0 && cb > forced ? forced : cb;
+      if (c == 1) launch_k2c<1>(a, m, st);
+      else if (c == 2) launch_k2c<2>(a, m, st);
+      else launch_k2c<4>(a, m, st);
+    } else if (var) launch_cb<kK2, true>(cb, a, m, st);
     else launch_cb<kK2, false>(cb, a, m, st);
   } else {
     throw ParoError(kInvalidArgument, "tma: mode must be K1 or K2");
