@@ -445,7 +445,8 @@ __global__ void __launch_bounds__(kNT, kMinCtas) tma_kernel(const MarchArgs a, c
 // one box the inverse diagonal, all into the ring slot of the p plane, so
 // the thread reads them from shared memory. x and r stay in registers: the
 // own rows of row t are loaded at step t and updated at step t+1.
-constexpr int kCS = kSlots * kHR + kNT;  // coefficient slot: [8][10][36] boxes + inverse-diagonal own box [8][32]
+constexpr int kCR = kRW * (kTY + 1);     // coefficient box rows y0-1 .. y0+7 (back weights reach y-1 only)
+constexpr int kCS = kSlots * kCR + kNT;  // coefficient slot: [8][9][36] boxes + inverse-diagonal own box [8][32]
 
 template <int CB>
 constexpr int k2c_data() {
@@ -457,7 +458,7 @@ constexpr size_t k2c_smem() {
 }
 
 template <int CB>
-__global__ void __launch_bounds__(kNT, kMinCtas)
+__global__ void __launch_bounds__(kNT, CB >= 8 ? 1 : kMinCtas)
     k2c_kernel(const MarchArgs a, const __grid_constant__ CUtensorMap mp, const __grid_constant__ CUtensorMap mcoef,
                const __grid_constant__ CUtensorMap minvd) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -508,14 +509,14 @@ __global__ void __launch_bounds__(kNT, kMinCtas)
   __syncthreads();
 
   auto issue = [&](int s, int z) {  // thread 0: p, coefficient and inverse-diagonal planes z into slot s
-    mbar_arm(&barP[s], nact * kHaloBytes + (kSlots * kHR + kNT) * 8u);
+    mbar_arm(&barP[s], nact * kHaloBytes + (kSlots * kCR + kNT) * 8u);
     double* d = planes + s * CB * kHB;
 #pragma unroll
     for (int j = 0; j < CB; ++j)
       if (act(j)) tma_load(d + j * kHB, &mp, x0 - 2, y0 - 1, z, c0 + j, &barP[s]);
     double* cf = coefs + s * kCS;
     tma_load(cf, &mcoef, x0 - 2, y0 - 1, z, 0, &barP[s]);
-    tma_load(cf + kSlots * kHR, &minvd, x0, y0, z, 0, &barP[s]);
+    tma_load(cf + kSlots * kCR, &minvd, x0, y0, z, 0, &barP[s]);
   };
   unsigned phP = 0;
   auto waitP = [&](int s) {
@@ -563,15 +564,15 @@ __global__ void __launch_bounds__(kNT, kMinCtas)
       const double* Pl = planes + sp(t) * CB * kHB;
       const double* Cp = coefs + sp(t) * kCS;
       double cN[4], cC[7];
-      cC[0] = Cp[1 * kHR + o0 - 1];        // slot 1 at (-1, 0)
-      cC[1] = Cp[2 * kHR + o0 - kRW];      // slot 2 at (0, -1)
-      cC[2] = Cp[3 * kHR + o0 - kRW - 1];  // slot 3 at (-1, -1)
+      cC[0] = Cp[1 * kCR + o0 - 1];        // slot 1 at (-1, 0)
+      cC[1] = Cp[2 * kCR + o0 - kRW];      // slot 2 at (0, -1)
+      cC[2] = Cp[3 * kCR + o0 - kRW - 1];  // slot 3 at (-1, -1)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) cC[3 + i] = Cp[i * kHR + o0];  // own slots 0..3
-      cN[0] = Cp[4 * kHR + o0];
-      cN[1] = Cp[5 * kHR + o0 - 1];
-      cN[2] = Cp[6 * kHR + o0 - kRW];
-      cN[3] = Cp[7 * kHR + o0 - kRW - 1];
+      for (int i = 0; i < 4; ++i) cC[3 + i] = Cp[i * kCR + o0];  // own slots 0..3
+      cN[0] = Cp[4 * kCR + o0];
+      cN[1] = Cp[5 * kCR + o0 - 1];
+      cN[2] = Cp[6 * kCR + o0 - kRW];
+      cN[3] = Cp[7 * kCR + o0 - kRW - 1];
       const long long orow = own0 + static_cast<long long>(t - 1) * S * P;  // row t-1
 #pragma unroll
       for (int j = 0; j < CB; ++j) {
@@ -615,8 +616,8 @@ __global__ void __launch_bounds__(kNT, kMinCtas)
       }
       // plane t's own slots 4..7 and 1/diag serve row t at the next step
 #pragma unroll
-      for (int i = 0; i < 4; ++i) cPp[i] = Cp[(4 + i) * kHR + o0];
-      invdP = Cp[kSlots * kHR + tid];
+      for (int i = 0; i < 4; ++i) cPp[i] = Cp[(4 + i) * kCR + o0];
+      invdP = Cp[kSlots * kCR + tid];
     }
   }
 
@@ -646,38 +647,40 @@ __global__ void __launch_bounds__(kNT, kMinCtas)
 // so a point needs only its own 8 coefficient slots (no back weights from
 // neighbours) and p_new at its forward neighbours (+x, +y, +z combinations):
 // half the stencil FMAs of the full row sum, a one-sided halo (34 x 9 boxes
-// from (x0, y0)) and one TMA box per plane for the 8 slots. The reduction
-// order differs from the row-sum form by rounding only.
+// from (x0, y0)) and 8 coalesced own-coefficient loads per plane, issued a
+// step ahead. The raw planes (r, p_old, 1/diag) run two steps ahead in a
+// 3-slot TMA ring (with one step the plane wait was 46 % of the stalls).
+// The reduction order differs from the row-sum form by rounding only.
 constexpr int kFW = 34;             // forward box row width (x0 .. x0+33; 16-byte aligned start)
 constexpr int kFR = kFW * 9;        // 306 doubles per forward box (rows y0 .. y0+8)
 constexpr int kFB = 320;            // slot stride (128-byte aligned)
-constexpr int kCO = kSlots * kNT;   // own coefficient box [8][8][32]
+constexpr int kFN = 3;              // raw ring slots
 
 template <bool VAR, int CB>
 constexpr int k1f_data() {
-  return 2 * (2 * CB + (VAR ? 1 : 0)) * kFB + 3 * CB * kFB + (VAR ? 2 * kCO : 0);
+  return kFN * (2 * CB + (VAR ? 1 : 0)) * kFB + 3 * CB * kFB;
 }
 template <bool VAR, int CB>
 constexpr size_t k1f_smem() {
-  return 128 + sizeof(double) * (k1f_data<VAR, CB>() + 4 + (kNT / 32) * CB);
+  return 128 + sizeof(double) * (k1f_data<VAR, CB>() + kFN + (kNT / 32) * CB);
 }
 
 template <bool VAR, int CB>
 __global__ void __launch_bounds__(kNT, kMinCtas)
     k1f_kernel(const MarchArgs a, const __grid_constant__ CUtensorMap mr, const __grid_constant__ CUtensorMap mpo,
-               const __grid_constant__ CUtensorMap minv, const __grid_constant__ CUtensorMap mcoef) {
+               const __grid_constant__ CUtensorMap minv) {
   constexpr int NARR = 2 * CB + (VAR ? 1 : 0);  // raw arrays: r, p_old (per column), inverse diagonal
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* smem = reinterpret_cast<double*>(smem_raw + ((128u - (su32(smem_raw) & 127u)) & 127u));
-  double* raw = smem;                         // [2][NARR][kFB]
-  double* ring = raw + 2 * NARR * kFB;        // p_new [3][CB][kFB]
-  double* coefs = ring + 3 * CB * kFB;        // [2][8][kNT] (VAR)
+  double* raw = smem;                         // [kFN][NARR][kFB]
+  double* ring = raw + kFN * NARR * kFB;      // p_new [3][CB][kFB]
   unsigned long long* barR = reinterpret_cast<unsigned long long*>(smem + k1f_data<VAR, CB>());
-  unsigned long long* barC = barR + 2;
-  double(*red)[CB] = reinterpret_cast<double(*)[CB]>(barC + 2);
+  double(*red)[CB] = reinterpret_cast<double(*)[CB]>(barR + kFN);
 
   const int S = a.S;
+  const int S2 = S * S;
   const int P = a.P;
+  const long long n = a.n;
   const long long ld = a.ld;
   const int tid = threadIdx.x;
   const int blk = blockIdx.y;
@@ -714,10 +717,7 @@ __global__ void __launch_bounds__(kNT, kMinCtas)
   const bool inside = gx < S && gy < S;
 
   if (tid == 0) {
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&barR[i], 1);
-      mbar_init(&barC[i], 1);
-    }
+    for (int i = 0; i < kFN; ++i) mbar_init(&barR[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -734,18 +734,10 @@ __global__ void __launch_bounds__(kNT, kMinCtas)
     }
     if (VAR) tma_load(d + 2 * CB * kFB, &minv, x0, y0, z, 0, &barR[s]);
   };
-  auto issue_coef = [&](int s, int z) {
-    mbar_arm(&barC[s], kCO * 8u);
-    tma_load(coefs + s * kCO, &mcoef, x0, y0, z, 0, &barC[s]);
-  };
-  unsigned phR = 0, phC = 0;
+  unsigned phR = 0;
   auto waitR = [&](int s) {
     mbar_wait(&barR[s], (phR >> s) & 1u);
     phR ^= 1u << s;
-  };
-  auto waitC = [&](int s) {
-    mbar_wait(&barC[s], (phC >> s) & 1u);
-    phC ^= 1u << s;
   };
   // raw plane z (slot s) -> p_new = z + beta p_old into ring slot q (linalg.cpp:179, 210)
   auto transform = [&](int s, int q) {
@@ -763,22 +755,33 @@ __global__ void __launch_bounds__(kNT, kMinCtas)
       }
     }
   };
+  // own coefficient slots of plane z (dense operator layout, a.op.coef)
+  const long long cown = inside ? static_cast<long long>(gy) * S + gx : 0;
+  double w[kSlots];
+  auto load_w = [&](int z) {
+    if (VAR) {
+      const double* cf = a.op.coef + static_cast<long long>(min(z, S - 1)) * S2 + cown;
+#pragma unroll
+      for (int o = 0; o < kSlots; ++o) w[o] = ldnc(cf + o * n);
+    } else {
+#pragma unroll
+      for (int o = 0; o < kSlots; ++o) w[o] = a.op.wc[o];
+    }
+  };
 
-  // ---- prologue: p_new planes z0, z0+1 in the ring, raw z0+2 and coefficients of z0 (and z0+1) in flight
+  // ---- prologue: p_new planes z0, z0+1 in the ring, raw planes z0+2, z0+3 in flight
   if (tid == 0) {
     issue_raw(0, z0);
     issue_raw(1, z0 + 1);
-    if (VAR) issue_coef(0, z0);
+    if (z0 + 2 <= z1) issue_raw(2, z0 + 2);
   }
+  load_w(z0);
   waitR(0);
   transform(0, 0);
   waitR(1);
   transform(1, 1);
   __syncthreads();
-  if (tid == 0) {
-    if (z0 + 2 <= z1) issue_raw(0, z0 + 2);
-    if (VAR && z0 + 1 < z1) issue_coef(1, z0 + 1);
-  }
+  if (tid == 0 && z0 + 3 <= z1) issue_raw(0, z0 + 3);
 
   double acc[CB];
 #pragma unroll
@@ -787,17 +790,7 @@ __global__ void __launch_bounds__(kNT, kMinCtas)
   const long long own0 = static_cast<long long>(c0) * ld + static_cast<long long>(gy) * P + gx;
   for (int t = z0; t < z1; ++t) {
     const int q0 = (t - z0) % 3, q1 = (t + 1 - z0) % 3;
-    if (VAR) waitC((t - z0) & 1);
     if (inside) {
-      double w[kSlots];
-      if (VAR) {
-        const double* cf = coefs + ((t - z0) & 1) * kCO + tid;
-#pragma unroll
-        for (int o = 0; o < kSlots; ++o) w[o] = cf[o * kNT];
-      } else {
-#pragma unroll
-        for (int o = 0; o < kSlots; ++o) w[o] = a.op.wc[o];
-      }
       const long long orow = own0 + static_cast<long long>(t) * S * P;
 #pragma unroll
       for (int j = 0; j < CB; ++j) {
@@ -815,15 +808,14 @@ __global__ void __launch_bounds__(kNT, kMinCtas)
         if (act(j)) a.dst[orow + j * ld] = pv;            // p_new (own points of plane t)
       }
     }
+    if (t + 1 < z1) load_w(t + 1);  // lands during the transform and the barrier
     if (t + 2 <= z1) {
-      waitR((t - z0) & 1);                      // raw plane t+2 landed
-      transform((t - z0) & 1, (t + 2 - z0) % 3);  // ring slot of plane t-1 (read at step t-1)
+      const int s2 = (t + 2 - z0) % kFN;
+      waitR(s2);                              // raw plane t+2 landed
+      transform(s2, (t + 2 - z0) % 3);        // ring slot of plane t-1 (read at step t-1)
     }
-    __syncthreads();  // p_new(t+2) visible; raw slot of t+2 and coefficient slot of t consumed
-    if (tid == 0) {
-      if (t + 3 <= z1) issue_raw((t - z0 + 1) & 1, t + 3);    // raw slot of t+1 (transformed at step t-1)
-      if (VAR && t + 2 < z1) issue_coef((t - z0) & 1, t + 2);
-    }
+    __syncthreads();  // p_new(t+2) visible; raw slot of t+2 consumed
+    if (tid == 0 && t + 4 <= z1) issue_raw((t + 4 - z0) % kFN, t + 4);  // slot of raw t+1 (transformed at step t-1)
   }
 
   const int warp = tid >> 5, lane = tid & 31;
@@ -836,7 +828,7 @@ __global__ void __launch_bounds__(kNT, kMinCtas)
   if (tid < CB && act(tid)) {
     double s = 0.0;
 #pragma unroll
-    for (int w = 0; w < kNT / 32; ++w) s += red[w][tid];
+    for (int w2 = 0; w2 < kNT / 32; ++w2) s += red[w2][tid];
     a.partials[(static_cast<long long>(c0 + tid) * 3 + 0) * a.nblk + blk] = s;
   }
 }
@@ -875,7 +867,7 @@ void launch_cb(int cb, const MarchArgs& a, const Maps& m, cudaStream_t st) {
 
 template <bool VAR, int CB>
 void launch_k1f(const MarchArgs& a, const CUtensorMap& mr, const CUtensorMap& mpo, const CUtensorMap& minv,
-                const CUtensorMap& mcoef, cudaStream_t st) {
+                cudaStream_t st) {
   const int groups = (a.K + CB - 1) / CB;
   constexpr size_t sm = k1f_smem<VAR, CB>();
   static std::once_flag once;
@@ -884,7 +876,7 @@ void launch_k1f(const MarchArgs& a, const CUtensorMap& mr, const CUtensorMap& mp
                                    static_cast<int>(sm)));
   });
   dim3 grid(groups, a.nblk);
-  k1f_kernel<VAR, CB><<<grid, kNT, sm, st>>>(a, mr, mpo, minv, mcoef);
+  k1f_kernel<VAR, CB><<<grid, kNT, sm, st>>>(a, mr, mpo, minv);
   PARO_CUDA(cudaGetLastError());
 }
 
@@ -951,7 +943,7 @@ void tma_plan(PcgTma& t, int S, long long ldi, int K, const double* r, const dou
   else t.invd_fwd = t.r_fwd;
   t.has_coef = coefp != nullptr;
   if (coefp) {  // the 8 slots at stride ldi
-    encode(t.coef_box, coefp, S, ldi, kSlots, kRW, kHY, kSlots);
+    encode(t.coef_box, coefp, S, ldi, kSlots, kRW, kTY + 1, kSlots);
     encode(t.coef_own, coefp, S, ldi, kSlots, kTX, kTY, kSlots);
   } else {
     t.coef_box = t.coef_own = t.r_halo;
@@ -968,7 +960,7 @@ void launch_tma(int mode, bool var, int cb, const MarchArgs& a, const PcgTma& t,
     const char* e = std::getenv("PARO_NO_K1F");  // experiment knob: K1 on the full row-sum kernel
     return e && e[0] == '1';
   }();
-  if (mode == kK1 && !no_k1f && (!var || t.has_coef)) {
+  if (mode == kK1 && !no_k1f) {
     static const int forced = [] {
       const char* e = std::getenv("PARO_MARCH_CB");
       return e ? std::atoi(e) : 0;
@@ -976,13 +968,13 @@ void launch_tma(int mode, bool var, int cb, const MarchArgs& a, const PcgTma& t,
     const int c = forced > 0 && cb > forced ? forced : cb;
     const CUtensorMap& po = p_is_p0 ? t.p0_fwd : t.p1_fwd;
     if (var) {
-      if (c == 1) launch_k1f<true, 1>(a, t.r_fwd, po, t.invd_fwd, t.coef_own, st);
-      else if (c == 2) launch_k1f<true, 2>(a, t.r_fwd, po, t.invd_fwd, t.coef_own, st);
-      else launch_k1f<true, 4>(a, t.r_fwd, po, t.invd_fwd, t.coef_own, st);
+      if (c == 1) launch_k1f<true, 1>(a, t.r_fwd, po, t.invd_fwd, st);
+      else if (c == 2) launch_k1f<true, 2>(a, t.r_fwd, po, t.invd_fwd, st);
+      else launch_k1f<true, 4>(a, t.r_fwd, po, t.invd_fwd, st);
     } else {
-      if (c == 1) launch_k1f<false, 1>(a, t.r_fwd, po, t.invd_fwd, t.r_fwd, st);
-      else if (c == 2) launch_k1f<false, 2>(a, t.r_fwd, po, t.invd_fwd, t.r_fwd, st);
-      else launch_k1f<false, 4>(a, t.r_fwd, po, t.invd_fwd, t.r_fwd, st);
+      if (c == 1) launch_k1f<false, 1>(a, t.r_fwd, po, t.invd_fwd, st);
+      else if (c == 2) launch_k1f<false, 2>(a, t.r_fwd, po, t.invd_fwd, st);
+      else launch_k1f<false, 4>(a, t.r_fwd, po, t.invd_fwd, st);
     }
   } else if (mode == kK1) {
     m.a = t.r_halo;
@@ -1005,9 +997,14 @@ void launch_tma(int mode, bool var, int cb, const MarchArgs& a, const PcgTma& t,
         const char* e = std::getenv("PARO_MARCH_CB");
         return e ? std::atoi(e) : 0;
       }();
+      static const bool cb8 = [] {
+        const char* e = std::getenv("PARO_K2C_CB8");  // experiment knob: 8 columns per CTA, one CTA per SM
+        return e && e[0] == '1';
+      }();
       const int c = forced > 0 && cb > forced ? forced : cb;
       if (c == 1) launch_k2c<1>(a, m, st);
       else if (c == 2) launch_k2c<2>(a, m, st);
+      else if (c >= 8 && cb8) launch_k2c<8>(a, m, st);
       else launch_k2c<4>(a, m, st);
     } else if (var) launch_cb<kK2, true>(cb, a, m, st);
     else launch_cb<kK2, false>(cb, a, m, st);
