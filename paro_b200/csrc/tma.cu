@@ -20,6 +20,7 @@
 
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "march.cuh"
 
@@ -74,6 +75,12 @@ __device__ __forceinline__ void bulk_wait_read() {
 template <int N>
 __device__ __forceinline__ void bulk_wait() {
   asm volatile("cp.async.bulk.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// predicated store without a branch around it
+__device__ __forceinline__ void st_if(double* p, double v, bool pred) {
+  asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.global.f64 [%0], %1;\n}\n" ::"l"(p), "d"(v),
+               "r"(static_cast<int>(pred)));
 }
 
 __device__ __forceinline__ double ldnc(const double* p) {
@@ -574,46 +581,52 @@ __global__ void __launch_bounds__(kNT, CB >= 8 ? 1 : kMinCtas)
       cN[2] = Cp[6 * kCR + o0 - kRW];
       cN[3] = Cp[7 * kCR + o0 - kRW - 1];
       const long long orow = own0 + static_cast<long long>(t - 1) * S * P;  // row t-1
+      // one column body for both kinds of step (rowP is uniform), stores
+      // predicated rather than branched, so the 4 columns' FMA chains can
+      // interleave
+      auto body = [&](auto has_row) {
+        constexpr bool ROWP = decltype(has_row)::value;
 #pragma unroll
-      for (int j = 0; j < CB; ++j) {
-        const double* Pj = Pl + j * kHB + ib;
-        const double vmm = Pj[0], v0m = Pj[1], vm0 = Pj[kRW], v00 = Pj[kRW + 1];
-        const double vp0 = Pj[kRW + 2], v0p = Pj[2 * kRW + 1], vpp = Pj[2 * kRW + 2];
-        if (rowP) {  // Pp terms of row t-1: A[v, v+o], o = 4..7
-          double s = sC[j];
-          s = fma(cPp[0], v00, s);
-          s = fma(cPp[1], vp0, s);
-          s = fma(cPp[2], v0p, s);
-          s = fma(cPp[3], vpp, s);
-          // x += alpha p ; r -= alpha q ; z = invd r  (linalg.cpp:202-206)
-          const double xv = __dadd_rn(xc[j], __dmul_rn(colA[j], cCur[j]));
-          const double rv = __dsub_rn(rc[j], __dmul_rn(colA[j], s));
-          if (act(j)) {
-            a.x[orow + j * ld] = xv;
-            a.r[orow + j * ld] = rv;
+        for (int j = 0; j < CB; ++j) {
+          const double* Pj = Pl + j * kHB + ib;
+          const double vmm = Pj[0], v0m = Pj[1], vm0 = Pj[kRW], v00 = Pj[kRW + 1];
+          const double vp0 = Pj[kRW + 2], v0p = Pj[2 * kRW + 1], vpp = Pj[2 * kRW + 2];
+          if (ROWP) {  // Pp terms of row t-1: A[v, v+o], o = 4..7
+            double s = sC[j];
+            s = fma(cPp[0], v00, s);
+            s = fma(cPp[1], vp0, s);
+            s = fma(cPp[2], v0p, s);
+            s = fma(cPp[3], vpp, s);
+            // x += alpha p ; r -= alpha q ; z = invd r  (linalg.cpp:202-206)
+            const double xv = __dadd_rn(xc[j], __dmul_rn(colA[j], cCur[j]));
+            const double rv = __dsub_rn(rc[j], __dmul_rn(colA[j], s));
+            st_if(a.x + orow + j * ld, xv, act(j));
+            st_if(a.r + orow + j * ld, rv, act(j));
+            const double zz = __dmul_rn(invdP, rv);
+            acc[j][0] = fma(rv, zz, acc[j][0]);
+            acc[j][1] = fma(rv, rv, acc[j][1]);
           }
-          const double zz = __dmul_rn(invdP, rv);
-          acc[j][0] = fma(rv, zz, acc[j][0]);
-          acc[j][1] = fma(rv, rv, acc[j][1]);
+          // centre terms of row t, Pm terms of row t+1 (see stream_kernel)
+          double c = sN[j];
+          c = fma(cC[2], vmm, c);
+          c = fma(cC[1], v0m, c);
+          c = fma(cC[0], vm0, c);
+          c = fma(cC[3], v00, c);
+          c = fma(cC[4], vp0, c);
+          c = fma(cC[5], v0p, c);
+          c = fma(cC[6], vpp, c);
+          double nx = 0.0;
+          nx = fma(cN[3], vmm, nx);
+          nx = fma(cN[2], v0m, nx);
+          nx = fma(cN[1], vm0, nx);
+          nx = fma(cN[0], v00, nx);
+          sC[j] = c;
+          sN[j] = nx;
+          cCur[j] = v00;
         }
-        // centre terms of row t, Pm terms of row t+1 (see stream_kernel)
-        double c = sN[j];
-        c = fma(cC[2], vmm, c);
-        c = fma(cC[1], v0m, c);
-        c = fma(cC[0], vm0, c);
-        c = fma(cC[3], v00, c);
-        c = fma(cC[4], vp0, c);
-        c = fma(cC[5], v0p, c);
-        c = fma(cC[6], vpp, c);
-        double nx = 0.0;
-        nx = fma(cN[3], vmm, nx);
-        nx = fma(cN[2], v0m, nx);
-        nx = fma(cN[1], vm0, nx);
-        nx = fma(cN[0], v00, nx);
-        sC[j] = c;
-        sN[j] = nx;
-        cCur[j] = v00;
-      }
+      };
+      if (rowP) body(std::true_type{});
+      else body(std::false_type{});
       // plane t's own slots 4..7 and 1/diag serve row t at the next step
 #pragma unroll
       for (int i = 0; i < 4; ++i) cPp[i] = Cp[(4 + i) * kCR + o0];
@@ -805,7 +818,7 @@ __global__ void __launch_bounds__(kNT, kMinCtas)
         s = fma(w[6], A1[kFW], s);
         s = fma(w[7], A1[kFW + 1], s);
         acc[j] = fma(pv, fma(2.0, s, w[0] * pv), acc[j]);  // p_v (A p)_v over the symmetric pairs
-        if (act(j)) a.dst[orow + j * ld] = pv;            // p_new (own points of plane t)
+        st_if(a.dst + orow + j * ld, pv, act(j));         // p_new (own points of plane t)
       }
     }
     if (t + 1 < z1) load_w(t + 1);  // lands during the transform and the barrier
