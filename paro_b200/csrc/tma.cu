@@ -586,25 +586,20 @@ __global__ void __launch_bounds__(kNT, CB >= 8 ? 1 : kMinCtas)
       // interleave
       auto body = [&](auto has_row) {
         constexpr bool ROWP = decltype(has_row)::value;
+        double sP[CB], pOld[CB];  // completed row sums of row t-1 and p at row t-1
 #pragma unroll
         for (int j = 0; j < CB; ++j) {
           const double* Pj = Pl + j * kHB + ib;
           const double vmm = Pj[0], v0m = Pj[1], vm0 = Pj[kRW], v00 = Pj[kRW + 1];
           const double vp0 = Pj[kRW + 2], v0p = Pj[2 * kRW + 1], vpp = Pj[2 * kRW + 2];
           if (ROWP) {  // Pp terms of row t-1: A[v, v+o], o = 4..7
-            double s = sC[j];
-            s = fma(cPp[0], v00, s);
-            s = fma(cPp[1], vp0, s);
-            s = fma(cPp[2], v0p, s);
-            s = fma(cPp[3], vpp, s);
-            // x += alpha p ; r -= alpha q ; z = invd r  (linalg.cpp:202-206)
-            const double xv = __dadd_rn(xc[j], __dmul_rn(colA[j], cCur[j]));
-            const double rv = __dsub_rn(rc[j], __dmul_rn(colA[j], s));
-            st_if(a.x + orow + j * ld, xv, act(j));
-            st_if(a.r + orow + j * ld, rv, act(j));
-            const double zz = __dmul_rn(invdP, rv);
-            acc[j][0] = fma(rv, zz, acc[j][0]);
-            acc[j][1] = fma(rv, rv, acc[j][1]);
+            double sv = sC[j];
+            sv = fma(cPp[0], v00, sv);
+            sv = fma(cPp[1], vp0, sv);
+            sv = fma(cPp[2], v0p, sv);
+            sv = fma(cPp[3], vpp, sv);
+            sP[j] = sv;
+            pOld[j] = cCur[j];
           }
           // centre terms of row t, Pm terms of row t+1 (see stream_kernel)
           double c = sN[j];
@@ -623,6 +618,21 @@ __global__ void __launch_bounds__(kNT, CB >= 8 ? 1 : kMinCtas)
           sC[j] = c;
           sN[j] = nx;
           cCur[j] = v00;
+        }
+        if (ROWP) {
+          // the row t-1 updates last, so the x, r loads issued at the top of
+          // the step have the stencil work above to land
+#pragma unroll
+          for (int j = 0; j < CB; ++j) {
+            // x += alpha p ; r -= alpha q ; z = invd r  (linalg.cpp:202-206)
+            const double xv = __dadd_rn(xc[j], __dmul_rn(colA[j], pOld[j]));
+            const double rv = __dsub_rn(rc[j], __dmul_rn(colA[j], sP[j]));
+            st_if(a.x + orow + j * ld, xv, act(j));
+            st_if(a.r + orow + j * ld, rv, act(j));
+            const double zz = __dmul_rn(invdP, rv);
+            acc[j][0] = fma(rv, zz, acc[j][0]);
+            acc[j][1] = fma(rv, rv, acc[j][1]);
+          }
         }
       };
       if (rowP) body(std::true_type{});
