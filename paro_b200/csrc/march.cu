@@ -917,7 +917,11 @@ void plan_march(MarchArgs& a, int S) {
   a.nTY = (S + kTY - 1) / kTY;
   const long long target = 148 * 4;
   long long zc = (static_cast<long long>(S) * a.nTX * a.nTY + target - 1) / target;
-  zc = std::max<long long>(4, std::min<long long>(32, zc));
+  static const int zc_max = [] {
+    const char* e = std::getenv("PARO_ZC");  // experiment knob: planes per CTA z-chunk (default 32)
+    return e ? std::atoi(e) : 32;
+  }();
+  zc = std::max<long long>(4, std::min<long long>(zc_max, zc));
   a.ZC = static_cast<int>(std::min<long long>(zc, S));
   a.nZ = (S + a.ZC - 1) / a.ZC;
   a.nblk = a.nTX * a.nTY * a.nZ;
