@@ -151,7 +151,7 @@ def pcg_traffic():
         t = json.loads(path.read_text())
     except (OSError, ValueError):
         return {}
-    return {"bytes": t["traffic_bytes_per_iteration"],
+    return {"bytes": t["traffic_bytes_per_iteration"], "algorithmic": t["algorithmic_bytes_per_iteration"],
             "note": f"dram read+write per PCG iteration at k=76 (K1+K2), {path.relative_to(ROOT)}; "
                     f"algorithmic {t['algorithmic_bytes_per_iteration']:.4g} B"}
 
@@ -301,7 +301,15 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if peak else None, "traffic": traffic.get("bytes"),
                          "traffic_note": traffic.get("note"),
-                         "kernel": "Step-3 Jacobi-PCG iteration (march K1+K2 + finalize), algorithmic n*(88k+64) B",
+                         # the algorithmic model counts the reference's 11 vector passes per
+                         # CG iteration; the fused two-pass scheme moves 8, so achieved/peak can pass 1.
+                         # dram_* scale the same live time by the measured DRAM bytes instead.
+                         "dram_achieved": achieved * traffic["bytes"] / traffic["algorithmic"]
+                         if traffic.get("algorithmic") else None,
+                         "dram_frac": achieved * traffic["bytes"] / traffic["algorithmic"] / peak
+                         if traffic.get("algorithmic") and peak else None,
+                         "kernel": "Step-3 Jacobi-PCG iteration (tma.cu k1f_kernel + k2c_kernel + finalize), "
+                                   "algorithmic n*(88k+64) B",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("_fallback") else "fallback"},
             "cpu_baseline": cpu,
             "e2e": e2e,
