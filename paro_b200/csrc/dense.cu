@@ -81,12 +81,19 @@ __device__ void fix_sign_seq(int n, double* v, int stride) {
 
 // jacobi_eig (linalg.cpp:243-302): a (n x n, destroyed), v (n x n) eigenvectors,
 // vals sorted ascending, vecs columns reordered accordingly into `out`.
-__device__ void warp_jacobi(int n, double* a_g, double* v_g, double tol, int max_sweeps, double* vals, double* out,
-                            int* order) {
-  const int lane = threadIdx.x;
+// Block-wide: every thread derives (c, s) of a rotation from the same shared
+// values (identical arithmetic, so identical results), then thread k applies
+// the rotation to row/column k of a and row k of v; the 2x2 block (p, q) is
+// done by one thread in the reference's order (column pass, then row pass).
+// Elements touched by different threads within a rotation are disjoint, so
+// one barrier per rotation keeps the reference's operation sequence.
+__device__ void block_jacobi(int n, double* a_g, double* v_g, double tol, int max_sweeps, double* vals, double* out,
+                             int* order) {
+  const int tid = threadIdx.x, nt = blockDim.x;
   // the rotation sequence is latency-bound: run it on shared-memory copies
   // when the launch provided 2 n^2 doubles of dynamic shared memory
   extern __shared__ double jsm[];
+  __shared__ double bc[2];
   unsigned dyn;
   asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
   double* a = a_g;
@@ -94,28 +101,30 @@ __device__ void warp_jacobi(int n, double* a_g, double* v_g, double tol, int max
   if (dyn >= 2u * n * n * sizeof(double)) {
     a = jsm;
     v = jsm + n * n;
-    for (int i = lane; i < n * n; i += 32) a[i] = a_g[i];
-    __syncwarp();
+    for (int i = tid; i < n * n; i += nt) a[i] = a_g[i];
   }
-  warp_fill(v, n * n, 0.0);
-  for (int i = lane; i < n; i += 32) v[i * n + i] = 1.0;
-  __syncwarp();
-  double fro = 0.0;
-  if (lane == 0) {
+  for (int i = tid; i < n * n; i += nt) v[i] = 0.0;
+  __syncthreads();
+  for (int i = tid; i < n; i += nt) v[i * n + i] = 1.0;
+  if (tid == 0) {
+    double fro = 0.0;
     for (int i = 0; i < n; ++i)
       for (int j = 0; j < n; ++j) fro += a[i * n + j] * a[i * n + j];
     fro = sqrt(fro);
     if (fro == 0.0) fro = 1.0;
+    bc[0] = fro;
   }
-  fro = __shfl_sync(0xffffffffu, fro, 0);
+  __syncthreads();
+  const double fro = bc[0];
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
-    double off = 0.0;
-    if (lane == 0) {
+    if (tid == 0) {
+      double off = 0.0;
       for (int i = 0; i < n; ++i)
         for (int j = i + 1; j < n; ++j) off += 2.0 * a[i * n + j] * a[i * n + j];
+      bc[1] = off;
     }
-    off = __shfl_sync(0xffffffffu, off, 0);
-    if (sqrt(off) <= tol * fro) break;
+    __syncthreads();
+    if (sqrt(bc[1]) <= tol * fro) break;
     for (int p = 0; p + 1 < n; ++p) {
       for (int q = p + 1; q < n; ++q) {
         const double apq = a[p * n + q];
@@ -124,29 +133,38 @@ __device__ void warp_jacobi(int n, double* a_g, double* v_g, double tol, int max
         const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
         const double c = 1.0 / sqrt(1.0 + t * t);
         const double s = t * c;
-        __syncwarp();
-        for (int k = lane; k < n; k += 32) {
-          const double akp = a[k * n + p], akq = a[k * n + q];
-          a[k * n + p] = c * akp - s * akq;
-          a[k * n + q] = s * akp + c * akq;
-        }
-        __syncwarp();
-        for (int k = lane; k < n; k += 32) {
-          const double apk = a[p * n + k], aqk = a[q * n + k];
-          a[p * n + k] = c * apk - s * aqk;
-          a[q * n + k] = s * apk + c * aqk;
-        }
-        for (int k = lane; k < n; k += 32) {
+        for (int k = tid; k < n; k += nt) {
+          if (k == p) {  // the (p, q) block: column pass, then row pass
+            double x0 = a[p * n + p], x1 = a[p * n + q];
+            a[p * n + p] = c * x0 - s * x1;
+            a[p * n + q] = s * x0 + c * x1;
+            x0 = a[q * n + p], x1 = a[q * n + q];
+            a[q * n + p] = c * x0 - s * x1;
+            a[q * n + q] = s * x0 + c * x1;
+            x0 = a[p * n + p], x1 = a[q * n + p];
+            a[p * n + p] = c * x0 - s * x1;
+            a[q * n + p] = s * x0 + c * x1;
+            x0 = a[p * n + q], x1 = a[q * n + q];
+            a[p * n + q] = c * x0 - s * x1;
+            a[q * n + q] = s * x0 + c * x1;
+          } else if (k != q) {
+            const double akp = a[k * n + p], akq = a[k * n + q];
+            a[k * n + p] = c * akp - s * akq;
+            a[k * n + q] = s * akp + c * akq;
+            const double apk = a[p * n + k], aqk = a[q * n + k];
+            a[p * n + k] = c * apk - s * aqk;
+            a[q * n + k] = s * apk + c * aqk;
+          }
           const double vkp = v[k * n + p], vkq = v[k * n + q];
           v[k * n + p] = c * vkp - s * vkq;
           v[k * n + q] = s * vkp + c * vkq;
         }
-        __syncwarp();
+        __syncthreads();
       }
     }
   }
   // ascending order of the diagonal (stable for exact ties)
-  if (lane == 0) {
+  if (tid == 0) {
     for (int i = 0; i < n; ++i) order[i] = i;
     for (int i = 1; i < n; ++i) {
       const int oi = order[i];
@@ -159,13 +177,13 @@ __device__ void warp_jacobi(int n, double* a_g, double* v_g, double tol, int max
       order[j + 1] = oi;
     }
   }
-  __syncwarp();
-  for (int j = lane; j < n; j += 32) vals[j] = a[order[j] * n + order[j]];
-  for (int idx = lane; idx < n * n; idx += 32) {
+  __syncthreads();
+  for (int j = tid; j < n; j += nt) vals[j] = a[order[j] * n + order[j]];
+  for (int idx = tid; idx < n * n; idx += nt) {
     const int i = idx / n, j = idx % n;
     out[i * n + j] = v[i * n + order[j]];
   }
-  __syncwarp();
+  __syncthreads();
 }
 
 }  // namespace
@@ -174,49 +192,61 @@ __device__ void warp_jacobi(int n, double* a_g, double* v_g, double tol, int max
 // vals (n), X row-major n x n (columns = B-orthonormal eigenvectors).
 __device__ int dense_sym_geneig_warp(int n, const double* A, const double* B, double* vals, double* X,
                                      const DenseScratch& w) {
+  // launched with a whole block: the order-sensitive / small parts run on warp
+  // 0, the Jacobi rotations on every thread
   const int lane = threadIdx.x;
-  if (!warp_symmetric(n, A) || !warp_symmetric(n, B)) return kPencil;
-  if (!warp_cholesky(n, B, w.l)) return kPencil;
-  // W = L^{-1} A, column j independent
-  for (int j = lane; j < n; j += 32) {
-    for (int i = 0; i < n; ++i) {
-      double s = A[i * n + j];
-      for (int k = 0; k < i; ++k) s -= w.l[i * n + k] * w.w[k * n + j];
-      w.w[i * n + j] = s / w.l[i * n + i];
+  __shared__ int st_sh;
+  if (threadIdx.x < 32) {
+    int st = kOk;
+    if (!warp_symmetric(n, A) || !warp_symmetric(n, B)) st = kPencil;
+    else if (!warp_cholesky(n, B, w.l)) st = kPencil;
+    if (st == kOk) {
+      // W = L^{-1} A, column j independent
+      for (int j = lane; j < n; j += 32) {
+        for (int i = 0; i < n; ++i) {
+          double s = A[i * n + j];
+          for (int k = 0; k < i; ++k) s -= w.l[i * n + k] * w.w[k * n + j];
+          w.w[i * n + j] = s / w.l[i * n + i];
+        }
+      }
+      __syncwarp();
+      // C = W L^{-T}, row i independent
+      for (int i = lane; i < n; i += 32) {
+        for (int j = 0; j < n; ++j) {
+          double s = w.w[i * n + j];
+          for (int k = 0; k < j; ++k) s -= w.c[i * n + k] * w.l[j * n + k];
+          w.c[i * n + j] = s / w.l[j * n + j];
+        }
+      }
+      __syncwarp();
+      for (int idx = lane; idx < n * n; idx += 32) {
+        const int i = idx / n, j = idx % n;
+        if (j > i) {
+          const double avg = 0.5 * (w.c[i * n + j] + w.c[j * n + i]);
+          w.a[i * n + j] = avg;
+          w.a[j * n + i] = avg;
+        } else if (j == i) {
+          w.a[i * n + i] = w.c[i * n + i];
+        }
+      }
+    }
+    if (lane == 0) st_sh = st;
+  }
+  __syncthreads();
+  if (st_sh != kOk) return st_sh;
+  block_jacobi(n, w.a, w.v, 1e-12, 60, vals, X, w.order);
+  if (threadIdx.x < 32) {
+    // x = L^{-T} y per column, then fix_sign
+    for (int col = lane; col < n; col += 32) {
+      for (int ii = n - 1; ii >= 0; --ii) {
+        double s = X[ii * n + col];
+        for (int k = ii + 1; k < n; ++k) s -= w.l[k * n + ii] * X[k * n + col];
+        X[ii * n + col] = s / w.l[ii * n + ii];
+      }
+      fix_sign_seq(n, X + col, n);
     }
   }
-  __syncwarp();
-  // C = W L^{-T}, row i independent
-  for (int i = lane; i < n; i += 32) {
-    for (int j = 0; j < n; ++j) {
-      double s = w.w[i * n + j];
-      for (int k = 0; k < j; ++k) s -= w.c[i * n + k] * w.l[j * n + k];
-      w.c[i * n + j] = s / w.l[j * n + j];
-    }
-  }
-  __syncwarp();
-  for (int idx = lane; idx < n * n; idx += 32) {
-    const int i = idx / n, j = idx % n;
-    if (j > i) {
-      const double avg = 0.5 * (w.c[i * n + j] + w.c[j * n + i]);
-      w.a[i * n + j] = avg;
-      w.a[j * n + i] = avg;
-    } else if (j == i) {
-      w.a[i * n + i] = w.c[i * n + i];
-    }
-  }
-  __syncwarp();
-  warp_jacobi(n, w.a, w.v, 1e-12, 60, vals, X, w.order);
-  // x = L^{-T} y per column, then fix_sign
-  for (int col = lane; col < n; col += 32) {
-    for (int ii = n - 1; ii >= 0; --ii) {
-      double s = X[ii * n + col];
-      for (int k = ii + 1; k < n; ++k) s -= w.l[k * n + ii] * X[k * n + col];
-      X[ii * n + col] = s / w.l[ii * n + ii];
-    }
-    fix_sign_seq(n, X + col, n);
-  }
-  __syncwarp();
+  __syncthreads();
   return kOk;
 }
 
@@ -375,17 +405,19 @@ __global__ void second_pass_kernel(int k, const double* G2, double* C2, double* 
 __global__ void pencil_direct_kernel(int k, const double* GA, const double* GB, double* vals, double* Y, double* At,
                                      double* Bt, double* X, DenseScratch w, int* status) {
   const int lane = threadIdx.x;
-  for (int idx = lane; idx < k * k; idx += 32) {
-    const int i = idx / k, j = idx % k;
-    At[i * k + j] = 0.5 * (GA[i + j * k] + GA[j + i * k]);
-    Bt[i * k + j] = 0.5 * (GB[i + j * k] + GB[j + i * k]);
-  }
-  __syncwarp();
+  if (lane < 32)
+    for (int idx = lane; idx < k * k; idx += 32) {
+      const int i = idx / k, j = idx % k;
+      At[i * k + j] = 0.5 * (GA[i + j * k] + GA[j + i * k]);
+      Bt[i * k + j] = 0.5 * (GB[i + j * k] + GB[j + i * k]);
+    }
+  __syncthreads();
   const int st = dense_sym_geneig_warp(k, At, Bt, vals, X, w);
   if (st != kOk) {
     if (lane == 0) *status = st;
     return;
   }
+  if (lane < 32)
   for (int idx = lane; idx < k * k; idx += 32) {
     const int i = idx % k, j = idx / k;
     Y[i + j * k] = X[i * k + j];
@@ -399,23 +431,23 @@ __global__ void pencil_direct_kernel(int k, const double* GA, const double* GB, 
 // Y = C2 X (column-major k x k) lifts the Ritz vectors onto Q1.
 __global__ void pencil_kernel(int k, const double* GA, const double* C2, const double* Bt, double* vals, double* Y,
                               double* At, double* X, DenseScratch w, int* status) {
-  const int lane = threadIdx.x;
-  // T = sym(GA) C2  (row-major)
-  for (int idx = lane; idx < k * k; idx += 32) {
+  const int lane = threadIdx.x, nt = blockDim.x;
+  // T = sym(GA) C2  (row-major); each entry one thread, fixed-order sums
+  for (int idx = lane; idx < k * k; idx += nt) {
     const int i = idx / k, j = idx % k;
     double s = 0.0;
     for (int m = 0; m < k; ++m) s += 0.5 * (GA[i + m * k] + GA[m + i * k]) * C2[m + j * k];
     w.w[i * k + j] = s;
   }
-  __syncwarp();
-  for (int idx = lane; idx < k * k; idx += 32) {
+  __syncthreads();
+  for (int idx = lane; idx < k * k; idx += nt) {
     const int i = idx / k, j = idx % k;
     double s = 0.0;
     for (int m = 0; m < k; ++m) s += C2[m + i * k] * w.w[m * k + j];
     At[i * k + j] = s;
   }
-  __syncwarp();
-  for (int idx = lane; idx < k * k; idx += 32) {
+  __syncthreads();
+  for (int idx = lane; idx < k * k; idx += nt) {
     const int i = idx / k, j = idx % k;
     if (j > i) {
       const double avg = 0.5 * (At[i * k + j] + At[j * k + i]);
@@ -423,13 +455,13 @@ __global__ void pencil_kernel(int k, const double* GA, const double* C2, const d
       At[j * k + i] = avg;
     }
   }
-  __syncwarp();
+  __syncthreads();
   const int st = dense_sym_geneig_warp(k, At, Bt, vals, X, w);
   if (st != kOk) {
     if (lane == 0) *status = st;
     return;
   }
-  for (int idx = lane; idx < k * k; idx += 32) {
+  for (int idx = lane; idx < k * k; idx += nt) {
     const int i = idx % k, j = idx / k;
     double s = 0.0;
     for (int m = 0; m < k; ++m) s += C2[i + m * k] * X[m * k + j];
@@ -446,7 +478,7 @@ size_t dense_jacobi_smem(int n) {
 void dense_configure() {
   static bool done = false;
   if (done) return;
-  const int mx = 227 * 1024;
+  const int mx = 220 * 1024;  // dense_jacobi_smem() caps at 220 KB; leaves room for the static shared variables
   PARO_CUDA(cudaFuncSetAttribute(geneig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   PARO_CUDA(cudaFuncSetAttribute(pencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   PARO_CUDA(cudaFuncSetAttribute(pencil_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));

@@ -1,4 +1,4 @@
-// K x K dense kernels of Step 4 (single warp; see dense.cu).
+// K x K dense kernels of Step 4 (see dense.cu).
 #pragma once
 
 #include "common.cuh"
@@ -15,7 +15,11 @@ struct DenseScratch {
   int* order = nullptr;
 };
 
-// dynamic shared memory for a kernel running warp_jacobi on n x n (0 = global)
+// threads of the pencil / geneig launches (the Jacobi rotations use all of
+// them, the order-sensitive small parts warp 0)
+constexpr int kDenseThreads = 128;
+
+// dynamic shared memory for a kernel running the Jacobi rotations on n x n (0 = global)
 size_t dense_jacobi_smem(int n);
 void dense_configure();
 

@@ -503,7 +503,7 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
       apply_op(ctx, A, nullptr, 0.0, k, Q1, n, W, n);
       gram(ctx, k, k, Q1, n, W, n, s.GA);
       dense_configure();
-      pencil_kernel<<<1, 32, dense_jacobi_smem(k), st>>>(k, s.GA, s.C2, s.Bt, s.vals, s.Y, s.At, s.X, s.w, s.status);
+      pencil_kernel<<<1, kDenseThreads, dense_jacobi_smem(k), st>>>(k, s.GA, s.C2, s.Bt, s.vals, s.Y, s.At, s.X, s.w, s.status);
       ++ctx.launches;
       if (read_int(ctx, s.status) != kOk) {
         ctx.err = "pencil: B is not positive definite";
@@ -524,7 +524,7 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
     gram(ctx, k, k, Q1, n, AQ, n, s.GA);
     gram(ctx, k, k, Q1, n, BQ, n, s.G2);
     dense_configure();
-    pencil_direct_kernel<<<1, 32, dense_jacobi_smem(k), st>>>(k, s.GA, s.G2, s.vals, s.Y, s.At, s.Bt, s.X, s.w, s.status);
+    pencil_direct_kernel<<<1, kDenseThreads, dense_jacobi_smem(k), st>>>(k, s.GA, s.G2, s.vals, s.Y, s.At, s.Bt, s.X, s.w, s.status);
     ++ctx.launches;
     if (read_int(ctx, s.status) != kOk) {
       ctx.err = "pencil: B is not positive definite";
@@ -567,7 +567,7 @@ int dense_sym_geneig(Ctx& ctx, int m, const double* A_host, const double* B_host
   PARO_CUDA(cudaMemcpyAsync(s.At, A_host, bytes, cudaMemcpyHostToDevice, st));
   PARO_CUDA(cudaMemcpyAsync(s.Bt, B_host, bytes, cudaMemcpyHostToDevice, st));
   dense_configure();
-  geneig_kernel<<<1, 32, dense_jacobi_smem(m), st>>>(m, s.At, s.Bt, s.vals, s.X, s.w, s.status);
+  geneig_kernel<<<1, kDenseThreads, dense_jacobi_smem(m), st>>>(m, s.At, s.Bt, s.vals, s.X, s.w, s.status);
   ++ctx.launches;
   PARO_CUDA(cudaGetLastError());
   const int status = read_int(ctx, s.status);
