@@ -161,6 +161,22 @@ __global__ void invd_kernel(const double* c0, double sigma, double m0, const dou
 
 __global__ void set_flag_kernel(int* flag, int v) { *flag = v; }
 
+// x of the listed columns: row-padded solver layout (rows of S at stride P,
+// column stride ldi) -> the caller's dense layout (column stride ld); one warp
+// per row
+__global__ void unpad_cols_kernel(const double* __restrict__ src, long long ldi, double* __restrict__ dst, long long ld,
+                                  const int* __restrict__ cols, int S, int P) {
+  const int c = cols[blockIdx.y];
+  const long long rows = static_cast<long long>(S) * S;
+  const int lane = threadIdx.x & 31;
+  const long long w0 = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+  const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  const double* s = src + c * ldi;
+  double* d = dst + c * ld;
+  for (long long r = w0; r < rows; r += nw)
+    for (int x = lane; x < S; x += 32) d[r * S + x] = s[r * P + x];
+}
+
 // 8 coefficient slots (dense, slot o at o*n) -> row-padded layout, slot o at o*ldi
 __global__ void pad_coef_kernel(const double* __restrict__ coef, long long n, int S, int P, long long ldi,
                                 double* __restrict__ out) {
@@ -322,7 +338,7 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
     PARO_CUDA(cudaMemsetAsync(v + static_cast<long long>(cols) * ldi, 0, sizeof(double) * kBulkPad, st));
   };
   for (double* v : {r, p0, p1, xi}) zero_margins(v, K, np);
-  int* flag = ctx.flag.get<int>(3);
+  int* flag = ctx.flag.get<int>(3 + K);  // 3 flags + the copy-out column list
 
   PARO_CUDA(cudaMemcpyAsync(dcols, cols.data(), sizeof(CgColumn) * K, cudaMemcpyHostToDevice, st));
   if (scale_host) PARO_CUDA(cudaMemcpyAsync(dscale, scale_host, sizeof(double) * K, cudaMemcpyHostToDevice, st));
@@ -489,15 +505,24 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
   if (trace.on)
     for (int c = 0; c < K; ++c)
       if (cols[c].status == kNotSpd) std::fprintf(stderr, "[pcg] NotSpd column %d at iteration %llu\n", c, cols[c].it);
-  for (int c = 0; c < K && !aborted; ++c)
-    if (before[c].active) {
-      if (P == g.S)
-        PARO_CUDA(cudaMemcpyAsync(x + c * ld, xi + c * ldi, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-      else  // row-padded -> dense
-        PARO_CUDA(cudaMemcpy2DAsync(x + c * ld, sizeof(double) * g.S, xi + c * ldi, sizeof(double) * P,
-                                    sizeof(double) * g.S, static_cast<size_t>(g.S) * g.S, cudaMemcpyDeviceToDevice,
-                                    st));
+  if (!aborted) {
+    std::vector<int> out_cols;
+    for (int c = 0; c < K; ++c)
+      if (before[c].active) out_cols.push_back(c);
+    if (!out_cols.empty()) {
+      if (P == g.S) {
+        for (int c : out_cols)
+          PARO_CUDA(cudaMemcpyAsync(x + c * ld, xi + c * ldi, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+      } else {  // row-padded -> dense, every column in one launch
+        int* dlist = flag + 3;
+        PARO_CUDA(cudaMemcpyAsync(dlist, out_cols.data(), sizeof(int) * out_cols.size(), cudaMemcpyHostToDevice, st));
+        unpad_cols_kernel<<<dim3(148 * 2, static_cast<unsigned>(out_cols.size())), 256, 0, st>>>(xi, ldi, x, ld, dlist,
+                                                                                               g.S, P);
+        PARO_CUDA(cudaGetLastError());
+        ++ctx.launches;
+      }
     }
+  }
   PARO_CUDA(cudaStreamSynchronize(st));
   trace.mark("copy-out");
   double col_iters = 0.0, batch_iters = 0.0;
