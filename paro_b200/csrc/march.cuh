@@ -93,6 +93,7 @@ inline int padded_row(int S) { return S + (S & 1); }
 struct PcgTma {
   alignas(64) CUtensorMap r_halo, p0_halo, p1_halo, invd_halo, invd_own, x_own, r_own, coef_box;
   CUtensorMap r_fwd, p0_fwd, p1_fwd, invd_fwd, coef_own;  // one-sided (forward) boxes of K1 (k1f_kernel)
+  CUtensorMap x_halo;                                     // setup (k0c_kernel): x0 = u planes
   bool has_coef = false;  // coef_box: the operator's 8 coefficient slots in the row-padded layout
 };
 // coefp (optional): the 8 coefficient slots of a variable operator in the
@@ -102,6 +103,8 @@ void tma_plan(PcgTma& t, int S, long long ldi, int K, const double* r, const dou
 // K1 (p_new -> a.dst; its p_old is p0 when p_is_p0) or K2 (its stencil source p is p0
 // when p_is_p0), both on the row-padded layout described by t.
 void launch_tma(int mode, bool var, int cb, const MarchArgs& a, const PcgTma& t, bool p_is_p0, cudaStream_t st);
+// PCG setup (warm start, rhs = (M u) * scale) on the row-padded layout with x = u already in place
+void launch_tma_setup(int cb, const MarchArgs& a, const PcgTma& t, cudaStream_t st);
 
 void launch_march(int mode, bool var, int cb, const MarchArgs& a, cudaStream_t st);
 // K1/K2 on padded solver buffers (bulk.cu): every vector operand is 16-byte

@@ -177,6 +177,21 @@ __global__ void unpad_cols_kernel(const double* __restrict__ src, long long ldi,
     for (int x = lane; x < S; x += 32) d[r * S + x] = s[r * P + x];
 }
 
+// K columns: the caller's dense layout (stride ld) -> row-padded solver layout
+// (rows of S at stride P, column stride ldi); one warp per row
+__global__ void pad_cols_kernel(const double* __restrict__ src, long long ld, double* __restrict__ dst, long long ldi,
+                                int S, int P) {
+  const int c = blockIdx.y;
+  const long long rows = static_cast<long long>(S) * S;
+  const int lane = threadIdx.x & 31;
+  const long long w0 = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+  const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  const double* s = src + c * ld;
+  double* d = dst + c * ldi;
+  for (long long r = w0; r < rows; r += nw)
+    for (int x = lane; x < S; x += 32) d[r * P + x] = s[r * S + x];
+}
+
 // 8 coefficient slots (dense, slot o at o*n) -> row-padded layout, slot o at o*ldi
 __global__ void pad_coef_kernel(const double* __restrict__ coef, long long n, int S, int P, long long ldi,
                                 double* __restrict__ out) {
@@ -364,6 +379,19 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
   m.cols = dcols;
   m.partials = partials;
 
+  // tensor maps of the solver buffers (and the padded coefficient copy)
+  PcgTma tmaps;
+  if (use_tma) {
+    double* coefp = nullptr;
+    if (var) {  // the operator's coefficients in the row-padded layout for K2's TMA staging
+      coefp = ctx.coefp.get<double>(static_cast<size_t>(kSlots) * ldi);
+      pad_coef_kernel<<<148 * 8, 256, 0, st>>>(op.coef, n, g.S, P, ldi, coefp);
+      PARO_CUDA(cudaGetLastError());
+      ++ctx.launches;
+    }
+    tma_plan(tmaps, g.S, ldi, K, r, p0, p1, xi, invd, coefp);
+  }
+
   // setup: r0, x0, bnorm, rz0, rnorm0
   m.src = src;
   m.dst = r;
@@ -372,7 +400,19 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
   m.P = use_tma ? P : 0;
   m.scale = dscale;
   m.rhs = rhs;
-  launch_march(warm ? kSetupWarm : kSetupCold, var, cb, m, st);
+  static const bool no_tma_setup = [] {
+    const char* e = std::getenv("PARO_NO_TMA_SETUP");  // experiment knob: setup on the LDGSTS kernel
+    return e && e[0] == '1';
+  }();
+  if (use_tma && var && warm && rhs == nullptr && m.mwcoef == nullptr && !no_tma_setup) {
+    // x0 = u copied into the solver layout, then r0 = (M u) scale - A u on TMA planes of x
+    pad_cols_kernel<<<dim3(148 * 2, K), 256, 0, st>>>(src, ld, xi, ldi, g.S, P);
+    PARO_CUDA(cudaGetLastError());
+    launch_tma_setup(cb, m, tmaps, st);
+    ctx.launches += 2;
+  } else {
+    launch_march(warm ? kSetupWarm : kSetupCold, var, cb, m, st);
+  }
   fin_kernel<<<K, kFinThreads, 0, st>>>(kFinSetup, dcols, partials, m.nblk, flag);
   zero_marked_kernel<<<dim3(148, K), 256, 0, st>>>(dcols, K, xi, ldi, np);
   ctx.launches += 3;
@@ -386,17 +426,6 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
     const char* e = std::getenv("PARO_K1_BULK");  // experiment knob
     return e && e[0] == '1';
   }();
-  PcgTma tmaps;
-  if (use_tma) {
-    double* coefp = nullptr;
-    if (var) {  // the operator's coefficients in the row-padded layout for K2's TMA staging
-      coefp = ctx.coefp.get<double>(static_cast<size_t>(kSlots) * ldi);
-      pad_coef_kernel<<<148 * 8, 256, 0, st>>>(op.coef, n, g.S, P, ldi, coefp);
-      PARO_CUDA(cudaGetLastError());
-      ++ctx.launches;
-    }
-    tma_plan(tmaps, g.S, ldi, K, r, p0, p1, xi, invd, coefp);
-  }
   auto enqueue_chunk = [&](cudaStream_t s) {
     for (int it = 0; it < chunk; ++it) {
       MarchArgs k1 = m;

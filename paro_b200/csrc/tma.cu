@@ -856,6 +856,203 @@ __global__ void __launch_bounds__(kNT, kMinCtas)
   }
 }
 
+// ---------------------------------------------------------------------------
+// PCG setup on the TMA path (k0c, warm start with the mass right-hand side,
+// source_solve_step paro.cpp:96-104 / cg_solve linalg.cpp:150-189):
+//   b = (M u) (lambda + sigma), r = b - A u, partials b'b, r'z, r'r,
+// with u already copied into the solver's x (row-padded, pad_cols_kernel).
+// The u planes, the 8 coefficient slots and 1/diag arrive by TMA exactly as
+// in k2c; both row sums are summed without FMA contraction in ascending
+// column order, i.e. the reference CSR matvec's operations (as the
+// stream_kernel setup it replaces).
+template <int CB>
+__global__ void __launch_bounds__(kNT, kMinCtas)
+    k0c_kernel(const MarchArgs a, const __grid_constant__ CUtensorMap mp, const __grid_constant__ CUtensorMap mcoef,
+               const __grid_constant__ CUtensorMap minvd) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* smem = reinterpret_cast<double*>(smem_raw + ((128u - (su32(smem_raw) & 127u)) & 127u));
+  double* planes = smem;                       // [kNP][CB][kHB]
+  double* coefs = planes + kNP * CB * kHB;     // [kNP][kCS]
+  unsigned long long* barP = reinterpret_cast<unsigned long long*>(smem + k2c_data<CB>());
+  double(*red)[CB * 3] = reinterpret_cast<double(*)[CB * 3]>(barP + kNP);
+
+  const int S = a.S;
+  const int P = a.P;
+  const long long ld = a.ldw;  // column stride of the solver buffers
+  const int tid = threadIdx.x;
+  const int blk = blockIdx.y;
+  const int c0 = blockIdx.x * CB;
+
+  unsigned actm = 0;
+  int nact = 0;
+  double scl[CB];
+#pragma unroll
+  for (int j = 0; j < CB; ++j) {
+    const int c = c0 + j;
+    const bool on = c < a.K && a.cols[c].active != 0;
+    scl[j] = 0.0;
+    if (on) {
+      actm |= 1u << j;
+      ++nact;
+      scl[j] = a.scale[c];  // rhs scale lambda + sigma (paro.cpp:96-98)
+    }
+  }
+  if (actm == 0) return;
+  auto act = [&](int j) { return (actm >> j) & 1u; };
+
+  const int bx = blk % a.nTX;
+  const int by = (blk / a.nTX) % a.nTY;
+  const int bz = blk / (a.nTX * a.nTY);
+  const int x0 = bx * kTX, y0 = by * kTY;
+  const int z0 = bz * a.ZC;
+  const int z1 = min(S, z0 + a.ZC);
+  const int tx = tid % kTX, ty = tid / kTX;
+  const int gx = x0 + tx, gy = y0 + ty;
+  const bool inside = gx < S && gy < S;
+
+  if (tid == 0) {
+    for (int s = 0; s < kNP; ++s) mbar_init(&barP[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](int s, int z) {
+    mbar_arm(&barP[s], nact * kHaloBytes + (kSlots * kCR + kNT) * 8u);
+    double* d = planes + s * CB * kHB;
+#pragma unroll
+    for (int j = 0; j < CB; ++j)
+      if (act(j)) tma_load(d + j * kHB, &mp, x0 - 2, y0 - 1, z, c0 + j, &barP[s]);
+    double* cf = coefs + s * kCS;
+    tma_load(cf, &mcoef, x0 - 2, y0 - 1, z, 0, &barP[s]);
+    tma_load(cf + kSlots * kCR, &minvd, x0, y0, z, 0, &barP[s]);
+  };
+  unsigned phP = 0;
+  auto waitP = [&](int s) {
+    mbar_wait(&barP[s], (phP >> s) & 1u);
+    phP ^= 1u << s;
+  };
+  auto sp = [&](int t) { return (t - z0 + 1) % kNP; };
+  auto madd = [](double acc, double w, double x) { return __dadd_rn(acc, __dmul_rn(w, x)); };
+
+  if (tid == 0) {
+    issue(0, z0 - 1);
+    issue(1, z0);
+  }
+
+  double sC[CB], sN[CB], mC[CB], mN[CB], acc[CB][3];
+#pragma unroll
+  for (int j = 0; j < CB; ++j) {
+    sC[j] = sN[j] = mC[j] = mN[j] = 0.0;
+    acc[j][0] = acc[j][1] = acc[j][2] = 0.0;
+  }
+  double mw[kSlots];
+#pragma unroll
+  for (int o = 0; o < kSlots; ++o) mw[o] = a.mw[o];
+  double cPp[4] = {0.0, 0.0, 0.0, 0.0}, invdP = 0.0;
+  const int o0 = (ty + 1) * kRW + tx + 2;
+  const int ib = ty * kRW + tx + 1;
+  const long long own0 = static_cast<long long>(c0) * ld + static_cast<long long>(gy) * P + gx;
+
+  for (int t = z0 - 1; t <= z1; ++t) {
+    const bool rowP = t - 1 >= z0;
+    waitP(sp(t));
+    __syncthreads();
+    if (tid == 0 && t + 2 <= z1) issue(sp(t + 2), t + 2);
+    if (inside) {
+      const double* Pl = planes + sp(t) * CB * kHB;
+      const double* Cp = coefs + sp(t) * kCS;
+      double cN[4], cC[7];
+      cC[0] = Cp[1 * kCR + o0 - 1];
+      cC[1] = Cp[2 * kCR + o0 - kRW];
+      cC[2] = Cp[3 * kCR + o0 - kRW - 1];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cC[3 + i] = Cp[i * kCR + o0];
+      cN[0] = Cp[4 * kCR + o0];
+      cN[1] = Cp[5 * kCR + o0 - 1];
+      cN[2] = Cp[6 * kCR + o0 - kRW];
+      cN[3] = Cp[7 * kCR + o0 - kRW - 1];
+      const long long orow = own0 + static_cast<long long>(t - 1) * S * P;
+#pragma unroll
+      for (int j = 0; j < CB; ++j) {
+        const double* Pj = Pl + j * kHB + ib;
+        const double vmm = Pj[0], v0m = Pj[1], vm0 = Pj[kRW], v00 = Pj[kRW + 1];
+        const double vp0 = Pj[kRW + 2], v0p = Pj[2 * kRW + 1], vpp = Pj[2 * kRW + 2];
+        if (rowP) {
+          double sv = sC[j];
+          sv = madd(sv, cPp[0], v00);
+          sv = madd(sv, cPp[1], vp0);
+          sv = madd(sv, cPp[2], v0p);
+          sv = madd(sv, cPp[3], vpp);
+          double m = mC[j];
+          m = madd(m, mw[4], v00);
+          m = madd(m, mw[5], vp0);
+          m = madd(m, mw[6], v0p);
+          m = madd(m, mw[7], vpp);
+          const double bb = __dmul_rn(m, scl[j]);  // b = (M u) scale (model.cpp:248-249)
+          const double rr = __dsub_rn(bb, sv);     // r = b - A x0 (linalg.cpp:184-185)
+          st_if(a.dst + orow + j * ld, rr, act(j));
+          const double zz = __dmul_rn(invdP, rr);
+          acc[j][0] += bb * bb;
+          acc[j][1] += rr * zz;
+          acc[j][2] += rr * rr;
+        }
+        double c = sN[j];
+        c = madd(c, cC[2], vmm);
+        c = madd(c, cC[1], v0m);
+        c = madd(c, cC[0], vm0);
+        c = madd(c, cC[3], v00);
+        c = madd(c, cC[4], vp0);
+        c = madd(c, cC[5], v0p);
+        c = madd(c, cC[6], vpp);
+        double nx = 0.0;
+        nx = madd(nx, cN[3], vmm);
+        nx = madd(nx, cN[2], v0m);
+        nx = madd(nx, cN[1], vm0);
+        nx = madd(nx, cN[0], v00);
+        sC[j] = c;
+        sN[j] = nx;
+        double m = mN[j];
+        m = madd(m, mw[3], vmm);
+        m = madd(m, mw[2], v0m);
+        m = madd(m, mw[1], vm0);
+        m = madd(m, mw[0], v00);
+        m = madd(m, mw[1], vp0);
+        m = madd(m, mw[2], v0p);
+        m = madd(m, mw[3], vpp);
+        double mx = 0.0;
+        mx = madd(mx, mw[7], vmm);
+        mx = madd(mx, mw[6], v0m);
+        mx = madd(mx, mw[5], vm0);
+        mx = madd(mx, mw[4], v00);
+        mC[j] = m;
+        mN[j] = mx;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cPp[i] = Cp[(4 + i) * kCR + o0];
+      invdP = Cp[kSlots * kCR + tid];
+    }
+  }
+
+  const int warp = tid >> 5, lane = tid & 31;
+#pragma unroll
+  for (int j = 0; j < CB; ++j)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double v = warp_sum(acc[j][q]);
+      if (lane == 0) red[warp][j * 3 + q] = v;
+    }
+  __syncthreads();
+  if (tid < CB * 3) {
+    const int j = tid / 3, q = tid % 3;
+    if (act(j)) {
+      double sum = 0.0;
+#pragma unroll
+      for (int w = 0; w < kNT / 32; ++w) sum += red[w][tid];
+      a.partials[(static_cast<long long>(c0 + j) * 3 + q) * a.nblk + blk] = sum;
+    }
+  }
+}
+
 struct Maps {
   CUtensorMap a, b, c;
 };
@@ -916,6 +1113,19 @@ void launch_k2c(const MarchArgs& a, const Maps& m, cudaStream_t st) {
   PARO_CUDA(cudaGetLastError());
 }
 
+template <int CB>
+void launch_k0c(const MarchArgs& a, const Maps& m, cudaStream_t st) {
+  const int groups = (a.K + CB - 1) / CB;
+  constexpr size_t sm = k2c_smem<CB>() + sizeof(double) * (kNT / 32) * CB;  // 3 partials per column
+  static std::once_flag once;
+  std::call_once(once, [] {
+    PARO_CUDA(cudaFuncSetAttribute(k0c_kernel<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+  });
+  dim3 grid(groups, a.nblk);
+  k0c_kernel<CB><<<grid, kNT, sm, st>>>(a, m.a, m.b, m.c);
+  PARO_CUDA(cudaGetLastError());
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* f = nullptr;
@@ -952,6 +1162,7 @@ void tma_plan(PcgTma& t, int S, long long ldi, int K, const double* r, const dou
   encode(t.p0_halo, p0, S, ldi, K, kRW, kHY);
   encode(t.p1_halo, p1, S, ldi, K, kRW, kHY);
   encode(t.x_own, x, S, ldi, K, kTX, kTY);
+  encode(t.x_halo, x, S, ldi, K, kRW, kHY);
   encode(t.r_own, r, S, ldi, K, kTX, kTY);
   if (invd) {
     encode(t.invd_halo, invd, S, ldi, 1, kRW, kHY);
@@ -971,6 +1182,24 @@ void tma_plan(PcgTma& t, int S, long long ldi, int K, const double* r, const dou
   } else {
     t.coef_box = t.coef_own = t.r_halo;
   }
+}
+
+void launch_tma_setup(int cb, const MarchArgs& a, const PcgTma& t, cudaStream_t st) {
+  if (!t.has_coef) throw ParoError(kInvalidArgument, "tma setup: needs the padded coefficients");
+  if (a.P != padded_row(a.S) || a.mwcoef != nullptr || a.rhs != nullptr)
+    throw ParoError(kInvalidArgument, "tma setup: row-padded layout and a constant rhs mass required");
+  Maps m;
+  m.a = t.x_halo;
+  m.b = t.coef_box;
+  m.c = t.invd_own;
+  static const int forced = [] {
+    const char* e = std::getenv("PARO_MARCH_CB");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int c = forced > 0 && cb > forced ? forced : cb;
+  if (c == 1) launch_k0c<1>(a, m, st);
+  else if (c == 2) launch_k0c<2>(a, m, st);
+  else launch_k0c<4>(a, m, st);
 }
 
 void launch_tma(int mode, bool var, int cb, const MarchArgs& a, const PcgTma& t, bool p_is_p0, cudaStream_t st) {
