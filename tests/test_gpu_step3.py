@@ -145,10 +145,11 @@ def test_hartree_matches_reference(ref, gpu_ctx_factory):
 
 @pytest.mark.parametrize("s", [17, 20, 33])
 def test_source_step_even_and_odd_rows(ref, gpu_ctx_factory, s):
-    """Step 3 through every plane-staging path: even and odd interior row
-    length S = s - 1 (the bulk-copy K2 lays rows out with stride 38 / 37),
-    tiles that overhang the lattice in x and y, K >= 4 (bulk K2) and K = 2
-    (LDGSTS K2), against the reference at the solver tolerance."""
+    """Step 3 through the TMA PCG passes: even and odd interior row length
+    S = s - 1 (row-padded solver layout with P = S or S + 1), tiles that
+    overhang the lattice in x and y, several z-chunks, K = 6 (a 4-column group
+    plus a partial one) and K = 2, against the reference at the solver
+    tolerance."""
     from paro_b200 import core
 
     sp = ref.Space(s, -6.0, 6.0)
@@ -171,3 +172,36 @@ def test_source_step_even_and_odd_rows(ref, gpu_ctx_factory, s):
         h = half.cpu().numpy()
         for c in range(k):
             np.testing.assert_allclose(h[c], half_ref[c], rtol=0, atol=50 * tol * np.abs(half_ref[c]).max())
+
+
+@pytest.mark.parametrize("k", [1, 3, 5, 9])
+def test_variable_cg_column_groups(ref, gpu_ctx_factory, k):
+    """Batched Jacobi-PCG on a variable operator (TMA passes with staged
+    coefficients, symmetric p'Ap) for column counts that leave partial
+    column groups and columns that stop at different iterations, against the
+    reference cg_solve column by column (linalg.cpp:143-223)."""
+    from paro_b200 import core
+
+    sp, ks = _ops(ref, s=21)
+    ctx = gpu_ctx_factory(sp.s, sp.lo, sp.hi)
+    a0 = ks.op("kinetic").copy().add_scaled(ks.op("vext")).add_scaled(ks.op("mass"), 3.0)
+    ga = core.Operator.from_csr(ctx, *a0.csr())
+    assert ga.variable
+    rng = np.random.default_rng(100 + k)
+    # right-hand sides of different smoothness converge in different counts
+    B = rng.standard_normal((k, sp.n)) * np.linspace(0.2, 1.0, k)[:, None]
+    B[::2] = np.cumsum(B[::2], axis=1) / np.sqrt(sp.n)
+    X0 = rng.standard_normal((k, sp.n)) * 1e-3
+    if k > 2:  # column 1 starts next to its solution and stops early
+        xs = rng.standard_normal(sp.n)
+        B[1] = a0.matvec(xs)
+        X0[1] = xs + 1e-9 * rng.standard_normal(sp.n)
+    res = core.cg_solve(ga, _dev(B), _dev(X0), tol=1e-11, max_iter=5000)
+    iters = []
+    for c in range(k):
+        x, it, r, conv = ref.cg(a0, B[c], X0[c], tol=1e-11, max_iter=5000)
+        iters.append(it)
+        assert abs(res.iterations[c] - it) <= 1, (c, res.iterations[c], it)
+        np.testing.assert_allclose(res.x[c].cpu().numpy(), x, rtol=0, atol=1e-8 * np.abs(x).max())
+    if k > 2:
+        assert len(set(iters)) > 1  # the batch really ran with mixed active masks
