@@ -30,6 +30,7 @@ extern "C" {
 
 typedef struct paro_ctx paro_ctx;
 typedef struct paro_op paro_op;
+typedef struct paro_csr paro_csr;
 
 enum {
   PARO_OK = 0,
@@ -209,6 +210,27 @@ int paro_estimate_eta(paro_ctx* ctx, int N, const double* U, long long ld, const
 int paro_total_energy(paro_ctx* ctx, int n_lambdas, const double* lambdas, int nocc, const double* occ,
                       const double* rho, const double* vh, int exchange_only, int nnuc, const double* charges,
                       const double* positions, double* e_out);
+
+/* ---------------------------------------------- general CSR operators ---- */
+/* SparseOperator (linalg.hpp:14-50) for matrices that are not the uniform
+ * Kuhn stencil (adapted meshes): the reference's CSR arrays
+ * (size_t row offsets, uint32 ascending columns per row, double values), host
+ * pointers. Independent of paro_grid_init. Replaces the same calls as the
+ * stencil operators on such matrices: matvec (linalg.cpp:88-94), add_scaled
+ * (:120-125, identical structures or PARO_INVALID_ARGUMENT), cg_solve
+ * (:143-223) and source_solve_step (paro.cpp:81-119). Vectors: device,
+ * k columns at stride ld, k <= 256. */
+int paro_csr_create(paro_ctx* ctx, size_t n, const size_t* row_offsets, const uint32_t* cols, const double* vals,
+                    paro_csr** out);
+int paro_csr_destroy(paro_csr* a);
+int paro_csr_add_scaled(paro_ctx* ctx, paro_csr* a, const paro_csr* b, double s);
+int paro_csr_apply(paro_ctx* ctx, const paro_csr* a, int k, const double* x, long long ld, double* y);
+int paro_csr_cg_solve(paro_ctx* ctx, const paro_csr* a, int k, const double* b, const double* x0, long long ld,
+                      double tol, size_t max_iter, int throw_on_max_iter, double* x, size_t* iterations,
+                      double* residual);
+int paro_csr_source_solve_step(paro_ctx* ctx, const paro_csr* a, const paro_csr* b, int k, const double* u_prev,
+                               long long ld, const double* lambdas, double tol, size_t max_iter, double sigma,
+                               double* u_half, size_t* iterations, double* residual);
 
 #ifdef __cplusplus
 }

@@ -111,6 +111,12 @@ SIGNATURES = {
     "paro_assemble_vext": (_I, [_P, _I, _DP, _DP, _D, C.POINTER(_P)]),
     "paro_assemble_harmonic": (_I, [_P, _D, C.POINTER(_P)]),
     "paro_op_add_scaled": (_I, [_P, _P, _P, _D]),
+    "paro_csr_create": (_I, [_P, _SZ, _SZP, C.POINTER(C.c_uint32), _DP, C.POINTER(_P)]),
+    "paro_csr_destroy": (_I, [_P]),
+    "paro_csr_add_scaled": (_I, [_P, _P, _P, _D]),
+    "paro_csr_apply": (_I, [_P, _P, _I, _P, _LL, _P]),
+    "paro_csr_cg_solve": (_I, [_P, _P, _I, _P, _P, _LL, _D, _SZ, _I, _P, _SZP, _DP]),
+    "paro_csr_source_solve_step": (_I, [_P, _P, _P, _I, _P, _LL, _DP, _D, _SZ, _D, _P, _SZP, _DP]),
     "paro_ks_form": (_I, [_P, _P, _P, _P, _P, _I, _P, C.POINTER(_LL)]),
     "paro_density": (_I, [_P, _I, _P, _LL, _DP, _P, _DP]),
     "paro_mix_density": (_I, [_P, _P, _P, _D, _P]),

@@ -499,3 +499,80 @@ def estimate_eta(ctx: Context, orbitals: torch.Tensor, lambdas, *, diffusion: fl
                                         int(exchange_only), _ptr(eta) if eta is not None else None, C.byref(tot)))
     return (tot.value, eta) if with_eta else tot.value
 
+class CsrOperator:
+    """SparseOperator (linalg.hpp:14-50) for general sparse matrices (adapted
+    meshes): CSR on the device, independent of the uniform
+    grid. Same call surface as the stencil Operator for apply / add_scaled /
+    cg_solve / source_solve_step."""
+
+    def __init__(self, ctx: Context, rows, cols, vals):
+        rows = np.ascontiguousarray(rows, np.uintp)
+        cols = np.ascontiguousarray(cols, np.uint32)
+        vals = np.ascontiguousarray(vals, np.float64)
+        self.ctx = ctx
+        self.n = len(rows) - 1
+        self.h = None
+        h = C.c_void_p()
+        ctx.check(N.lib().paro_csr_create(ctx.h, self.n, rows.ctypes.data_as(C.POINTER(C.c_size_t)),
+                                          cols.ctypes.data_as(C.POINTER(C.c_uint32)), vals.ctypes.data_as(_DP),
+                                          C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                N.lib().paro_csr_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def add_scaled(self, other: "CsrOperator", s: float = 1.0) -> "CsrOperator":
+        """this += s * other on identical structures (linalg.cpp:120-125)."""
+        self.ctx.check(N.lib().paro_csr_add_scaled(self.ctx.h, self.h, other.h, s))
+        return self
+
+    def apply(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """y = A x for k columns (matvec, linalg.cpp:88-94)."""
+        squeeze = x.dim() == 1
+        xc = _as_cols(x, self.n).contiguous()
+        y = out if out is not None else torch.empty_like(xc)
+        self.ctx.check(N.lib().paro_csr_apply(self.ctx.h, self.h, xc.shape[0], _ptr(xc), self.n, _ptr(y)))
+        return y[0] if squeeze else y
+
+
+def csr_cg_solve(a: CsrOperator, b: torch.Tensor, x0: torch.Tensor | None = None, tol: float = 1e-10,
+                 max_iter: int = 10000, throw_on_max_iter: bool = True) -> CgResult:
+    """cg_solve (linalg.cpp:143-223) on a general CSR operator, k right-hand sides."""
+    ctx = a.ctx
+    squeeze = b.dim() == 1
+    bc = _as_cols(b, a.n).contiguous()
+    k = bc.shape[0]
+    x = torch.empty_like(bc)
+    x0c = _as_cols(x0, a.n).contiguous() if x0 is not None else None
+    it = (C.c_size_t * k)()
+    res = (C.c_double * k)()
+    st = N.lib().paro_csr_cg_solve(ctx.h, a.h, k, _ptr(bc), _ptr(x0c) if x0c is not None else None, a.n, tol,
+                                   max_iter, int(throw_on_max_iter), _ptr(x), it, res)
+    ctx.check(st)
+    iters, resid = list(it), list(res)
+    return CgResult(x[0] if squeeze else x, iters, resid, [r <= tol for r in resid])
+
+
+def csr_source_solve_step(a: CsrOperator, b: CsrOperator, u_prev: torch.Tensor, lambdas, tol: float = 1e-10,
+                          max_iter: int = 100000, sigma: float = 0.0, report: dict | None = None) -> torch.Tensor:
+    """source_solve_step (paro.cpp:81-119) on general CSR operators."""
+    ctx = a.ctx
+    u = _as_cols(u_prev, a.n).contiguous()
+    k = u.shape[0]
+    if len(lambdas) != k:
+        raise N.InvalidArgumentError("source_solve_step: orbital/lambda count mismatch")
+    y = torch.empty_like(u)
+    lam = (C.c_double * k)(*[float(v) for v in lambdas])
+    it = (C.c_size_t * k)()
+    res = (C.c_double * k)()
+    st = N.lib().paro_csr_source_solve_step(ctx.h, a.h, b.h, k, _ptr(u), a.n, lam, tol, max_iter, sigma, _ptr(y),
+                                            it, res)
+    if report is not None:
+        report.update(iterations=list(it), residual=list(res))
+    ctx.check(st)
+    return y

@@ -14,6 +14,7 @@
 #include "fields.hpp"
 #include "ritz.hpp"
 #include "solver.hpp"
+#include "csr.hpp"
 
 struct paro_ctx {
   paro_b200::Ctx c;
@@ -21,6 +22,9 @@ struct paro_ctx {
 struct paro_op {
   paro_b200::Op o;
   paro_ctx* owner = nullptr;
+};
+struct paro_csr {
+  paro_b200::CsrOp a;
 };
 
 using namespace paro_b200;
@@ -80,7 +84,7 @@ int paro_ctx_destroy(paro_ctx* ctx) {
   cudaStreamSynchronize(ctx->c.stream);
   for (DevBuf* b : {&ctx->c.partials, &ctx->c.cols, &ctx->c.scale, &ctx->c.invd, &ctx->c.pbuf0, &ctx->c.pbuf1,
                     &ctx->c.flag, &ctx->c.ws_a, &ctx->c.ws_b, &ctx->c.ws_c, &ctx->c.ws_d, &ctx->c.ws_e,
-                    &ctx->c.ws_small, &ctx->c.ws_small2, &ctx->c.dst_tab, &ctx->c.wtab, &ctx->c.shifted, &ctx->c.coefp, &ctx->c.pcg_x, &ctx->c.ws_gram,
+                    &ctx->c.ws_small, &ctx->c.ws_small2, &ctx->c.dst_tab, &ctx->c.wtab, &ctx->c.shifted, &ctx->c.coefp, &ctx->c.csr_ws, &ctx->c.csr_ws2, &ctx->c.csr_io, &ctx->c.pcg_x, &ctx->c.ws_gram,
                     &ctx->c.ws_small3})
     b->release();
   if (ctx->c.cublas) cublasDestroy(ctx->c.cublas);
@@ -608,6 +612,64 @@ int paro_fix_sign(paro_ctx* ctx, int k, double* v, long long ld) {
   return guarded(ctx, [&] {
     fix_sign_columns(ctx->c, v, ld, k);
     return kOk;
+  });
+}
+
+// ------------------------------------------------ general CSR operators
+int paro_csr_create(paro_ctx* ctx, size_t n, const size_t* rows, const uint32_t* cols, const double* vals,
+                    paro_csr** out) {
+  return guarded(ctx, [&] {
+    if (!rows || !cols || !vals || !out) throw ParoError(kInvalidArgument, "csr_create: null argument");
+    auto* h = new paro_csr();
+    try {
+      csr_create(ctx->c, static_cast<long long>(n), rows, cols, vals, h->a);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+    return kOk;
+  });
+}
+
+int paro_csr_destroy(paro_csr* a) {
+  delete a;
+  return kOk;
+}
+
+int paro_csr_add_scaled(paro_ctx* ctx, paro_csr* a, const paro_csr* b, double s) {
+  return guarded(ctx, [&] {
+    csr_add_scaled(ctx->c, a->a, b->a, s);
+    return kOk;
+  });
+}
+
+int paro_csr_apply(paro_ctx* ctx, const paro_csr* a, int k, const double* x, long long ld, double* y) {
+  return guarded(ctx, [&] {
+    csr_apply(ctx->c, a->a, k, x, ld, y);
+    PARO_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    return kOk;
+  });
+}
+
+int paro_csr_cg_solve(paro_ctx* ctx, const paro_csr* a, int k, const double* b, const double* x0, long long ld,
+                      double tol, size_t max_iter, int throw_on_max, double* x, size_t* iters, double* resid) {
+  return guarded(ctx, [&] {
+    SolveReport rep;
+    const int st = csr_cg_solve(ctx->c, a->a, k, b, x0, ld, tol, max_iter, throw_on_max != 0, x, &rep);
+    fill_report(rep, iters, resid);
+    return st;
+  });
+}
+
+int paro_csr_source_solve_step(paro_ctx* ctx, const paro_csr* a, const paro_csr* b, int k, const double* u,
+                               long long ld, const double* lambdas, double tol, size_t max_iter, double sigma,
+                               double* out, size_t* iters, double* resid) {
+  return guarded(ctx, [&] {
+    SolveReport rep;
+    const int st = csr_source_solve(ctx->c, a->a, b->a, sigma, k, u, ld, lambdas, tol, max_iter, out, &rep);
+    fill_report(rep, iters, resid);
+    return st;
   });
 }
 

@@ -65,6 +65,7 @@ struct Ctx {
   DevBuf pcg_x;                      // PCG iterate in the padded solver layout
   DevBuf shifted;                    // (A + sigma M) coefficients of the current shifted solve
   DevBuf coefp;                      // the same in the row-padded layout (TMA staging in the PCG passes)
+  DevBuf csr_ws, csr_ws2, csr_io;    // general-CSR solver: interleaved work vectors, retry iterate, rhs/x
   int* pinned_count = nullptr;       // mapped host memory for the active-column poll
   int* pinned_count_dev = nullptr;
 
