@@ -77,6 +77,38 @@ struct DevOp {
   DevOp& operator=(const DevOp&) = delete;
 };
 
+// general CSR operator on the device (adapted meshes)
+struct DevCsr {
+  paro_csr* op = nullptr;
+  explicit DevCsr(const SparseOperator& a) {
+    check(paro_csr_create(g.ctx, a.dimension(), a.row_offsets().data(), a.col_indices().data(), a.values().data(),
+                          &op));
+  }
+  ~DevCsr() {
+    if (op) paro_csr_destroy(op);
+  }
+  DevCsr(const DevCsr&) = delete;
+  DevCsr& operator=(const DevCsr&) = delete;
+};
+
+void ensure_ctx() {
+  if (!g.ctx && paro_ctx_create(0, nullptr, &g.ctx) != PARO_OK) throw Error(paro_ctx_last_error(nullptr));
+}
+
+// The stencil kernels serve operators of the bound uniform lattice whose
+// pattern is the P1/Kuhn stencil; everything else (adapted meshes) takes the
+// general CSR kernels.
+bool on_lattice(const SparseOperator& a) {
+  if (!g.ctx || g.n != a.dimension()) return false;
+  paro_op* op = nullptr;
+  const int st = paro_op_from_csr(g.ctx, a.dimension(), a.row_offsets().data(), a.col_indices().data(),
+                                  a.values().data(), &op);
+  if (op) paro_op_destroy(op);
+  if (st == PARO_INVALID_ARGUMENT) return false;
+  check(st);
+  return true;
+}
+
 void need(std::size_t n) {
   if (!g.ctx || g.n != n)
     throw InvalidArgumentError("paro::gpu: no device grid of dimension " + std::to_string(n) +
@@ -126,11 +158,11 @@ bool bound_to(const FeSpace& space) { return g.ctx && g.mesh_id == space.mesh().
 
 CgResult cg_solve(const SparseOperator& a, const std::vector<double>& b, const CgOptions& opts) {
   const std::size_t n = a.dimension();
-  need(n);
+  ensure_ctx();
   if (b.size() != n) throw InvalidArgumentError("cg: dimension mismatch");
   if (opts.precond != Preconditioner::diagonal)
     throw InvalidArgumentError("paro::gpu::cg_solve: only the Jacobi preconditioner is implemented");
-  DevOp A(a);
+  const bool lattice = on_lattice(a);
   DevVec db(n), dx(n);
   db.up(b.data(), n);
   DevVec dx0(opts.x0 ? n : 1);
@@ -140,8 +172,15 @@ CgResult cg_solve(const SparseOperator& a, const std::vector<double>& b, const C
   }
   std::size_t it = 0;
   double res = 0.0;
-  check(paro_cg_solve(g.ctx, A.op, 1, db.p, opts.x0 ? dx0.p : nullptr, static_cast<long long>(n), opts.tol,
-                      opts.max_iter, opts.throw_on_max_iter ? 1 : 0, dx.p, &it, &res));
+  if (lattice) {
+    DevOp A(a);
+    check(paro_cg_solve(g.ctx, A.op, 1, db.p, opts.x0 ? dx0.p : nullptr, static_cast<long long>(n), opts.tol,
+                        opts.max_iter, opts.throw_on_max_iter ? 1 : 0, dx.p, &it, &res));
+  } else {
+    DevCsr A(a);
+    check(paro_csr_cg_solve(g.ctx, A.op, 1, db.p, opts.x0 ? dx0.p : nullptr, static_cast<long long>(n), opts.tol,
+                            opts.max_iter, opts.throw_on_max_iter ? 1 : 0, dx.p, &it, &res));
+  }
   CgResult r;
   r.x.resize(n);
   dx.down(r.x.data(), n);
@@ -158,13 +197,19 @@ std::vector<std::vector<double>> source_solve_step(const SparseOperator& a, cons
   if (u_prev.size() != lambdas.size())
     throw InvalidArgumentError("source_solve_step: orbital/lambda count mismatch");
   const std::size_t n = a.dimension(), k = u_prev.size();
-  need(n);
+  ensure_ctx();
   if (k == 0) return {};
-  DevOp A(a), B(b);
   DevVec du = pack(u_prev, n);
   DevVec dh(k * n);
-  check(paro_source_solve_step(g.ctx, A.op, B.op, static_cast<int>(k), du.p, static_cast<long long>(n),
-                               lambdas.data(), opts.tol, opts.max_iter, opts.sigma, dh.p, nullptr, nullptr));
+  if (on_lattice(a) && on_lattice(b)) {
+    DevOp A(a), B(b);
+    check(paro_source_solve_step(g.ctx, A.op, B.op, static_cast<int>(k), du.p, static_cast<long long>(n),
+                                 lambdas.data(), opts.tol, opts.max_iter, opts.sigma, dh.p, nullptr, nullptr));
+  } else {  // adapted meshes: general CSR kernels, same semantics
+    DevCsr A(a), B(b);
+    check(paro_csr_source_solve_step(g.ctx, A.op, B.op, static_cast<int>(k), du.p, static_cast<long long>(n),
+                                     lambdas.data(), opts.tol, opts.max_iter, opts.sigma, dh.p, nullptr, nullptr));
+  }
   return unpack(dh, k, n);
 }
 
