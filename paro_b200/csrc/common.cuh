@@ -63,6 +63,7 @@ struct CgColumn {
   double rz;
   double pq;
   double alpha;
+  double alpha_prev;  // alpha of the previous iteration (deferred x updates, tma.cu k2c)
   double beta;
   double rnorm;
   double tol;

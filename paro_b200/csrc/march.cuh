@@ -78,6 +78,7 @@ struct MarchArgs {
   int with_dot = 0;              // Apply: accumulate x.y
   long long ldw = 0;             // Setup: stride of the x, r outputs (0: ld)
   int bulk = 0;                  // K1/K2: operands in padded solver buffers -> bulk-copy kernel
+  int xmode = 2;                 // K2 x update: 2 every iteration; deferred pairs (k2c): 0 none, 1 x += a' p' + a p
   int P = 0;                     // row length of the row-padded solver layout (0: dense S);
                                  // Setup writes x, r there, the TMA passes read/write it
 };
@@ -103,6 +104,8 @@ void tma_plan(PcgTma& t, int S, long long ldi, int K, const double* r, const dou
 // K1 (p_new -> a.dst; its p_old is p0 when p_is_p0) or K2 (its stencil source p is p0
 // when p_is_p0), both on the row-padded layout described by t.
 void launch_tma(int mode, bool var, int cb, const MarchArgs& a, const PcgTma& t, bool p_is_p0, cudaStream_t st);
+// true when K2 of a variable operator runs on k2c_kernel (which supports deferred x updates)
+bool tma_k2c_active();
 // PCG setup (warm start, rhs = (M u) * scale) on the row-padded layout with x = u already in place
 void launch_tma_setup(int cb, const MarchArgs& a, const PcgTma& t, cudaStream_t st);
 

@@ -90,6 +90,7 @@ __global__ void fin_kernel(int mode, CgColumn* cols, const double* partials, int
       atomicExch(flags + 1, 1);
       return;
     }
+    col.alpha_prev = col.alpha;
     col.alpha = col.rz / pq;
   } else {
     const double rzn = sum_partials(partials, c, 0, nblk, sh);

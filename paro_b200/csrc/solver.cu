@@ -54,8 +54,12 @@ __global__ void set_flag_kernel(int* flag, int v) { *flag = v; }
 // x of the listed columns: row-padded solver layout (rows of S at stride P,
 // column stride ldi) -> the caller's dense layout (column stride ld); one warp
 // per row
+// With deferred x updates (k2c pairs), a column whose last iteration index
+// was even still owes x += alpha p of that iteration (p in the p1 buffer):
+// applied here, fl(x + fl(alpha p)), exactly the skipped single update.
 __global__ void unpad_cols_kernel(const double* __restrict__ src, long long ldi, double* __restrict__ dst, long long ld,
-                                  const int* __restrict__ cols, int S, int P) {
+                                  const int* __restrict__ cols, int S, int P, const CgColumn* __restrict__ cst,
+                                  const double* __restrict__ p1, int deferred) {
   const int c = cols[blockIdx.y];
   const long long rows = static_cast<long long>(S) * S;
   const int lane = threadIdx.x & 31;
@@ -63,8 +67,14 @@ __global__ void unpad_cols_kernel(const double* __restrict__ src, long long ldi,
   const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
   const double* s = src + c * ldi;
   double* d = dst + c * ld;
+  const bool pending = deferred && (cst[c].it & 1ull);
+  const double al = cst[c].alpha;
+  const double* pp = p1 + c * ldi;
   for (long long r = w0; r < rows; r += nw)
-    for (int x = lane; x < S; x += 32) d[r * S + x] = s[r * P + x];
+    for (int x = lane; x < S; x += 32) {
+      const double v = s[r * P + x];
+      d[r * S + x] = pending ? __dadd_rn(v, __dmul_rn(al, pp[r * P + x])) : v;
+    }
 }
 
 // K columns: the caller's dense layout (stride ld) -> row-padded solver layout
@@ -316,6 +326,10 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
     const char* e = std::getenv("PARO_K1_BULK");  // experiment knob
     return e && e[0] == '1';
   }();
+  // x updates in pairs of iterations on the k2c pass (half the x traffic):
+  // even iterations leave x, odd ones apply both updates; a column stopping
+  // after an even iteration gets its last update at the copy-out
+  const bool deferred = use_tma && var && tma_k2c_active();
   auto enqueue_chunk = [&](cudaStream_t s) {
     for (int it = 0; it < chunk; ++it) {
       MarchArgs k1 = m;
@@ -334,6 +348,8 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
       k2.src = k1.dst;
       k2.x = xi;
       k2.r = r;
+      k2.xmode = deferred ? (it & 1) : 2;  // chunk is even: it has the global iteration's parity
+      k2.pold = k1.pold;                   // p of the previous iteration
       if (use_tma) launch_tma(kK2, var, cb, k2, tmaps, (it & 1) != 0, s);
       else if (op.mcoef || K < 4) launch_march(kK2, var, cb, k2, s);  // narrow batches: LDGSTS kernel
       else launch_bulk(kK2, var, cb, k2, s);
@@ -429,14 +445,14 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
     for (int c = 0; c < K; ++c)
       if (before[c].active) out_cols.push_back(c);
     if (!out_cols.empty()) {
-      if (P == g.S) {
+      if (P == g.S && !deferred) {
         for (int c : out_cols)
           PARO_CUDA(cudaMemcpyAsync(x + c * ld, xi + c * ldi, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-      } else {  // row-padded -> dense, every column in one launch
+      } else {  // row-padded -> dense (+ a pending deferred update), every column in one launch
         int* dlist = flag + 3;
         PARO_CUDA(cudaMemcpyAsync(dlist, out_cols.data(), sizeof(int) * out_cols.size(), cudaMemcpyHostToDevice, st));
-        unpad_cols_kernel<<<dim3(148 * 2, static_cast<unsigned>(out_cols.size())), 256, 0, st>>>(xi, ldi, x, ld, dlist,
-                                                                                               g.S, P);
+        unpad_cols_kernel<<<dim3(148 * 2, static_cast<unsigned>(out_cols.size())), 256, 0, st>>>(
+            xi, ldi, x, ld, dlist, g.S, P, dcols, p1, deferred ? 1 : 0);
         PARO_CUDA(cudaGetLastError());
         ++ctx.launches;
       }

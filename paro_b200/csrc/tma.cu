@@ -464,7 +464,11 @@ constexpr size_t k2c_smem() {
   return 128 + sizeof(double) * (k2c_data<CB>() + kNP + (kNT / 32) * CB * 2);
 }
 
-template <int CB>
+// XM: x update mode. 2: x += alpha p every iteration. Deferred pairs: 0 (even
+// iterations) leaves x untouched, 1 (odd) applies both pending updates,
+// x = fl(fl(x + fl(alpha' p')) + fl(alpha p)) with p' = the previous direction
+// (a.pold) -- the same operations as two single updates, at half the x traffic.
+template <int CB, int XM>
 __global__ void __launch_bounds__(kNT, CB >= 8 ? 1 : kMinCtas)
     k2c_kernel(const MarchArgs a, const __grid_constant__ CUtensorMap mp, const __grid_constant__ CUtensorMap mcoef,
                const __grid_constant__ CUtensorMap minvd) {
@@ -497,6 +501,10 @@ __global__ void __launch_bounds__(kNT, CB >= 8 ? 1 : kMinCtas)
     }
   }
   if (actm == 0) return;
+  // XM == 1: alpha of the previous iteration, parked in the (loop-idle)
+  // reduction scratch instead of registers
+  double* colA2 = &red[0][0];
+  if (XM == 1 && tid < CB) colA2[tid] = c0 + tid < a.K ? a.cols[c0 + tid].alpha_prev : 0.0;
   auto act = [&](int j) { return (actm >> j) & 1u; };
 
   const int bx = blk % a.nTX;
@@ -538,12 +546,12 @@ __global__ void __launch_bounds__(kNT, CB >= 8 ? 1 : kMinCtas)
   }
 
   double sC[CB], sN[CB], cCur[CB], acc[CB][2];
-  double xc[CB], rc[CB];  // own x, r of row t-1
+  double xc[CB], rc[CB], pp[CB];  // own x, r (and previous direction) of row t-1
 #pragma unroll
   for (int j = 0; j < CB; ++j) {
     sC[j] = sN[j] = cCur[j] = 0.0;
     acc[j][0] = acc[j][1] = 0.0;
-    xc[j] = rc[j] = 0.0;
+    xc[j] = rc[j] = pp[j] = 0.0;
   }
   double cPp[4] = {0.0, 0.0, 0.0, 0.0}, invdP = 0.0;  // own slots 4..7 and 1/diag of plane t-1
   const int o0 = (ty + 1) * kRW + tx + 2;               // own point in a coefficient box
@@ -559,7 +567,8 @@ __global__ void __launch_bounds__(kNT, CB >= 8 ? 1 : kMinCtas)
 #pragma unroll
       for (int j = 0; j < CB; ++j)
         if (act(j)) {
-          xc[j] = ldnc(a.x + o + j * ld);
+          if (XM != 0) xc[j] = ldnc(a.x + o + j * ld);
+          if (XM == 1) pp[j] = ldnc(a.pold + o + j * ld);
           rc[j] = ldnc(a.r + o + j * ld);
         }
     }
@@ -625,9 +634,14 @@ __global__ void __launch_bounds__(kNT, CB >= 8 ? 1 : kMinCtas)
 #pragma unroll
           for (int j = 0; j < CB; ++j) {
             // x += alpha p ; r -= alpha q ; z = invd r  (linalg.cpp:202-206)
-            const double xv = __dadd_rn(xc[j], __dmul_rn(colA[j], pOld[j]));
+            if (XM == 2) {
+              const double xv = __dadd_rn(xc[j], __dmul_rn(colA[j], pOld[j]));
+              st_if(a.x + orow + j * ld, xv, act(j));
+            } else if (XM == 1) {
+              const double xv = __dadd_rn(__dadd_rn(xc[j], __dmul_rn(colA2[j], pp[j])), __dmul_rn(colA[j], pOld[j]));
+              st_if(a.x + orow + j * ld, xv, act(j));
+            }
             const double rv = __dsub_rn(rc[j], __dmul_rn(colA[j], sP[j]));
-            st_if(a.x + orow + j * ld, xv, act(j));
             st_if(a.r + orow + j * ld, rv, act(j));
             const double zz = __dmul_rn(invdP, rv);
             acc[j][0] = fma(rv, zz, acc[j][0]);
@@ -644,6 +658,7 @@ __global__ void __launch_bounds__(kNT, CB >= 8 ? 1 : kMinCtas)
     }
   }
 
+  if (XM == 1) __syncthreads();  // colA2 lives in the reduction scratch
   const int warp = tid >> 5, lane = tid & 31;
 #pragma unroll
   for (int j = 0; j < CB; ++j)
@@ -1100,17 +1115,25 @@ void launch_k1f(const MarchArgs& a, const CUtensorMap& mr, const CUtensorMap& mp
   PARO_CUDA(cudaGetLastError());
 }
 
-template <int CB>
-void launch_k2c(const MarchArgs& a, const Maps& m, cudaStream_t st) {
+template <int CB, int XM>
+void launch_k2c_x(const MarchArgs& a, const Maps& m, cudaStream_t st) {
   const int groups = (a.K + CB - 1) / CB;
   constexpr size_t sm = k2c_smem<CB>();
   static std::once_flag once;
   std::call_once(once, [] {
-    PARO_CUDA(cudaFuncSetAttribute(k2c_kernel<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    PARO_CUDA(cudaFuncSetAttribute(k2c_kernel<CB, XM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(sm)));
   });
   dim3 grid(groups, a.nblk);
-  k2c_kernel<CB><<<grid, kNT, sm, st>>>(a, m.a, m.b, m.c);
+  k2c_kernel<CB, XM><<<grid, kNT, sm, st>>>(a, m.a, m.b, m.c);
   PARO_CUDA(cudaGetLastError());
+}
+
+template <int CB>
+void launch_k2c(const MarchArgs& a, const Maps& m, cudaStream_t st) {
+  if (a.xmode == 0) launch_k2c_x<CB, 0>(a, m, st);
+  else if (a.xmode == 1) launch_k2c_x<CB, 1>(a, m, st);
+  else launch_k2c_x<CB, 2>(a, m, st);
 }
 
 template <int CB>
@@ -1184,6 +1207,14 @@ void tma_plan(PcgTma& t, int S, long long ldi, int K, const double* r, const dou
   }
 }
 
+bool tma_k2c_active() {
+  static const bool no_k2c = [] {
+    const char* e = std::getenv("PARO_NO_K2C");  // experiment knob: coefficients by per-thread loads
+    return e && e[0] == '1';
+  }();
+  return !no_k2c;
+}
+
 void launch_tma_setup(int cb, const MarchArgs& a, const PcgTma& t, cudaStream_t st) {
   if (!t.has_coef) throw ParoError(kInvalidArgument, "tma setup: needs the padded coefficients");
   if (a.P != padded_row(a.S) || a.mwcoef != nullptr || a.rhs != nullptr)
@@ -1238,11 +1269,7 @@ void launch_tma(int mode, bool var, int cb, const MarchArgs& a, const PcgTma& t,
     m.a = p_is_p0 ? t.p0_halo : t.p1_halo;
     m.b = t.x_own;
     m.c = t.r_own;
-    static const bool no_k2c = [] {
-      const char* e = std::getenv("PARO_NO_K2C");  // experiment knob: coefficients by per-thread loads
-      return e && e[0] == '1';
-    }();
-    if (var && t.has_coef && !no_k2c) {
+    if (var && t.has_coef && tma_k2c_active()) {
       m.b = t.coef_box;
       m.c = t.invd_own;
       static const int forced = [] {
@@ -1258,6 +1285,8 @@ void launch_tma(int mode, bool var, int cb, const MarchArgs& a, const PcgTma& t,
       else if (c == 2) launch_k2c<2>(a, m, st);
       else if (c >= 8 && cb8) launch_k2c<8>(a, m, st);
       else launch_k2c<4>(a, m, st);
+    } else if (a.xmode != 2) {
+      throw ParoError(kInvalidArgument, "tma: deferred x updates need the k2c pass");
     } else if (var) launch_cb<kK2, true>(cb, a, m, st);
     else launch_cb<kK2, false>(cb, a, m, st);
   } else {
