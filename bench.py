@@ -173,6 +173,8 @@ def main():
     ap.add_argument("--workload", default="cluster32")
     ap.add_argument("--ref-sample", type=int, default=0, help="reference sample mesh subdivisions")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=int(os.environ.get("PARO_E2E_CHUNKS", "2")),
+                    help="column chunks of the host->device orbital copy in the e2e replay")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -253,7 +255,7 @@ def main():
             td.barrier()
         e0.record()
         for i in range(args.steps):
-            tr = run.step_host(args.warmup + i, h_orb, h_rho)
+            tr = run.step_host(args.warmup + i, h_orb, h_rho, chunks=args.e2e_chunks)
         e1.record()
         torch.cuda.synchronize()
         e_ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda", dtype=torch.float64)
