@@ -107,8 +107,7 @@ constexpr unsigned kOwnBytes = kNT * 8;          // 32 x 8 box
 constexpr int kNP = 3;                           // halo'd plane ring
 constexpr int kNX = 4;                           // K2 own-row ring (in-place update + store)
 
-// Each tensor map is its own __grid_constant__ parameter (wrapped in a struct
-// the descriptors faulted with an illegal instruction on this driver).
+// Each tensor map is its own __grid_constant__ parameter.
 // K1: ma = r, mb = p_old, mc = invd (halo'd boxes); K2: ma = p (halo'd box),
 // mb = x, mc = r (own-row boxes).
 
