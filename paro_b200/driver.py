@@ -232,6 +232,8 @@ class ParoRun:
         self.k = orb.shape[0]
         self.lambdas = lam
         self.clamped = 0
+        self._notspd_probe = []  # orbitals that met NotSpd in the last failing Step-3 attempt
+        self.probe_hits = 0      # Step-3 attempts decided by the probe alone
         self._chunks = None      # step_host: (c0, c1, copy event) of the local Step-3 columns
         self._out = None         # step_host: (copy stream, host orbitals) filled after Step 4
         self._copy_stream = None
@@ -255,6 +257,16 @@ class ParoRun:
         chunks = self._chunks if self._chunks is not None else [(c0, c1, None)]
         for attempt in range(5):
             self.last_attempts = attempt + 1
+            # NotSpd probe: an attempt fails as soon as any orbital's CG meets
+            # p'Ap <= 0, and each column's CG does not depend on the batch it
+            # runs in, so the orbitals that failed the last failing attempt are
+            # solved alone first; if one of them fails again the whole attempt
+            # has the same outcome without solving the other columns
+            # (the last attempt always runs in full: its error is the result)
+            if self._notspd_probe and attempt < 4 and self._probe(a, chunks, c0, c1, sigma, tol, attempt):
+                self.probe_hits += 1
+                sigma = 2.0 * sigma + 1.0
+                continue
             first, final, iters = [], [], []
             for k0, k1, ev in chunks:
                 if ev is not None and attempt == 0:
@@ -271,6 +283,8 @@ class ParoRun:
                 iters += i
             first = d.allgather_ints(first, counts, self._idev())
             final = d.allgather_ints(final, counts, self._idev())
+            if NOT_SPD in first:
+                self._notspd_probe = [c for c, f in enumerate(first) if f == NOT_SPD]
             code, col = step3_outcome(first, final)
             if code == NOT_SPD and attempt < 4:
                 sigma = 2.0 * sigma + 1.0
@@ -281,6 +295,25 @@ class ParoRun:
         all_iters = d.allgather_ints(iters, counts, self._idev())
         d.allgather_columns(local, counts, self.half)
         return sigma, all_iters
+
+    def _probe(self, a, chunks, c0, c1, sigma, tol, attempt) -> bool:
+        """Solve this rank's probe orbitals alone at sigma; True if any rank's
+        probe meets NotSpd (then the attempt fails like the full batch would)."""
+        w, be, d = self.w, self.be, self.dist
+        mine = [c for c in self._notspd_probe if c0 <= c < c1]
+        hit = 0
+        if mine:
+            if attempt == 0:  # step_host: the probe columns' copies must have landed
+                for k0, k1, ev in chunks:
+                    if ev is not None and any(k0 <= c < k1 for c in mine):
+                        torch.cuda.current_stream(be.device).wait_event(ev)
+            idx = torch.tensor(mine, device=self.orb.device)
+            u = self.orb.index_select(0, idx)
+            out = torch.empty_like(u)
+            f, _, _, _ = be.source_solve(a, u, [self.lambdas[c] for c in mine], sigma, tol, w.cg_max_iter, out)
+            hit = 1 if NOT_SPD in f else 0
+        hits = d.allgather_ints([hit], [1] * d.world, self._idev())
+        return any(h == 1 for h in hits)
 
     def _local(self, k):
         if self._half_local is None or self._half_local.shape[0] < k:

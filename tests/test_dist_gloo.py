@@ -9,7 +9,7 @@ import socket
 import pytest
 import torch.multiprocessing as mp
 
-CASES = [("oscillator@s8", 3), ("water@s12", 2), ("h2@s8", 2)]
+CASES = [("oscillator@s8", 3), ("water@s12", 2), ("h2@s8", 2), ("source64@s8", 3)]
 
 
 def _free_port() -> int:
@@ -77,3 +77,28 @@ def test_shard_and_outcome_logic():
     assert step3_outcome([OK, NOT_SPD, ITER_LIMIT], [OK, NOT_SPD, ITER_LIMIT]) == (ITER_LIMIT, 2)
     assert step3_outcome([OK, NOT_SPD, ITER_LIMIT], [OK, NOT_SPD, OK]) == (NOT_SPD, 1)
     assert step3_outcome([ITER_LIMIT, OK], [OK, OK]) == (OK, -1)
+
+
+def test_notspd_probe_keeps_the_trace():
+    """source64 escalates sigma every outer iteration (the first Step-3
+    attempt meets NotSpd); from the second iteration on the probe decides that
+    attempt from the previously failing orbital alone. The trace (lambdas,
+    sigma, CG iterations, orbitals) must equal the full-batch run's."""
+    from paro_b200 import configs
+    from paro_b200.driver import Dist, ParoRun
+    from portbackend import PortBackend
+
+    w = configs.get("source64@s8")
+
+    def run(probe):
+        r = ParoRun(w, PortBackend(w), Dist(), timers=False)
+        if not probe:
+            r._probe = lambda *a, **k: False
+        out = [r.step(i) for i in range(3)]
+        return r, [(list(t.lambdas), t.sigma, list(t.cg_iterations)) for t in out]
+
+    rp, tp = run(True)
+    rf, tf = run(False)
+    assert rp.probe_hits >= 1 and rf.probe_hits == 0
+    assert tp == tf
+    assert (rp.orb[: rp.k].numpy() == rf.orb[: rf.k].numpy()).all()
