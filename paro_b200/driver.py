@@ -363,7 +363,13 @@ class ParoRun:
             if h_rho is not None:
                 self.rho_in.copy_(h_rho, non_blocking=True)
                 main.wait_event(cs.record_event())
-            bounds = [c0 + ((c1 - c0) * i) // chunks for i in range(chunks + 1)]
+            # the first chunk is small (a multiple of the 4-column groups) so
+            # the Step-3 solves start early; the rest arrive while it runs
+            first = min(c1 - c0, max(4, ((c1 - c0) // 5 + 3) // 4 * 4)) if chunks == 2 else 0
+            if first:
+                bounds = [c0, c0 + first, c1]
+            else:
+                bounds = [c0 + ((c1 - c0) * i) // chunks for i in range(chunks + 1)]
             ranges = [(bounds[i], bounds[i + 1]) for i in range(chunks) if bounds[i + 1] > bounds[i]]
             evs = []
             for k0, k1 in ranges:
