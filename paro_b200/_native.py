@@ -6,9 +6,12 @@ product path raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 _LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libparo_b200.so"
+if os.environ.get("PARO_LIB"):  # experiment knob: A/B against another in-tree build of the same library
+    _LIB_PATH = Path(os.environ["PARO_LIB"]).resolve()
 
 _P = C.c_void_p
 _D = C.c_double

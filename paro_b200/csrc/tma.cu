@@ -825,24 +825,40 @@ __global__ void __launch_bounds__(kNT, kMinCtas)
   for (int j = 0; j < CB; ++j) acc[j] = 0.0;
   const int io = ty * kFW + tx;  // own point in a forward box
   const long long own0 = static_cast<long long>(c0) * ld + static_cast<long long>(gy) * P + gx;
+  // the four in-plane values a point reads of plane t+1 at step t are the
+  // ones it reads of plane t at step t+1: carried in registers, so every
+  // p_new plane is read from shared memory once
+  double cv[CB][4];
+#pragma unroll
+  for (int j = 0; j < CB; ++j) {
+    const double* A0 = ring + j * kFB + io;  // plane z0 (ring slot 0)
+    cv[j][0] = A0[0];
+    cv[j][1] = A0[1];
+    cv[j][2] = A0[kFW];
+    cv[j][3] = A0[kFW + 1];
+  }
   for (int t = z0; t < z1; ++t) {
-    const int q0 = (t - z0) % 3, q1 = (t + 1 - z0) % 3;
+    const int q1 = (t + 1 - z0) % 3;
     if (inside) {
       const long long orow = own0 + static_cast<long long>(t) * S * P;
 #pragma unroll
       for (int j = 0; j < CB; ++j) {
-        const double* A0 = ring + q0 * CB * kFB + j * kFB + io;  // plane t
         const double* A1 = ring + q1 * CB * kFB + j * kFB + io;  // plane t+1
-        const double pv = A0[0];
-        double s = w[1] * A0[1];
-        s = fma(w[2], A0[kFW], s);
-        s = fma(w[3], A0[kFW + 1], s);
-        s = fma(w[4], A1[0], s);
-        s = fma(w[5], A1[1], s);
-        s = fma(w[6], A1[kFW], s);
-        s = fma(w[7], A1[kFW + 1], s);
+        const double pv = cv[j][0];
+        const double n0 = A1[0], n1 = A1[1], n2 = A1[kFW], n3 = A1[kFW + 1];
+        double s = w[1] * cv[j][1];
+        s = fma(w[2], cv[j][2], s);
+        s = fma(w[3], cv[j][3], s);
+        s = fma(w[4], n0, s);
+        s = fma(w[5], n1, s);
+        s = fma(w[6], n2, s);
+        s = fma(w[7], n3, s);
         acc[j] = fma(pv, fma(2.0, s, w[0] * pv), acc[j]);  // p_v (A p)_v over the symmetric pairs
         st_if(a.dst + orow + j * ld, pv, act(j));         // p_new (own points of plane t)
+        cv[j][0] = n0;
+        cv[j][1] = n1;
+        cv[j][2] = n2;
+        cv[j][3] = n3;
       }
     }
     if (t + 1 < z1) load_w(t + 1);  // lands during the transform and the barrier

@@ -9,6 +9,7 @@ sigma, and size-independent density checksums (integral, L2 norm) of rho_out,
 plus the P1/Kuhn mass and stiffness stencils of a grid.
 """
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -21,6 +22,7 @@ from oracle import ref  # noqa: E402
 from paro_b200 import configs  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
+WORKERS = os.cpu_count() or 1  # per-column results do not depend on the worker count (parallel.hpp:10-12)
 
 
 def ks_trace(name, iters):
@@ -28,7 +30,8 @@ def ks_trace(name, iters):
     sp = ref.Space(w.subdivisions, w.lo, w.hi)
     ks = ref.KsSystem(sp, w.charges, w.positions, w.n_electrons, w.eps)
     g = configs.guess_vectors(w)
-    loop = ref.KsLoop(ks, g, w.cg_tol_start, w.cg_tol, w.cg_tol_factor, w.cg_max_iter, w.mixing_alpha, w.drop_tol)
+    loop = ref.KsLoop(ks, g, w.cg_tol_start, w.cg_tol, w.cg_tol_factor, w.cg_max_iter, w.mixing_alpha, w.drop_tol,
+                      WORKERS)
     rows = []
     lam0 = loop.get("lambdas").tolist()
     for it in range(iters):
@@ -49,7 +52,7 @@ def linear_trace(name, iters):
     b = ref.Op.mass(sp)
     g = configs.guess_vectors(w)
     loop = ref.LinLoop(sp, a, b, g, w.n_orbitals, w.cg_tol_start, w.cg_tol, w.cg_tol_factor, w.cg_max_iter,
-                       w.drop_tol)
+                       w.drop_tol, WORKERS)
     lam0 = loop.get("lambdas").tolist()
     rows = []
     for it in range(iters):
@@ -73,6 +76,29 @@ def stencils():
     return out
 
 
+# BASELINE configs at full size where the reference finishes here (configs[0]
+# H2 at 33^3 for all 20 iterations, configs[1] the oscillator at 65^3 for all
+# 40), and configs[2..4] on 65^3 meshes of the same generators (SURVEY 8d:
+# "run configs 4 and 5 scaled down (same generators at s = 64) fully on both
+# sides").  python tests/golden/make_golden.py full
+FULL = {
+    "h2": ("ks", 20),
+    "oscillator": ("linear", 40),
+    "water@s64": ("ks", 6),
+    "source64@s64": ("linear", 1),
+    "cluster32@s64": ("ks", 3),
+}
+
+
+def main_full(names=None):
+    for name, (kind, iters) in FULL.items():
+        if names and name not in names:
+            continue
+        fx = ks_trace(name, iters) if kind == "ks" else linear_trace(name, iters)
+        (OUT / f"full_{name.replace('@', '_')}.json").write_text(json.dumps(fx, indent=1))
+        print("wrote", name, flush=True)
+
+
 def main():
     fixtures = {
         "h2@s16": ks_trace("h2@s16", 6),
@@ -88,4 +114,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "full":
+        main_full(sys.argv[2:])
+    else:
+        main()

@@ -31,3 +31,14 @@ def test_gpu_matches_golden_trace(name):
             assert core.integrate(ctx, run.rho_out) == pytest.approx(row["rho_integral"], rel=1e-12)
             assert abs(core.norm_l2(ctx, run.rho_out) - row["rho_l2"]) <= 1e-7
             assert abs(tr.rho_residual - row["rho_residual"]) <= 1e-7
+
+
+FULL = sorted(p.stem for p in GOLDEN.glob("full_*.json"))
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_gpu_matches_golden_trace_full_size(name):
+    """BASELINE configs[0] and [1] at their full sizes and iteration counts
+    (H2 33^3 x 20, oscillator 65^3 x 40), configs[2..4] on 65^3 meshes of the
+    same generators (tests/golden/make_golden.py full)."""
+    test_gpu_matches_golden_trace(name)
