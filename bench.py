@@ -311,7 +311,7 @@ def main():
     a_ms = a0.elapsed_time(a1) / reps
     a_bytes = be.n * (16 * (c1 - c0) + 64)
     a_gbs = a_bytes / (a_ms * 1e-3) / 1e9
-    apply_line = {"kernel": "march.cu stream_kernel<Apply> (paro_op_apply), variable KS form, "
+    apply_line = {"kernel": "tma.cu k3f_kernel (paro_op_apply, bit-exact CSR row sums), variable KS form, "
                             f"k={c1 - c0} columns per launch", "ms": a_ms, "algorithmic_bytes": a_bytes,
                   "achieved_gbs": a_gbs, "frac_of_8tbs_nominal": a_gbs / 8000.0,
                   "frac_of_measured": a_gbs / peak if peak else None}

@@ -110,6 +110,12 @@ bool tma_k2c_active();
 void launch_tma_setup(int cb, const MarchArgs& a, const PcgTma& t, cudaStream_t st);
 
 void launch_march(int mode, bool var, int cb, const MarchArgs& a, cudaStream_t st);
+// y = A x on the dense layout by TMA through a flat 2S-wide view of x (odd S,
+// ld == n, 16-byte aligned x; coefp: the variable operator's coefficients in
+// the row-padded layout at slot stride ldi); apply_flat_ok says whether the
+// operands qualify (otherwise the apply stays on stream_kernel).
+bool apply_flat_ok(bool var, const MarchArgs& a);
+void launch_apply_flat(bool var, int cb, const MarchArgs& a, const double* coefp, long long ldi, cudaStream_t st);
 // K1/K2 on padded solver buffers (bulk.cu): every vector operand is 16-byte
 // aligned, has an even column stride and at least kBulkPad readable elements
 // before its first and after its last column.

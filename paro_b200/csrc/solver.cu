@@ -176,7 +176,23 @@ void apply_op(Ctx& ctx, const Op& a, const Op* shift, double sigma, int K, const
   m.op = preshift(ctx, make_opdev(ctx, a, shift, sigma));
   m.src = x;
   m.dst = y;
-  launch_march(kApply, a.var, pick_cb(K), m, ctx.stream);
+  if (apply_flat_ok(a.var, m)) {
+    const double* coefp = nullptr;
+    long long ldi = 0;
+    if (a.var) {  // the coefficients in the row-padded layout for the TMA staging
+      const int S = ctx.grid.S;
+      const int P = padded_row(S);
+      ldi = ((static_cast<long long>(S) * S * P + 2 * kBulkPad + 31) / 32) * 32;
+      double* cp = ctx.coefp.get<double>(static_cast<size_t>(kSlots) * ldi);
+      pad_coef_kernel<<<148 * 8, 256, 0, ctx.stream>>>(m.op.coef, ctx.grid.n, S, P, ldi, cp);
+      PARO_CUDA(cudaGetLastError());
+      ++ctx.launches;
+      coefp = cp;
+    }
+    launch_apply_flat(a.var, pick_cb(K), m, coefp, ldi, ctx.stream);
+  } else {
+    launch_march(kApply, a.var, pick_cb(K), m, ctx.stream);
+  }
   ++ctx.launches;
 }
 

@@ -1164,6 +1164,254 @@ void launch_k0c(const MarchArgs& a, const Maps& m, cudaStream_t st) {
   PARO_CUDA(cudaGetLastError());
 }
 
+
+// ---------------------------------------------------------------------------
+// Batched operator apply y = A x on the caller's DENSE layout (odd S, column
+// stride n), x planes staged by TMA (k3f). A tensor map needs 16-byte strides,
+// which the dense rows (S doubles, S odd) do not have, so x is described as a
+// flat 2-D view of the whole [K][n] buffer with rows of 2S doubles: lattice
+// row g (= c S^2 + z S + y over all columns) is element (g/2, x) of the view
+// when g is even and (g/2, S + x) when g is odd. The ten halo rows of a tile
+// plane alternate in parity, so they arrive as two boxes of 5 view rows x 36,
+// one per parity; an even row's box starts at x0 - 2 and an odd row's at
+// S + x0 - 1, both 16-byte aligned (odd S). Neighbours outside the lattice
+// are other rows / planes / columns in the flat view and are masked to zero
+// by the consumer (the Dirichlet elimination, fem.cpp:21-28). Coefficients of
+// a variable operator come from the row-padded copy by one [8][9][36] box per
+// plane exactly as in k2c. Row sums: the streaming sums of stream_kernel in
+// ascending column order without FMA contraction, i.e. the operations of the
+// reference CSR matvec (linalg.cpp:88-94), so y is bit-identical to it.
+constexpr int kFV = 5 * kRW;  // one parity box: 5 view rows x 36
+constexpr int kFS = 192;      // parity box stride (128-byte aligned)
+constexpr int kFC = 2 * kFS;  // per-column plane slot
+
+template <bool VAR, int CB>
+constexpr int k3f_data() {
+  return kNP * CB * kFC + (VAR ? kNP * kSlots * kCR : 0);
+}
+template <bool VAR, int CB>
+constexpr size_t k3f_smem() {
+  return 128 + sizeof(double) * (k3f_data<VAR, CB>() + kNP);
+}
+
+__device__ __forceinline__ void tma_load2(double* dst, const CUtensorMap* map, int x, int y, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::
+          "r"(su32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(su32(bar))
+      : "memory");
+}
+
+template <bool VAR, int CB>
+__global__ void __launch_bounds__(kNT, VAR ? kMinCtas : 3)
+    k3f_kernel(const MarchArgs a, const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mcoef) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* smem = reinterpret_cast<double*>(smem_raw + ((128u - (su32(smem_raw) & 127u)) & 127u));
+  double* planes = smem;                    // [kNP][CB][kFC]: parity boxes [2][5][36] per column
+  double* coefs = planes + kNP * CB * kFC;  // [kNP][kSlots][kCR] (VAR)
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + k3f_data<VAR, CB>());
+
+  const int S = a.S;
+  const int S2 = S * S;
+  const int tid = threadIdx.x;
+  const int blk = blockIdx.y;
+  const int c0 = blockIdx.x * CB;
+  const int ncol = min(CB, a.K - c0);
+
+  const int bx = blk % a.nTX;
+  const int by = (blk / a.nTX) % a.nTY;
+  const int bz = blk / (a.nTX * a.nTY);
+  const int x0 = bx * kTX, y0 = by * kTY;
+  const int z0 = bz * a.ZC;
+  const int z1 = min(S, z0 + a.ZC);
+  const int tx = tid % kTX, ty = tid / kTX;
+  const int gx = x0 + tx, gy = y0 + ty;
+  const bool inside = gx < S && gy < S;
+
+  if (tid == 0) {
+    for (int s = 0; s < kNP; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // thread 0: plane z of the x columns (two parity boxes each) and of the coefficients into slot s
+  auto issue = [&](int s, int z) {
+    const bool zin = z >= 0 && z < S;
+    mbar_arm(&bar[s], (zin ? static_cast<unsigned>(ncol) * 2u * kFV * 8u : 0u) + (VAR ? kSlots * kCR * 8u : 0u));
+    if (zin) {
+#pragma unroll
+      for (int j = 0; j < CB; ++j) {
+        if (j >= ncol) continue;
+        const int gf = (c0 + j) * S2 + z * S + y0 - 1;  // lattice row of halo row 0
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int g = gf + h;
+          tma_load2(planes + (s * CB + j) * kFC + h * kFS, &mx, (g & 1) ? S + x0 - 1 : x0 - 2, g >> 1, &bar[s]);
+        }
+      }
+    }
+    if (VAR) tma_load(coefs + s * kSlots * kCR, &mcoef, x0 - 2, y0 - 1, z, 0, &bar[s]);
+  };
+  unsigned ph = 0;
+
+  if (tid == 0) {
+    issue(0, z0 - 1);
+    issue(1, z0);
+  }
+
+  double sC[CB], sN[CB];
+#pragma unroll
+  for (int j = 0; j < CB; ++j) sC[j] = sN[j] = 0.0;
+  double cPp[4] = {0.0, 0.0, 0.0, 0.0};  // own slots 4..7 of plane t-1
+  const int o0 = (ty + 1) * kRW + tx + 2;
+  const long long own = static_cast<long long>(gy) * S + gx;
+  auto madd = [](double s, double w, double x) { return __dadd_rn(s, __dmul_rn(w, x)); };
+
+  // tiles touching the lattice boundary: halo cells outside the lattice hold
+  // other rows / planes / columns of the flat view and are zeroed in shared
+  // memory once the plane has landed (the Dirichlet elimination), so the
+  // stencil body itself needs no masks
+  const bool edge = x0 == 0 || x0 + kTX >= S || y0 == 0 || y0 + kTY >= S;
+  auto zero_edges = [&](int s, int t) {
+    const int ex0 = x0 == 0 ? 1 : 0, ex1 = x0 + kTX >= S ? 1 : 0;  // halo columns x = -1, x = S
+    const int ey0 = y0 == 0 ? 1 : 0, ey1 = y0 + kTY >= S ? 1 : 0;  // halo rows y = -1, y = S
+    const int ncolx = (ex0 + ex1) * (kTY + 2), nrowx = (ey0 + ey1) * (kTX + 2);
+    const int per = ncolx + nrowx;
+    for (int i = tid; i < CB * per; i += kNT) {
+      const int j = i / per, q = i % per;
+      int hy, x;
+      if (q < ncolx) {
+        hy = q % (kTY + 2);
+        x = (ex0 && q < kTY + 2) ? -1 : S;
+      } else {
+        const int r = q - ncolx;
+        hy = (ey0 && r < kTX + 2) ? 0 : S - y0 + 1;
+        x = x0 - 1 + r % (kTX + 2);
+      }
+      const int sh = ((c0 + j + t + y0 - 1 + hy) & 1) ? 1 : 2;
+      planes[(s * CB + j) * kFC + (hy & 1) * kFS + (hy >> 1) * kRW + (x - x0) + sh] = 0.0;
+    }
+  };
+  // thread-constant parts of the three window rows' offsets (row y-1 and y+1
+  // share a box; the parity shift of row y-1 alternates with the column)
+  const int offm = (ty & 1) * kFS + (ty >> 1) * kRW + tx;
+  const int off0 = ((ty + 1) & 1) * kFS + ((ty + 1) >> 1) * kRW + tx;
+  // output row pointers of the CB columns (row z0 first), advanced a plane per completed row
+  double* yrow[CB];
+#pragma unroll
+  for (int j = 0; j < CB; ++j)
+    yrow[j] = a.dst + static_cast<long long>(min(c0 + j, a.K - 1)) * a.ld + static_cast<long long>(z0) * S2 + own;
+
+  for (int t = z0 - 1; t <= z1; ++t) {
+    const int s = (t - z0 + 1) % kNP;
+    mbar_wait(&bar[s], (ph >> s) & 1u);
+    ph ^= 1u << s;
+    const bool zin = t >= 0 && t < S;
+    if (edge && zin) zero_edges(s, t);
+    __syncthreads();  // slot of plane t-1 (read at step t-1) may be refilled; zeroed edges visible
+    if (tid == 0 && t + 2 <= z1) issue((t + 3 - z0) % kNP, t + 2);
+    if (!inside) continue;
+    const bool rowP = t - 1 >= z0;
+    double wN[4], wC[7];
+    if (VAR) {
+      const double* Cp = coefs + s * kSlots * kCR;
+      wC[0] = Cp[1 * kCR + o0 - 1];        // slot 1 at (-1, 0)
+      wC[1] = Cp[2 * kCR + o0 - kRW];      // slot 2 at (0, -1)
+      wC[2] = Cp[3 * kCR + o0 - kRW - 1];  // slot 3 at (-1, -1)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) wC[3 + i] = Cp[i * kCR + o0];  // own slots 0..3
+      wN[0] = Cp[4 * kCR + o0];
+      wN[1] = Cp[5 * kCR + o0 - 1];
+      wN[2] = Cp[6 * kCR + o0 - kRW];
+      wN[3] = Cp[7 * kCR + o0 - kRW - 1];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) wN[i] = a.op.wc[4 + i];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) wC[i] = a.op.wc[1 + i];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) wC[3 + i] = a.op.wc[i];
+    }
+    double wP[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) wP[i] = VAR ? cPp[i] : a.op.wc[4 + i];
+    // window rows of column j: row y-1 / y+1 at Rm + j kFC, row y at R0 + j kFC,
+    // with the parity shift alternating between even and odd columns
+    const int par = (c0 + t + y0 - 1 + ty) & 1;  // parity of row y-1 in column c0
+    const double* slot = planes + s * CB * kFC;
+    const double* RmE = slot + offm + (par ? 1 : 2);
+    const double* RmO = slot + offm + (par ? 2 : 1);
+    const double* R0E = slot + off0 + (par ? 2 : 1);
+    const double* R0O = slot + off0 + (par ? 1 : 2);
+    auto body = [&](auto zin_t) {
+      constexpr bool ZIN = decltype(zin_t)::value;
+#pragma unroll
+      for (int j = 0; j < CB; ++j) {
+        double vmm = 0.0, v0m = 0.0, vm0 = 0.0, v00 = 0.0, vp0 = 0.0, v0p = 0.0, vpp = 0.0;
+        if (ZIN) {
+          const double* Rm = ((j & 1) ? RmO : RmE) + j * kFC;
+          const double* R0 = ((j & 1) ? R0O : R0E) + j * kFC;
+          vmm = Rm[-1];
+          v0m = Rm[0];
+          vm0 = R0[-1];
+          v00 = R0[0];
+          vp0 = R0[1];
+          v0p = Rm[kRW];
+          vpp = Rm[kRW + 1];
+        }
+        if (rowP) {  // Pp terms complete row t-1 (forward slots 4..7)
+          double r = sC[j];
+          r = madd(r, wP[0], v00);
+          r = madd(r, wP[1], vp0);
+          r = madd(r, wP[2], v0p);
+          r = madd(r, wP[3], vpp);
+          st_if(yrow[j], r, j < ncol);
+        }
+        // centre terms of row t (back 3..1, diagonal, forward 1..3), Pm terms of row t+1 (back 7..4)
+        double c = sN[j];
+        c = madd(c, wC[2], vmm);
+        c = madd(c, wC[1], v0m);
+        c = madd(c, wC[0], vm0);
+        c = madd(c, wC[3], v00);
+        c = madd(c, wC[4], vp0);
+        c = madd(c, wC[5], v0p);
+        c = madd(c, wC[6], vpp);
+        double nx = madd(0.0, wN[3], vmm);  // +0 start as the CSR row sum (keeps the sign of zero)
+        nx = madd(nx, wN[2], v0m);
+        nx = madd(nx, wN[1], vm0);
+        nx = madd(nx, wN[0], v00);
+        sC[j] = c;
+        sN[j] = nx;
+      }
+    };
+    if (zin) body(std::true_type{});
+    else body(std::false_type{});
+    if (rowP) {
+#pragma unroll
+      for (int j = 0; j < CB; ++j) yrow[j] += S2;
+    }
+    if (VAR) {
+      const double* Cp = coefs + s * kSlots * kCR;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cPp[i] = Cp[(4 + i) * kCR + o0];
+    }
+  }
+}
+
+template <bool VAR, int CB>
+void launch_k3f(const MarchArgs& a, const CUtensorMap& mx, const CUtensorMap& mc, cudaStream_t st) {
+  const int groups = (a.K + CB - 1) / CB;
+  constexpr size_t sm = k3f_smem<VAR, CB>();
+  static std::once_flag once;
+  std::call_once(once, [] {
+    PARO_CUDA(cudaFuncSetAttribute(k3f_kernel<VAR, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(sm)));
+  });
+  dim3 grid(groups, a.nblk);
+  k3f_kernel<VAR, CB><<<grid, kNT, sm, st>>>(a, mx, mc);
+  PARO_CUDA(cudaGetLastError());
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* f = nullptr;
@@ -1219,6 +1467,70 @@ void tma_plan(PcgTma& t, int S, long long ldi, int K, const double* r, const dou
     encode(t.coef_own, coefp, S, ldi, kSlots, kTX, kTY, kSlots);
   } else {
     t.coef_box = t.coef_own = t.r_halo;
+  }
+}
+
+bool apply_flat_ok(bool var, const MarchArgs& a) {
+  static const bool off = [] {
+    const char* e = std::getenv("PARO_NO_FLAT_APPLY");  // experiment knob: apply on stream_kernel
+    return e && e[0] == '1';
+  }();
+  const int S = a.S;
+  if (off || (S & 1) == 0 || a.ld != a.n || a.with_dot || a.op.mcoef != nullptr) return false;
+  if (var && a.op.sigma != 0.0) return false;
+  if ((reinterpret_cast<uintptr_t>(a.src) & 15) != 0) return false;
+  const long long rows = static_cast<long long>(a.K) * S * S;  // lattice rows of all columns
+  if (rows / 2 + 1 > (1ll << 31) - 1) return false;
+  // an odd row count leaves the last lattice row in a half-filled view row:
+  // it is read only if the allocation extends S doubles past the operand
+  const long long vrows = (rows + 1) / 2;
+  if ((rows & 1) != 0) {
+    static PFN_cuMemGetAddressRange_v3020 range = [] {
+      void* f = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      PARO_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q));
+      return q == cudaDriverEntryPointSuccess ? reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(f) : nullptr;
+    }();
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range == nullptr || range(&base, &size, reinterpret_cast<CUdeviceptr>(a.src)) != CUDA_SUCCESS) return false;
+    const uintptr_t need = reinterpret_cast<uintptr_t>(a.src + rows * S + S);
+    if (need > static_cast<uintptr_t>(base) + size) return false;
+  }
+  return true;
+}
+
+void launch_apply_flat(bool var, int cb, const MarchArgs& a, const double* coefp, long long ldi, cudaStream_t st) {
+  const int S = a.S;
+  const long long rows = static_cast<long long>(a.K) * S * S;
+  const long long vrows = (rows + 1) / 2;
+  if (var && coefp == nullptr) throw ParoError(kInvalidArgument, "apply: padded coefficients missing");
+  CUtensorMap mx, mc;
+  {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(2 * S), static_cast<cuuint64_t>(vrows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(2 * S) * 8};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kRW), 5};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encoder()(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(a.src), dims, strides,
+                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw ParoError(kCuda, "tma: flat view encode failed (" + std::to_string(r) + ")");
+  }
+  if (var) encode(mc, coefp, S, ldi, kSlots, kRW, kTY + 1, kSlots);
+  else mc = mx;
+  static const int forced = [] {
+    const char* e = std::getenv("PARO_MARCH_CB");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int c = forced > 0 && cb > forced ? forced : cb;
+  if (var) {
+    if (c == 1) launch_k3f<true, 1>(a, mx, mc, st);
+    else if (c == 2) launch_k3f<true, 2>(a, mx, mc, st);
+    else launch_k3f<true, 4>(a, mx, mc, st);
+  } else {
+    if (c == 1) launch_k3f<false, 1>(a, mx, mc, st);
+    else if (c == 2) launch_k3f<false, 2>(a, mx, mc, st);
+    else launch_k3f<false, 4>(a, mx, mc, st);
   }
 }
 

@@ -237,6 +237,13 @@ class ParoRun:
         self._chunks = None      # step_host: (c0, c1, copy event) of the local Step-3 columns
         self._out = None         # step_host: (copy stream, host orbitals) filled after Step 4
         self._copy_stream = None
+        self.timeline = None     # profiling: list of (label, CUDA event) marks, or None
+
+    def _mark(self, label, stream=None):
+        if self.timeline is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(stream)
+            self.timeline.append((label, ev))
 
     def _sync(self):
         if self.timers:
@@ -338,7 +345,9 @@ class ParoRun:
         o0, o1, _ = self.dist.shard(orb.shape[0])
         cs.wait_stream(torch.cuda.current_stream(self.be.device))
         with torch.cuda.stream(cs):
+            self._mark("d2h_start", cs)
             h_orb[o0:o1].copy_(orb[o0:o1], non_blocking=True)
+            self._mark("d2h_end", cs)
 
     def step_host(self, it: int, h_orb: torch.Tensor, h_rho: torch.Tensor | None = None,
                   chunks: int = 2) -> Trace:
@@ -372,9 +381,11 @@ class ParoRun:
                 bounds = [c0 + ((c1 - c0) * i) // chunks for i in range(chunks + 1)]
             ranges = [(bounds[i], bounds[i + 1]) for i in range(chunks) if bounds[i + 1] > bounds[i]]
             evs = []
+            self._mark("h2d_start", cs)
             for k0, k1 in ranges:
                 self.orb[k0:k1].copy_(h_orb[k0:k1], non_blocking=True)
                 evs.append(cs.record_event())
+                self._mark(f"h2d_cols_{k0}_{k1}", cs)
         self._chunks = [(k0, k1, ev) for (k0, k1), ev in zip(ranges, evs)]
         self._out = (cs, h_orb)
         try:
@@ -399,8 +410,10 @@ class ParoRun:
         t_meshgen = time.perf_counter() - t2
         a_in, cl = be.ks_form(self.rho_in, vh_in, "in")
         self.clamped += cl
+        self._mark("step3_start")
         ts = time.perf_counter()
         sigma, iters = self.step3(a_in, it)
+        self._mark("step3_end")
         self._sync()
         t_source = time.perf_counter() - ts
         tp = time.perf_counter()
@@ -410,6 +423,7 @@ class ParoRun:
         a_half, cl = be.ks_form(rho_half, vh_half, "half")
         self.clamped += cl
         orb, lam, defect = be.ritz(half, a_half, N_, w.drop_tol, self.orb)
+        self._mark("ritz_end")
         if self._out is not None:  # step_host: the orbitals leave while the density work runs
             self._copy_out(orb)
         self._sync()
@@ -420,6 +434,7 @@ class ParoRun:
         e_tot = be.energy(lam, self.occ, rho_out, vh_out)
         res = be.rho_residual(rho_out, self.rho_in)
         be.mix(self.rho_in, rho_out, w.mixing_alpha, out=self.rho_in)
+        self._mark("step_end")
         self._sync()
         return Trace(it + 1, lam[: w.n_orbitals], e_tot, res, sigma, defect, iters, t_source, t_project,
                      time.perf_counter() - t0, eta, t_meshgen, be.n)

@@ -49,6 +49,34 @@ def main():
     res["step_host_s"], _ = timed(lambda: run.step_host(3, h_orb, h_rho, chunks=a.chunks))
     res["step_host2_s"], _ = timed(lambda: run.step_host(4, h_orb, h_rho, chunks=a.chunks))
     res["serial_estimate_s"] = res["h2d_s"] + res["step_s"] + res["d2h_s"]
+    # both directions at once (full-duplex PCIe)
+    scratch = torch.empty_like(run.half[:K])
+    cs = torch.cuda.Stream()
+
+    def both():
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            h_orb.copy_(scratch, non_blocking=True)
+        run.orb[:K].copy_(h_orb_b, non_blocking=True)
+        torch.cuda.current_stream().wait_stream(cs)
+
+    h_orb_b = torch.empty_like(h_orb, pin_memory=True)
+    h_orb_b.copy_(h_orb)
+    res["h2d_plus_d2h_concurrent_s"], _ = timed(both)
+    h_orb.copy_(run.orb[:K])
+    h_rho.copy_(run.rho_in)
+    # timeline of one step_host: marks on the main and the copy stream
+    run.timeline = []
+    start = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record()
+    run.step_host(5, h_orb, h_rho, chunks=a.chunks)
+    end = torch.cuda.Event(enable_timing=True)
+    end.record()
+    torch.cuda.synchronize()
+    res["timeline_ms"] = {lbl: round(start.elapsed_time(ev), 2) for lbl, ev in run.timeline}
+    res["timeline_ms"]["returned"] = round(start.elapsed_time(end), 2)
+    run.timeline = None
     print(json.dumps(res))
 
 

@@ -1,7 +1,9 @@
 """GPU runs of the BASELINE generators (scaled meshes) against the committed
 golden fixtures produced by the compiled reference (tests/golden/make_golden.py).
-North-star tolerances: eigenvalues 1e-8 relative, energy 1e-8 Ha; the density
-is compared through its size-independent checksums (integral, L2 norm)."""
+North-star tolerances: eigenvalues 1e-8 relative (with a 1e-10 Ha absolute
+floor for eigenvalues near zero, a hundredth of the energy bar), energy
+1e-8 Ha; the density is compared through its size-independent checksums
+(integral, L2 norm)."""
 import json
 from pathlib import Path
 
@@ -23,7 +25,7 @@ def test_gpu_matches_golden_trace(name):
     np.testing.assert_allclose(run.lambdas[: len(fx["lambdas0"])], fx["lambdas0"], rtol=1e-10)
     for row in fx["trace"]:
         tr = run.step(row["iter"] - 1)
-        np.testing.assert_allclose(tr.lambdas, row["lambdas"], rtol=1e-8, atol=0)
+        np.testing.assert_allclose(tr.lambdas, row["lambdas"], rtol=1e-8, atol=1e-10)
         assert tr.sigma == pytest.approx(row["sigma"], rel=1e-12, abs=1e-14)
         if "e_tot" in row:
             assert abs(tr.e_tot - row["e_tot"]) <= 1e-8

@@ -205,3 +205,27 @@ def test_variable_cg_column_groups(ref, gpu_ctx_factory, k):
         np.testing.assert_allclose(res.x[c].cpu().numpy(), x, rtol=0, atol=1e-8 * np.abs(x).max())
     if k > 2:
         assert len(set(iters)) > 1  # the batch really ran with mixed active masks
+
+
+@pytest.mark.parametrize("s,K", [(12, 1), (12, 4), (40, 5), (40, 9), (70, 2), (34, 3)])
+def test_apply_flat_view_bit_exact(ref, gpu_ctx_factory, s, K):
+    """The dense-layout TMA apply (tma.cu k3f_kernel: x through the flat
+    2S-wide view, parity boxes, lattice masks) against the reference CSR
+    matvec: odd S with partial tiles, column counts that leave partial column
+    groups and odd lattice-row totals, variable and constant operators, plus
+    an 8-byte-misaligned column view (which stays on stream_kernel)."""
+    from paro_b200 import core
+
+    sp, ks = _ops(ref, s=s, lo=-7.0, hi=7.0)
+    ctx = gpu_ctx_factory(sp.s, sp.lo, sp.hi)
+    rng = np.random.default_rng(s * 100 + K)
+    X = rng.standard_normal((K + 1, sp.n))
+    Xd = _dev(X)
+    mass, kin, vext = (ks.op(w) for w in ("mass", "kinetic", "vext"))
+    a0 = kin.copy().add_scaled(vext)
+    for op in (mass, a0):
+        g = core.Operator.from_csr(ctx, *op.csr())
+        for view, rows in ((Xd[:K], range(K)), (Xd[1:], range(1, K + 1))):
+            Y = g.apply(view).cpu().numpy()
+            for i, c in enumerate(rows):
+                np.testing.assert_array_equal(Y[i], op.matvec(X[c]))
