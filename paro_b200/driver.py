@@ -234,6 +234,7 @@ class ParoRun:
         self.clamped = 0
         self._notspd_probe = []  # orbitals that met NotSpd in the last failing Step-3 attempt
         self.probe_hits = 0      # Step-3 attempts decided by the probe alone
+        self._fail_attempts = 0  # NotSpd attempts of the last Step 3 (the probe runs for that many)
         self._chunks = None      # step_host: (c0, c1, copy event) of the local Step-3 columns
         self._out = None         # step_host: (copy stream, host orbitals) filled after Step 4
         self._copy_stream = None
@@ -268,26 +269,44 @@ class ParoRun:
             # p'Ap <= 0, and each column's CG does not depend on the batch it
             # runs in, so the orbitals that failed the last failing attempt are
             # solved alone first; if one of them fails again the whole attempt
-            # has the same outcome without solving the other columns
+            # has the same outcome without solving the other columns, and if
+            # none does their solutions are final and the batch skips them
             # (the last attempt always runs in full: its error is the result)
-            if self._notspd_probe and attempt < 4 and self._probe(a, chunks, c0, c1, sigma, tol, attempt):
-                self.probe_hits += 1
-                sigma = 2.0 * sigma + 1.0
-                continue
-            first, final, iters = [], [], []
+            done = {}
+            # probing pays off for the attempts that failed last step; a probe
+            # that passes only moves its columns out of the batch (a lone column
+            # solves slower than inside the batch), so later attempts run in full
+            if self._notspd_probe and attempt < min(4, self._fail_attempts):
+                hit, done = self._probe(a, chunks, c0, c1, sigma, tol, attempt, local)
+                if hit:
+                    self.probe_hits += 1
+                    sigma = 2.0 * sigma + 1.0
+                    continue
+            n_loc = c1 - c0
+            first, final, iters = [OK] * n_loc, [OK] * n_loc, [0] * n_loc
+            for c, (f, g, i) in done.items():
+                first[c - c0], final[c - c0], iters[c - c0] = f, g, i
+            failed = False
             for k0, k1, ev in chunks:
                 if ev is not None and attempt == 0:
                     torch.cuda.current_stream(be.device).wait_event(ev)
-                if NOT_SPD in first:
-                    first += [OK] * (k1 - k0)
-                    final += [OK] * (k1 - k0)
-                    iters += [0] * (k1 - k0)
+                if failed:  # the first NotSpd ends the attempt like the batch abort (other columns report OK)
                     continue
-                f, g, i, _ = be.source_solve(a, self.orb[k0:k1], self.lambdas[k0:k1], sigma, tol, w.cg_max_iter,
-                                             local[k0 - c0:k1 - c0])
-                first += f
-                final += g
-                iters += i
+                # contiguous runs of this chunk's columns the probe has not solved
+                runs, start = [], None
+                for c in range(k0, k1 + 1):
+                    if c < k1 and c not in done:
+                        start = c if start is None else start
+                    elif start is not None:
+                        runs.append((start, c))
+                        start = None
+                for r0, r1 in runs:
+                    f, g, i, _ = be.source_solve(a, self.orb[r0:r1], self.lambdas[r0:r1], sigma, tol, w.cg_max_iter,
+                                                 local[r0 - c0:r1 - c0])
+                    first[r0 - c0:r1 - c0], final[r0 - c0:r1 - c0], iters[r0 - c0:r1 - c0] = f, g, i
+                    if NOT_SPD in f:
+                        failed = True
+                        break
             first = d.allgather_ints(first, counts, self._idev())
             final = d.allgather_ints(final, counts, self._idev())
             if NOT_SPD in first:
@@ -298,17 +317,21 @@ class ParoRun:
                 continue
             if code != OK:
                 raise N.ERRORS.get(code, N.Error)(f"source_solve_step: orbital {col} failed")
+            self._fail_attempts = attempt
             break
         all_iters = d.allgather_ints(iters, counts, self._idev())
         d.allgather_columns(local, counts, self.half)
         return sigma, all_iters
 
-    def _probe(self, a, chunks, c0, c1, sigma, tol, attempt) -> bool:
-        """Solve this rank's probe orbitals alone at sigma; True if any rank's
-        probe meets NotSpd (then the attempt fails like the full batch would)."""
+    def _probe(self, a, chunks, c0, c1, sigma, tol, attempt, local):
+        """Solve this rank's probe orbitals alone at sigma. Returns (hit, done):
+        hit if any rank's probe meets NotSpd (then the attempt fails like the
+        full batch would); otherwise done maps each local probe column to its
+        (first status, final status, iterations), its solution already in
+        `local` -- the same per-column result the batch would produce."""
         w, be, d = self.w, self.be, self.dist
         mine = [c for c in self._notspd_probe if c0 <= c < c1]
-        hit = 0
+        hit, done = 0, {}
         if mine:
             if attempt == 0:  # step_host: the probe columns' copies must have landed
                 for k0, k1, ev in chunks:
@@ -317,10 +340,14 @@ class ParoRun:
             idx = torch.tensor(mine, device=self.orb.device)
             u = self.orb.index_select(0, idx)
             out = torch.empty_like(u)
-            f, _, _, _ = be.source_solve(a, u, [self.lambdas[c] for c in mine], sigma, tol, w.cg_max_iter, out)
-            hit = 1 if NOT_SPD in f else 0
+            f, g, i, _ = be.source_solve(a, u, [self.lambdas[c] for c in mine], sigma, tol, w.cg_max_iter, out)
+            if NOT_SPD in f:
+                hit = 1
+            else:
+                local.index_copy_(0, idx - c0, out)
+                done = {c: (f[q], g[q], i[q]) for q, c in enumerate(mine)}
         hits = d.allgather_ints([hit], [1] * d.world, self._idev())
-        return any(h == 1 for h in hits)
+        return any(h == 1 for h in hits), done
 
     def _local(self, k):
         if self._half_local is None or self._half_local.shape[0] < k:

@@ -82,7 +82,8 @@ def test_shard_and_outcome_logic():
 def test_notspd_probe_keeps_the_trace():
     """source64 escalates sigma every outer iteration (the first Step-3
     attempt meets NotSpd); from the second iteration on the probe decides that
-    attempt from the previously failing orbital alone. The trace (lambdas,
+    attempt from the previously failing orbital alone, and a probe that
+    passes hands its solution to the batch. The trace (lambdas,
     sigma, CG iterations, orbitals) must equal the full-batch run's."""
     from paro_b200 import configs
     from paro_b200.driver import Dist, ParoRun
@@ -93,7 +94,7 @@ def test_notspd_probe_keeps_the_trace():
     def run(probe):
         r = ParoRun(w, PortBackend(w), Dist(), timers=False)
         if not probe:
-            r._probe = lambda *a, **k: False
+            r._probe = lambda *a, **k: (False, {})
         out = [r.step(i) for i in range(3)]
         return r, [(list(t.lambdas), t.sigma, list(t.cg_iterations)) for t in out]
 
