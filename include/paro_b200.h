@@ -150,6 +150,16 @@ int paro_rayleigh_ritz(paro_ctx* ctx, const paro_op* a_form, const paro_op* b, i
  * accepted: host array of k (input index of each kept vector) or NULL. */
 int paro_b_orthonormalize(paro_ctx* ctx, const paro_op* b, int k, const double* u, double drop_tol, double* q,
                           int* k_out, int* accepted);
+/* baseline_geneig (linalg.cpp:615-623; BaselineOptions linalg.hpp:136-140):
+ * the lowest `count` eigenpairs of (A, B) by shift-inverted block subspace
+ * iteration (baseline_subspace, linalg.cpp:531-611) on the device, without
+ * the reference's 50,000-dof cap. The reference's initial_guess (paro.cpp:
+ * 63-79) is this plus gram_defect. max_iter: outer iterations (400);
+ * seed: the random start. lambdas: host array of count (ascending);
+ * vectors: device, count columns, ld == n, fix_sign applied; iterations:
+ * host or NULL. PARO_ITERATION_LIMIT if it does not converge. */
+int paro_baseline_geneig(paro_ctx* ctx, const paro_op* a, const paro_op* b, int count, size_t max_iter,
+                         unsigned long long seed, double* lambdas, double* vectors, long long ld, int* iterations);
 /* dense_sym_geneig on one warp of the device, host row-major m x m in/out. */
 int paro_dense_sym_geneig(paro_ctx* ctx, int m, const double* a, const double* b, double* values, double* vectors);
 /* fix_sign (linalg.cpp:229-241) on k device columns. */

@@ -382,6 +382,24 @@ int ref_gram_defect(std::size_t k, std::size_t n, const double* u, void* b, doub
   return guarded([&] { *defect = gram_defect(unpack(k, n, u), static_cast<OpH*>(b)->op); });
 }
 
+// baseline_geneig (linalg.cpp:615-623): values[count], vectors column-major
+// [count][n] (vector j at vecs + j n).
+int ref_baseline_geneig(void* a, void* b, std::size_t count, std::size_t max_iter, std::uint64_t seed,
+                        double* vals, double* vecs) {
+  return guarded([&] {
+    BaselineOptions o;
+    o.max_iter = max_iter;
+    o.seed = seed;
+    const SparseOperator& A = static_cast<OpH*>(a)->op;
+    const EigenPairs e = baseline_geneig(A, static_cast<OpH*>(b)->op, count, o);
+    const std::size_t n = A.dimension();
+    for (std::size_t j = 0; j < count; ++j) {
+      vals[j] = e.values[j];
+      for (std::size_t i = 0; i < n; ++i) vecs[j * n + i] = e.vectors(i, j);
+    }
+  });
+}
+
 // Dense pencil (row-major A, B of size m x m); vectors row-major, columns = eigenvectors.
 int ref_dense_sym_geneig(std::size_t m, const double* a, const double* b, double* vals, double* vecs) {
   return guarded([&] {

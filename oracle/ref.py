@@ -113,6 +113,7 @@ def lib():
             "ref_b_orthonormalize": (C.c_int, [_SZ, _SZ, _DP, _P, _D, _DP, _SZP, _SZP, _SZP]),
             "ref_gram_defect": (C.c_int, [_SZ, _SZ, _DP, _P, _DP]),
             "ref_dense_sym_geneig": (C.c_int, [_SZ, _DP, _DP, _DP, _DP]),
+            "ref_baseline_geneig": (C.c_int, [_P, _P, _SZ, _SZ, C.c_uint64, _DP, _DP]),
             "ref_jacobi_eig": (C.c_int, [_SZ, _DP, _D, C.c_int, _DP, _DP]),
             "ref_fix_sign": (None, [_SZ, _DP]),
             "ref_density": (C.c_int, [_P, _SZ, _DP, _DP, _DP, _DP]),
@@ -314,6 +315,16 @@ def gram_defect(U, b: Op) -> float:
     d = C.c_double(0)
     _check(lib().ref_gram_defect(U.shape[0], U.shape[1], _dp(U), b.h, C.byref(d)))
     return d.value
+
+
+def baseline_geneig(a: "Op", b: "Op", count: int, max_iter: int = 400, seed: int = 7):
+    """baseline_geneig (linalg.cpp:615-623): dense (Eigen shim) up to 5,000 dofs,
+    else baseline_subspace; -> (values[count], vectors[count, n])."""
+    n = a.n
+    vals = np.zeros(count)
+    vecs = np.zeros((count, n))
+    _check(lib().ref_baseline_geneig(a.h, b.h, count, max_iter, seed, _dp(vals), _dp(vecs)))
+    return vals, vecs
 
 
 def dense_sym_geneig(A, B):

@@ -107,6 +107,7 @@ SIGNATURES = {
     "paro_hartree_solve": (_I, [_P, _P, _P, _P, _D, _P, _SZP]),
     "paro_rayleigh_ritz": (_I, [_P, _P, _P, _I, _P, _LL, _SZ, _D, _DP, _P, _LL, C.POINTER(_I), _DP]),
     "paro_dense_sym_geneig": (_I, [_P, _I, _DP, _DP, _DP, _DP]),
+    "paro_baseline_geneig": (_I, [_P, _P, _P, _I, _SZ, C.c_ulonglong, _DP, _P, _LL, C.POINTER(_I)]),
     "paro_b_orthonormalize": (_I, [_P, _P, _I, _P, _D, _P, C.POINTER(_I), C.POINTER(_I)]),
     "paro_fix_sign": (_I, [_P, _I, _P, _LL]),
     "paro_assemble_mass": (_I, [_P, C.POINTER(_P)]),

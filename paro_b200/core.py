@@ -336,6 +336,35 @@ def rayleigh_ritz(candidates: torch.Tensor, a_form: Operator, b: Operator, min_k
     return OrbitalSet(V[:kk], list(lam)[:kk], defect.value)
 
 
+def baseline_geneig(a: Operator, b: Operator, count: int, max_iter: int = 400, seed: int = 7):
+    """baseline_geneig (linalg.cpp:615-623): the lowest `count` eigenpairs of
+    (A, B) -> (lambdas, vectors [count, n], outer iterations). Device block
+    subspace iteration (baseline_subspace, linalg.cpp:531-611) with no dof cap;
+    raises IterationLimitError if it does not converge in max_iter."""
+    ctx = a.ctx
+    V = ctx.empty(count, ctx.n)
+    lam = (C.c_double * count)()
+    its = C.c_int(0)
+    ctx.check(N.lib().paro_baseline_geneig(ctx.h, a.h, b.h, int(count), int(max_iter), int(seed), lam, _ptr(V), ctx.n,
+                                           C.byref(its)))
+    return list(lam), V, its.value
+
+
+def initial_guess(a0: Operator, b: Operator, count: int, max_iter: int = 400, seed: int = 7) -> OrbitalSet:
+    """initial_guess (paro.cpp:63-79): baseline eigenpairs of the core operator
+    as the starting orbital set, with its B-Gram defect."""
+    if count <= 0:
+        raise N.InvalidArgumentError("initial_guess: count must be positive")
+    if count > a0.ctx.n:
+        raise N.InvalidArgumentError("initial_guess: more orbitals requested than coarse dofs")
+    lam, V, _ = baseline_geneig(a0, b, count, max_iter, seed)
+    G = torch.empty((count, a0.ctx.n), dtype=torch.float64, device=V.device)
+    b.apply(V, out=G)
+    gram = V @ G.T
+    defect = float((gram - torch.eye(count, dtype=gram.dtype, device=gram.device)).abs().tril().max())
+    return OrbitalSet(V, lam, defect)
+
+
 def b_orthonormalize(vectors: torch.Tensor, b: Operator, drop_tol: float) -> torch.Tensor:
     """b_orthonormalize (linalg.cpp:409-439) -> accepted B-orthonormal vectors [k, n]."""
     ctx = b.ctx

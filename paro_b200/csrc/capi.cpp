@@ -431,6 +431,13 @@ int paro_b_orthonormalize(paro_ctx* ctx, const paro_op* b, int k, const double* 
   return guarded(ctx, [&] { return b_orthonormalize(ctx->c, b->o, k, u, drop_tol, q, k_out, accepted); });
 }
 
+int paro_baseline_geneig(paro_ctx* ctx, const paro_op* a, const paro_op* b, int count, size_t max_iter,
+                         unsigned long long seed, double* lambdas, double* vectors, long long ld, int* iterations) {
+  return guarded(ctx, [&] {
+    return baseline_geneig(ctx->c, a->o, b->o, count, max_iter, seed, lambdas, vectors, ld, iterations);
+  });
+}
+
 int paro_dense_sym_geneig(paro_ctx* ctx, int m, const double* a, const double* b, double* vals, double* vecs) {
   return guarded(ctx, [&] { return dense_sym_geneig(ctx->c, m, a, b, vals, vecs); });
 }

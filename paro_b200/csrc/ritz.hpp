@@ -22,5 +22,8 @@ int b_orthonormalize(Ctx& ctx, const Op& B, int K, const double* U, double drop_
                      int* accepted);
 
 void fix_sign_columns(Ctx& ctx, double* V, long long ld, int k);
+// baseline_geneig (linalg.cpp:615-623) on the device (baseline.cu)
+int baseline_geneig(Ctx& ctx, const Op& A, const Op& B, int count, unsigned long long max_iter,
+                    unsigned long long seed, double* vals_host, double* V, long long ldv, int* iters_out);
 
 }  // namespace paro_b200

@@ -151,6 +151,12 @@ class GpuBackend:
     def source_solve(self, a, u, lambdas, sigma, tol, max_iter, out):
         return self.core.source_solve_columns(a, self.mass, u, lambdas, tol, max_iter, sigma, out)
 
+    def initial_guess(self, a, count, out):
+        """initial_guess (paro.cpp:63-79) on the device: baseline eigenpairs of a."""
+        og = self.core.initial_guess(a, self.mass, count)
+        out[:count].copy_(og.orbitals)
+        return out[:count], list(og.lambdas), og.gram_defect
+
     def ritz(self, cands, a, min_keep, drop_tol, out):
         r = self.core.rayleigh_ritz(cands, a, self.mass, min_keep, drop_tol, out=out)
         return r.orbitals, list(r.lambdas), r.gram_defect
@@ -214,21 +220,32 @@ class ParoRun:
         self.half = backend.empty(K, n)
         self.orb = backend.empty(K, n)
         self._half_local = None
-        g = guess if guess is not None else guess_vectors(w)
-        cands = backend.from_host(g) if not torch.is_tensor(g) else g
+        # guess="baseline": the reference drivers' own start, initial_guess =
+        # baseline eigenpairs of the core / linear operator (paro.cpp:278,
+        # 499-505); otherwise the generator's guess columns, Ritz-projected
+        baseline = isinstance(guess, str) and guess == "baseline"
+        if not baseline:
+            g = guess if guess is not None else guess_vectors(w)
+            cands = backend.from_host(g) if not torch.is_tensor(g) else g
+
+        def start(a):
+            if baseline:
+                return backend.initial_guess(a, K, self.orb)
+            return backend.ritz(cands, a, K, w.drop_tol, self.orb)
+
         if w.kind == "ks":
             self.occ = [2.0] * (w.n_electrons // 2)
             if len(self.occ) != w.n_orbitals:
                 raise N.InvalidArgumentError("kohn-sham: config.n_orbitals must equal N_e / 2")
             a0 = backend.core_hamiltonian()
             # initial guess: V_H = V_xc = 0 linearisation (paro.cpp:499-505)
-            orb, lam, _ = backend.ritz(cands, a0, K, w.drop_tol, self.orb)
+            orb, lam, _ = start(a0)
             self.rho_in = backend.density(orb, self.occ, out=backend.empty(n))
             self.rho_half = backend.empty(n)
             self.rho_out = backend.empty(n)
             self.vh = backend.empty(n)
         else:
-            orb, lam, _ = backend.ritz(cands, backend.form, K, w.drop_tol, self.orb)
+            orb, lam, _ = start(backend.form)
         self.k = orb.shape[0]
         self.lambdas = lam
         self.clamped = 0
