@@ -3,6 +3,7 @@
 // paro::gpu drop-ins and cross-checked with the CPU reference (paro::*) on a
 // 3-D Kohn-Sham system. Built by `make -C oracle dropin` next to the reference
 // objects; run on a GPU box by tests/test_gpu_dropin.py. Exit code 0 = pass.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <random>
@@ -88,6 +89,23 @@ int main() {
   const OrbitalSet back = gpu::rayleigh_ritz(ref_set.orbitals, a0, mass, space, 4, 1e-10);
   for (std::size_t j = 0; j < 4; ++j)
     CHECK(std::abs(back.lambdas[j] - ref_set.lambdas[j]) <= 1e-10 * std::abs(ref_set.lambdas[j]));
+
+  // baseline_geneig / initial_guess (linalg.cpp:615-623, paro.cpp:63-79):
+  // GPU subspace iteration vs the reference (Eigen-shim dense route at n = 729)
+  {
+    const EigenPairs rb = baseline_geneig(a0, mass, 3);
+    const EigenPairs gb = gpu::baseline_geneig(a0, mass, 3);
+    for (std::size_t j = 0; j < 3; ++j) {
+      CHECK(std::abs(gb.values[j] - rb.values[j]) <= 1e-9 * std::max(1.0, std::abs(rb.values[j])));
+      double d = 0.0, m = 0.0;
+      for (std::size_t i = 0; i < n; ++i) {
+        d = std::max(d, std::abs(gb.vectors(i, j) - rb.vectors(i, j)));
+        m = std::max(m, std::abs(rb.vectors(i, j)));
+      }
+      CHECK(d <= 1e-6 * m);
+    }
+    CHECK(throws<InvalidArgumentError>([&] { gpu::baseline_geneig(a0, mass, 0); }));
+  }
 
   // degenerate span raises (test_paro.cpp:196-200)
   std::vector<double> e0(n, 0.0);

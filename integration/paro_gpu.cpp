@@ -256,6 +256,26 @@ OrthonormalizeResult b_orthonormalize(const std::vector<std::vector<double>>& ve
   return r;
 }
 
+EigenPairs baseline_geneig(const SparseOperator& a, const SparseOperator& b, std::size_t count,
+                           const BaselineOptions& opts) {
+  const std::size_t n = a.dimension();
+  if (b.dimension() != n) throw InvalidArgumentError("baseline: pencil dimension mismatch");
+  if (count == 0 || count > n) throw InvalidArgumentError("baseline: bad eigenpair count");
+  need(n);
+  DevOp A(a), B(b);
+  DevVec dv(count * n);
+  EigenPairs out;
+  out.values.assign(count, 0.0);
+  int its = 0;
+  check(paro_baseline_geneig(g.ctx, A.op, B.op, static_cast<int>(count), opts.max_iter, opts.seed,
+                             out.values.data(), dv.p, static_cast<long long>(n), &its));
+  const std::vector<std::vector<double>> cols = unpack(dv, count, n);
+  out.vectors = DenseMatrix(n, count);
+  for (std::size_t j = 0; j < count; ++j)
+    for (std::size_t i = 0; i < n; ++i) out.vectors(i, j) = cols[j][i];
+  return out;
+}
+
 EigenPairs dense_sym_geneig(const DenseSymPencil& pencil) {
   const std::size_t m = pencil.a.rows();
   if (pencil.a.cols() != m || pencil.b.rows() != m || pencil.b.cols() != m)

@@ -44,6 +44,11 @@ OrthonormalizeResult b_orthonormalize(const std::vector<std::vector<double>>& ve
 /// dense_sym_geneig (linalg.cpp:341-393) on one warp of the device
 EigenPairs dense_sym_geneig(const DenseSymPencil& pencil);
 
+/// baseline_geneig (linalg.cpp:615-623): device block subspace iteration,
+/// no 50,000-dof cap (initial_guess, paro.cpp:63-79, calls this)
+EigenPairs baseline_geneig(const SparseOperator& a, const SparseOperator& b, std::size_t count,
+                           const BaselineOptions& opts = {});
+
 /// density_from_orbitals (model.cpp:192-223)
 Density density_from_orbitals(const std::vector<DiscreteFunction>& orbitals, const std::vector<double>& occupations);
 
