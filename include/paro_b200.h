@@ -68,6 +68,13 @@ int paro_ctx_set_ritz_mode(paro_ctx* ctx, int mode);
  * the constant 7-point stencil, else PCG (default). The tol-1e-11 PCG iterate
  * lies within ~1e-12 (relative) of the exact solution. */
 int paro_ctx_set_hartree_mode(paro_ctx* ctx, int mode);
+/* Host copy-out of the next rayleigh_ritz result (one shot): as soon as the
+ * new orbitals are final (after fix_sign, before the Gram certificate), their
+ * columns [c0, c1) are copied to pinned host memory `host` (column stride ldh)
+ * on `copy_stream`, which then holds the copy; the caller synchronises that
+ * stream. host == NULL clears a pending request. For callers that keep the
+ * orbitals in host memory, like the reference's std::vector interface. */
+int paro_ctx_set_ritz_copyout(paro_ctx* ctx, void* copy_stream, double* host, long long ldh, int c0, int c1);
 
 /* Device memory helpers for callers without their own allocator. */
 int paro_malloc(paro_ctx* ctx, size_t bytes, void** dev);

@@ -84,6 +84,7 @@ SIGNATURES = {
     "paro_ctx_synchronize": (_I, [_P]),
     "paro_ctx_set_ritz_mode": (_I, [_P, _I]),
     "paro_ctx_set_hartree_mode": (_I, [_P, _I]),
+    "paro_ctx_set_ritz_copyout": (_I, [_P, _P, _P, _LL, _I, _I]),
     "paro_ctx_stats": (_I, [_P, _DP, _I]),
     "paro_malloc": (_I, [_P, _SZ, C.POINTER(_P)]),
     "paro_free": (_I, [_P, _P]),

@@ -88,6 +88,13 @@ class Context:
     def synchronize(self):
         self.check(N.lib().paro_ctx_synchronize(self.h))
 
+    def set_ritz_copyout(self, stream: torch.cuda.Stream, host: torch.Tensor, c0: int, c1: int):
+        """One-shot: the next rayleigh_ritz copies its orbital columns [c0, c1)
+        to the pinned host tensor `host` [K, n] on `stream` as soon as they are
+        final (overlapping the Gram certificate); synchronise `stream` to use them."""
+        self.check(N.lib().paro_ctx_set_ritz_copyout(self.h, C.c_void_p(stream.cuda_stream), _ptr(host),
+                                                      host.stride(0), c0, c1))
+
     def set_hartree_mode(self, mode: str) -> "Context":
         """'cg': Jacobi-PCG to tol (reference algorithm); 'dst': exact DST-I solve when applicable."""
         self.check(N.lib().paro_ctx_set_hartree_mode(self.h, {"cg": 0, "dst": 1}[mode]))

@@ -366,7 +366,7 @@ struct RuleDev {
   int n = 0;
 };
 
-RuleDev upload_rule(DevBuf& buf, const Rule& r) {
+RuleDev upload_rule(Ctx& ctx, DevBuf& buf, const Rule& r) {
   const size_t m = r.points.size();
   std::vector<double> host(5 * m);
   for (size_t q = 0; q < m; ++q) {
@@ -374,7 +374,7 @@ RuleDev upload_rule(DevBuf& buf, const Rule& r) {
     host[4 * m + q] = r.weights[q];
   }
   double* d = buf.get<double>(host.size());
-  PARO_CUDA(cudaMemcpy(d, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice));
+  small_h2d(ctx, d, host.data(), sizeof(double) * host.size());
   return {d, d + 4 * m, static_cast<int>(m)};
 }
 
@@ -399,12 +399,12 @@ void assemble(Ctx& ctx, const AssembleSpec& spec, Op& out) {
   // stiffness and non-singular weighted masses use simplex_rule(3, 2);
   // the singular policy uses degree 5 everywhere and the 2-level subdivided
   // degree-5 rule near a nucleus (SingularQuadPolicy, fem.hpp:71-76)
-  const RuleDev main = upload_rule(rule_main, simplex_rule3(singular ? 5 : 2));
+  const RuleDev main = upload_rule(ctx, rule_main, simplex_rule3(singular ? 5 : 2));
   a.nq = main.n;
   a.qp = main.p;
   a.qw = main.w;
   if (singular) {
-    const RuleDev sub = upload_rule(rule_sub, subdivided_rule3(5, 2));
+    const RuleDev sub = upload_rule(ctx, rule_sub, subdivided_rule3(5, 2));
     a.nqs = sub.n;
     a.qps = sub.p;
     a.qws = sub.w;
@@ -414,7 +414,7 @@ void assemble(Ctx& ctx, const AssembleSpec& spec, Op& out) {
     const std::vector<double>& nuc = spec.nuclei;
     if (nuc.empty() || nuc.size() % 4 != 0) throw ParoError(kInvalidArgument, "external_potential: no nuclei");
     double* d = nuc_buf.get<double>(nuc.size() + 1);
-    PARO_CUDA(cudaMemcpy(d, nuc.data(), sizeof(double) * nuc.size(), cudaMemcpyHostToDevice));
+    small_h2d(ctx, d, nuc.data(), sizeof(double) * nuc.size());
     a.nuc = d;
     a.nnuc = static_cast<int>(nuc.size() / 4);
     a.eps2 = spec.eps * spec.eps;
@@ -451,9 +451,8 @@ void assemble(Ctx& ctx, const AssembleSpec& spec, Op& out) {
   PARO_CUDA(cudaGetLastError());
   int hflags = 0;
   unsigned long long hclamps = 0;
-  PARO_CUDA(cudaMemcpyAsync(&hflags, flags, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
-  if (clamps) PARO_CUDA(cudaMemcpyAsync(&hclamps, clamps, sizeof(hclamps), cudaMemcpyDeviceToHost, ctx.stream));
-  PARO_CUDA(cudaStreamSynchronize(ctx.stream));
+  small_d2h(ctx, &hflags, flags, sizeof(int));
+  if (clamps) small_d2h(ctx, &hclamps, clamps, sizeof(hclamps));
   if (spec.clamped) *spec.clamped = static_cast<long long>(hclamps);
   if (hflags & 1) throw ParoError(kError, "external potential evaluated at a nucleus");
   if (hflags & 2) throw ParoError(kError, "weighted mass: non-finite coefficient");
@@ -493,7 +492,7 @@ void add_scaled(Ctx& ctx, Op& a, const Op& b, double s) {
   }
   static thread_local DevBuf wbuf;
   double* dw = wbuf.get<double>(kSlots);
-  PARO_CUDA(cudaMemcpyAsync(dw, b.w, sizeof(double) * kSlots, cudaMemcpyHostToDevice, ctx.stream));
+  small_h2d(ctx, dw, b.w, sizeof(double) * kSlots);
   add_scaled_kernel<<<148 * 8, 256, 0, ctx.stream>>>(a.coef, b.var ? b.coef : nullptr, dw, s, n);
   ++ctx.launches;
   PARO_CUDA(cudaGetLastError());

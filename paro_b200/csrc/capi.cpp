@@ -89,6 +89,7 @@ int paro_ctx_destroy(paro_ctx* ctx) {
     b->release();
   if (ctx->c.cublas) cublasDestroy(ctx->c.cublas);
   if (ctx->c.pinned_count) cudaFreeHost(ctx->c.pinned_count);
+  paro_b200::xfer_release(ctx->c);
   delete ctx;
   return kOk;
 }
@@ -117,6 +118,18 @@ int paro_ctx_stats(paro_ctx* ctx, double out[8], int reset) {
 int paro_ctx_set_hartree_mode(paro_ctx* ctx, int mode) {
   return guarded(ctx, [&] {
     ctx->c.hartree_mode = mode;
+    return kOk;
+  });
+}
+
+int paro_ctx_set_ritz_copyout(paro_ctx* ctx, void* copy_stream, double* host, long long ldh, int c0, int c1) {
+  return guarded(ctx, [&] {
+    auto& co = ctx->c.ritz_copyout;
+    co.stream = static_cast<cudaStream_t>(copy_stream);
+    co.host = host;
+    co.ldh = ldh;
+    co.c0 = c0;
+    co.c1 = c1;
     return kOk;
   });
 }

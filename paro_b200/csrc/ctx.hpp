@@ -44,6 +44,9 @@ struct Op {
   bool owns = false;
 };
 
+constexpr size_t kXferSlot = 64 * 1024;  // small-transfer staging (xfer.cu)
+constexpr int kXferSlots = 32;
+
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -57,6 +60,13 @@ struct Ctx {
   DevBuf partials, cols, scale, invd, pbuf0, pbuf1, flag;
   DevBuf ws_a, ws_b, ws_c, ws_d, ws_e, ws_small, ws_small2, ws_small3;
   bool force_cgs2 = false;           // Step 4: skip the Cholesky-QR path
+  struct {                           // one-shot host copy-out of the next Ritz orbitals
+    cudaStream_t stream = nullptr;
+    double* host = nullptr;
+    long long ldh = 0;
+    int c0 = 0, c1 = 0;
+    cudaEvent_t ready = nullptr;
+  } ritz_copyout;
   int hartree_mode = 1;              // 0: Jacobi-PCG (reference algorithm), 1: DST-I when applicable
   int dst_S = 0;                     // grid of the cached DST-I tables
   DevBuf dst_tab;
@@ -66,6 +76,15 @@ struct Ctx {
   DevBuf shifted;                    // (A + sigma M) coefficients of the current shifted solve
   DevBuf coefp;                      // the same in the row-padded layout (TMA staging in the PCG passes)
   DevBuf csr_ws, csr_ws2, csr_io;    // general-CSR solver: interleaved work vectors, retry iterate, rhs/x
+  struct {                           // mapped pinned staging of the small transfers (xfer.cu)
+    unsigned char* rd = nullptr;
+    unsigned char* rd_dev = nullptr;
+    unsigned char* wr = nullptr;
+    unsigned char* wr_dev = nullptr;
+    cudaEvent_t ev[kXferSlots] = {};
+    bool used[kXferSlots] = {};
+    int next = 0;
+  } xfer;
   int* pinned_count = nullptr;       // mapped host memory for the active-column poll
   int* pinned_count_dev = nullptr;
 
@@ -82,5 +101,10 @@ struct Ctx {
     if (!grid_set) throw ParoError(kInvalidArgument, "paro_b200: grid not initialised");
   }
 };
+
+// small operands host<->device through mapped pinned memory (no copy engine, xfer.cu)
+void small_d2h(Ctx& ctx, void* host, const void* dev, size_t bytes);  // synchronises ctx.stream
+void small_h2d(Ctx& ctx, void* dev, const void* host, size_t bytes);  // stream-ordered on ctx.stream
+void xfer_release(Ctx& ctx);
 
 }  // namespace paro_b200

@@ -174,7 +174,7 @@ double cell_reduce(Ctx& ctx, int mode, const double* f, const double* g, int exc
     host[16 + q] = r4.weights[q];
   }
   double* drule = rule.get<double>(20);
-  PARO_CUDA(cudaMemcpyAsync(drule, host.data(), sizeof(double) * 20, cudaMemcpyHostToDevice, ctx.stream));
+  small_h2d(ctx, drule, host.data(), sizeof(double) * 20);
   const long long ncell = static_cast<long long>(gr.s) * gr.s * gr.s;
   const long long blocks = (ncell + kRedThreads - 1) / kRedThreads;
   double* partials = part.get<double>(blocks + 1);
@@ -184,8 +184,7 @@ double cell_reduce(Ctx& ctx, int mode, const double* f, const double* g, int exc
   ctx.launches += 2;
   PARO_CUDA(cudaGetLastError());
   double out = 0.0;
-  PARO_CUDA(cudaMemcpyAsync(&out, partials + blocks, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
-  PARO_CUDA(cudaStreamSynchronize(ctx.stream));
+  small_d2h(ctx, &out, partials + blocks, sizeof(double));
   host.clear();
   return out;
 }
@@ -200,7 +199,7 @@ double density(Ctx& ctx, int nocc, const double* U, long long ld, const double* 
   }
   static thread_local DevBuf occ;
   double* docc = occ.get<double>(nocc);
-  PARO_CUDA(cudaMemcpyAsync(docc, occ_host, sizeof(double) * nocc, cudaMemcpyHostToDevice, ctx.stream));
+  small_h2d(ctx, docc, occ_host, sizeof(double) * nocc);
   const long long n = ctx.grid.n;
   density_kernel<<<grid1d(n), 256, 0, ctx.stream>>>(nocc, U, ld, docc, n, rho);
   ++ctx.launches;

@@ -366,15 +366,13 @@ Small small_buffers(Ctx& ctx, int K) {
 
 int read_int(Ctx& ctx, const int* d) {
   int v = 0;
-  PARO_CUDA(cudaMemcpyAsync(&v, d, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
-  PARO_CUDA(cudaStreamSynchronize(ctx.stream));
+  small_d2h(ctx, &v, d, sizeof(int));
   return v;
 }
 
 double read_double(Ctx& ctx, const double* d) {
   double v = 0;
-  PARO_CUDA(cudaMemcpyAsync(&v, d, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
-  PARO_CUDA(cudaStreamSynchronize(ctx.stream));
+  small_d2h(ctx, &v, d, sizeof(double));
   return v;
 }
 
@@ -445,6 +443,10 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
   if (ld != n || ldv != n) throw ParoError(kInvalidArgument, "rayleigh_ritz: vectors must be contiguous (ld == n)");
   cudaStream_t st = ctx.stream;
   cublasSetStream(ctx.cublas, st);
+  struct ClearCopyout {  // the copy-out request is one-shot
+    Ctx& c;
+    ~ClearCopyout() { c.ritz_copyout.host = nullptr; }
+  } clear_copyout{ctx};
   double* W = ctx.ws_b.get<double>(static_cast<size_t>(K) * n);
   double* Q1 = ctx.ws_c.get<double>(static_cast<size_t>(K) * n);
   Small s = small_buffers(ctx, K);
@@ -466,6 +468,17 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
     // lift, sign convention, certificate (paro.cpp:157-174)
     rotate(ctx, kk, kk, Qb, n, s.Y, kk, V, ldv);
     fix_sign_columns(ctx, V, ldv, kk);
+    // final orbitals: a pending host copy-out starts now, overlapping the certificate
+    auto& co = ctx.ritz_copyout;
+    if (co.host != nullptr) {
+      if (co.ready == nullptr) PARO_CUDA(cudaEventCreateWithFlags(&co.ready, cudaEventDisableTiming));
+      PARO_CUDA(cudaEventRecord(co.ready, st));
+      PARO_CUDA(cudaStreamWaitEvent(co.stream, co.ready, 0));
+      const int c1 = std::min(co.c1, kk);
+      for (int c = co.c0; c < c1; ++c)
+        PARO_CUDA(cudaMemcpyAsync(co.host + static_cast<long long>(c) * co.ldh, V + static_cast<long long>(c) * ldv,
+                                  sizeof(double) * n, cudaMemcpyDeviceToHost, co.stream));
+    }
     apply_op(ctx, B, nullptr, 0.0, kk, V, ldv, W, n);
     gram(ctx, kk, kk, V, ldv, W, n, s.G3);
     defect_kernel<<<1, 256, 0, st>>>(kk, s.G3, s.defect);
@@ -533,8 +546,7 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
     d = finish(Q1, k);
   }
   if (info) info->k = k;
-  PARO_CUDA(cudaMemcpyAsync(lambdas, s.vals, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
-  PARO_CUDA(cudaStreamSynchronize(st));
+  small_d2h(ctx, lambdas, s.vals, sizeof(double) * k);
   *k_out = k;
   *defect = d;
   if (d > 1e-8) {

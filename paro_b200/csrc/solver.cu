@@ -271,8 +271,8 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
   for (double* v : {r, p0, p1, xi}) zero_margins(v, K, np);
   int* flag = ctx.flag.get<int>(3 + K);  // 3 flags + the copy-out column list
 
-  PARO_CUDA(cudaMemcpyAsync(dcols, cols.data(), sizeof(CgColumn) * K, cudaMemcpyHostToDevice, st));
-  if (scale_host) PARO_CUDA(cudaMemcpyAsync(dscale, scale_host, sizeof(double) * K, cudaMemcpyHostToDevice, st));
+  small_h2d(ctx, dcols, cols.data(), sizeof(CgColumn) * K);
+  if (scale_host) small_h2d(ctx, dscale, scale_host, sizeof(double) * K);
 
   // Jacobi preconditioner and the SPD diagonal check (linalg.cpp:164-173)
   set_flag_kernel<<<1, 1, 0, st>>>(flag, 0);
@@ -449,7 +449,7 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
   if (graph) PARO_CUDA(cudaGraphDestroy(graph));
   trace.mark("iterations");
   std::vector<CgColumn> before = cols;
-  PARO_CUDA(cudaMemcpy(cols.data(), dcols, sizeof(CgColumn) * K, cudaMemcpyDeviceToHost));
+  small_d2h(ctx, cols.data(), dcols, sizeof(CgColumn) * K);
   // an aborted batch (NotSpd: the sigma policy restarts the step) has no result to return
   bool aborted = false;
   for (int c = 0; c < K; ++c) aborted |= abort_on_not_spd && cols[c].status == kNotSpd;
@@ -466,7 +466,7 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
           PARO_CUDA(cudaMemcpyAsync(x + c * ld, xi + c * ldi, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
       } else {  // row-padded -> dense (+ a pending deferred update), every column in one launch
         int* dlist = flag + 3;
-        PARO_CUDA(cudaMemcpyAsync(dlist, out_cols.data(), sizeof(int) * out_cols.size(), cudaMemcpyHostToDevice, st));
+        small_h2d(ctx, dlist, out_cols.data(), sizeof(int) * out_cols.size());
         unpad_cols_kernel<<<dim3(148 * 2, static_cast<unsigned>(out_cols.size())), 256, 0, st>>>(
             xi, ldi, x, ld, dlist, g.S, P, dcols, p1, deferred ? 1 : 0);
         PARO_CUDA(cudaGetLastError());

@@ -157,6 +157,10 @@ class GpuBackend:
         out[:count].copy_(og.orbitals)
         return out[:count], list(og.lambdas), og.gram_defect
 
+    def ritz_copyout(self, stream, host, c0, c1):
+        """One-shot host copy-out of the next ritz's orbital columns [c0, c1) (step_host)."""
+        self.ctx.set_ritz_copyout(stream, host, c0, c1)
+
     def ritz(self, cands, a, min_keep, drop_tol, out):
         r = self.core.rayleigh_ritz(cands, a, self.mass, min_keep, drop_tol, out=out)
         return r.orbitals, list(r.lambdas), r.gram_defect
@@ -354,14 +358,16 @@ class ParoRun:
                 for k0, k1, ev in chunks:
                     if ev is not None and any(k0 <= c < k1 for c in mine):
                         torch.cuda.current_stream(be.device).wait_event(ev)
-            idx = torch.tensor(mine, device=self.orb.device)
-            u = self.orb.index_select(0, idx)
+            # device-side gather (a host->device index upload would queue on the
+            # copy engine behind step_host's orbital transfer)
+            u = torch.stack([self.orb[c] for c in mine])
             out = torch.empty_like(u)
             f, g, i, _ = be.source_solve(a, u, [self.lambdas[c] for c in mine], sigma, tol, w.cg_max_iter, out)
             if NOT_SPD in f:
                 hit = 1
             else:
-                local.index_copy_(0, idx - c0, out)
+                for q, c in enumerate(mine):
+                    local[c - c0].copy_(out[q])
                 done = {c: (f[q], g[q], i[q]) for q, c in enumerate(mine)}
         hits = d.allgather_ints([hit], [1] * d.world, self._idev())
         return any(h == 1 for h in hits), done
@@ -382,6 +388,18 @@ class ParoRun:
         if self.w.kind == "ks":
             return self._ks_step(it)
         return self._linear_step(it)
+
+    def _arm_copy_out(self):
+        """step_host: the library copies this rank's block of the new orbitals
+        to the host on the side stream as soon as Step 4 has them final
+        (before its Gram certificate)."""
+        if self._out is None or not hasattr(self.be, "ritz_copyout"):
+            return False
+        cs, h_orb = self._out
+        o0, o1, _ = self.dist.shard(self.k)
+        self._mark("d2h_armed", cs)
+        self.be.ritz_copyout(cs, h_orb, o0, o1)
+        return True
 
     def _copy_out(self, orb):
         """step_host: this rank's block of the new orbitals to the host (side stream)."""
@@ -418,11 +436,15 @@ class ParoRun:
                 main.wait_event(cs.record_event())
             # the first chunk is small (a multiple of the 4-column groups) so
             # the Step-3 solves start early; the rest arrive while it runs
-            first = min(c1 - c0, max(4, ((c1 - c0) // 5 + 3) // 4 * 4)) if chunks == 2 else 0
-            if first:
+            kl = c1 - c0
+            if chunks == 2:
+                first = min(kl, max(4, (kl // 5 + 3) // 4 * 4))
                 bounds = [c0, c0 + first, c1]
+            elif chunks == 3:  # 8 / 24 / rest of 76: each chunk's solve covers the next one's copy
+                first = min(kl, max(4, (kl // 10 + 3) // 4 * 4))
+                bounds = [c0, c0 + first, min(c1, c0 + 4 * first), c1]
             else:
-                bounds = [c0 + ((c1 - c0) * i) // chunks for i in range(chunks + 1)]
+                bounds = [c0 + (kl * i) // chunks for i in range(chunks + 1)]
             ranges = [(bounds[i], bounds[i + 1]) for i in range(chunks) if bounds[i + 1] > bounds[i]]
             evs = []
             self._mark("h2d_start", cs)
@@ -466,10 +488,13 @@ class ParoRun:
         vh_half = be.hartree(rho_half, out=self.vh)
         a_half, cl = be.ks_form(rho_half, vh_half, "half")
         self.clamped += cl
+        armed = self._arm_copy_out()
         orb, lam, defect = be.ritz(half, a_half, N_, w.drop_tol, self.orb)
         self._mark("ritz_end")
-        if self._out is not None:  # step_host: the orbitals leave while the density work runs
+        if self._out is not None and not armed:  # step_host: the orbitals leave while the density work runs
             self._copy_out(orb)
+        if self._out is not None and orb.shape[0] != self.k:
+            self._copy_out(orb)  # a dropped candidate changed the shard: copy the final block explicitly
         self._sync()
         t_project = time.perf_counter() - tp
         self.k, self.lambdas = orb.shape[0], lam
@@ -494,8 +519,9 @@ class ParoRun:
         self._sync()
         t_source = time.perf_counter() - t0
         tp = time.perf_counter()
+        armed = self._arm_copy_out()
         orb, lam, defect = be.ritz(self.half[: self.k], be.form, w.n_orbitals, w.drop_tol, self.orb)
-        if self._out is not None:
+        if self._out is not None and (not armed or orb.shape[0] != self.k):
             self._copy_out(orb)
         self._sync()
         self.k, self.lambdas = orb.shape[0], lam
