@@ -11,6 +11,7 @@
 // tall-skinny Grams / rotations as FP64 DGEMMs and the K x K work in
 // single-warp kernels (dense.cu).
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -157,6 +158,116 @@ __global__ void __launch_bounds__(kGThreads) gram_sym_kernel(const double* __res
     }
 }
 
+// The same split-K upper-triangle Gram with the tile sets fixed at compile
+// time (nb = number of 8-column blocks): every DMMA, fragment load and
+// accumulator is unconditional, which removes the per-tile predicates that
+// cost ~16 instructions per DMMA in the generic kernel. Same staging, tile
+// assignment, k order and partial layout, so the partials are identical.
+template <int NB, int RLO, int RHI, int CLO, int CHI>
+__device__ __forceinline__ void gram_tiles(double (*xs)[kGR][kGRow], double (*ys)[kGR][kGRow], int lane, int st,
+                                           double (&acc)[kGPairsMax][2]) {
+  const int fr = lane & 3, fc = lane >> 2;
+#pragma unroll 2
+  for (int k0 = 0; k0 < kGR; k0 += 4) {
+    const int row = k0 + fr;
+    const int sw = gswz(row);
+    double a[RHI - RLO > 0 ? RHI - RLO : 1], b[CHI - CLO > 0 ? CHI - CLO : 1];
+#pragma unroll
+    for (int i = 0; i < RHI - RLO; ++i) a[i] = xs[st][row][((RLO + i) * kGB + fc) ^ sw];
+#pragma unroll
+    for (int j = 0; j < CHI - CLO; ++j) b[j] = ys[st][row][((CLO + j) * kGB + fc) ^ sw];
+    int t = 0;
+#pragma unroll
+    for (int i = 0; i < RHI - RLO; ++i)
+#pragma unroll
+      for (int j = 0; j < CHI - CLO; ++j)
+        if (CLO + j >= RLO + i) {
+          dmma(acc[t][0], acc[t][1], a[i], b[j]);
+          ++t;
+        }
+  }
+}
+
+template <int NB, int RLO, int RHI, int CLO, int CHI>
+__device__ __forceinline__ void gram_store(double* part, int lane, const double (&acc)[kGPairsMax][2]) {
+  const int fr = lane & 3, fc = lane >> 2;
+  int t = 0;
+#pragma unroll
+  for (int i = 0; i < RHI - RLO; ++i)
+#pragma unroll
+    for (int j = 0; j < CHI - CLO; ++j)
+      if (CLO + j >= RLO + i) {
+        double* o = part + (static_cast<long long>(blockIdx.x) * kGPairsMax + gpair(RLO + i, CLO + j, NB)) * (kGB * kGB);
+        o[fc * kGB + 2 * fr] = acc[t][0];
+        o[fc * kGB + 2 * fr + 1] = acc[t][1];
+        ++t;
+      }
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kGThreads) gram_sym_fixed_kernel(const double* __restrict__ X, long long ldx,
+                                                                   const double* __restrict__ Y, long long ldy,
+                                                                   int k, long long n, long long chunk,
+                                                                   double* __restrict__ part) {
+  extern __shared__ __align__(16) double gsm[];
+  auto xs = reinterpret_cast<double(*)[kGR][kGRow]>(gsm);
+  auto ys = reinterpret_cast<double(*)[kGR][kGRow]>(gsm + 2 * kGR * kGRow);
+  const long long r0 = blockIdx.x * chunk;
+  const long long r1 = min(n, r0 + chunk);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int H = (NB + 1) / 2, M = (NB - H) / 2;
+  double acc[kGPairsMax][2];  // only the first (warp's tile count) entries are live
+#pragma unroll
+  for (int t = 0; t < kGPairsMax; ++t) acc[t][0] = acc[t][1] = 0.0;
+
+  constexpr int kCStep = kGThreads / kGR;
+  const int lrow = threadIdx.x % kGR, lcol = threadIdx.x / kGR;
+  const int lsw = gswz(lrow);
+  const double* xb = X + lcol * ldx + lrow;
+  const double* yb = Y + lcol * ldy + lrow;
+  auto issue = [&](int st, long long rb) {
+    const bool rin = rb + lrow < r1;
+    const double* px = xb + rb;
+    const double* py = yb + rb;
+#pragma unroll
+    for (int q = 0; q < (NB * kGB + kCStep - 1) / kCStep; ++q) {
+      const int col = lcol + q * kCStep;
+      const bool v = rin && col < k;
+      const int sc = col ^ lsw;
+      gcp8(&xs[st][lrow][sc], v ? px : X, v);
+      gcp8(&ys[st][lrow][sc], v ? py : Y, v);
+      px += kCStep * ldx;
+      py += kCStep * ldy;
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+
+  int st = 0;
+  issue(0, r0);
+  for (long long rb = r0; rb < r1; rb += kGR, st ^= 1) {
+    if (rb + kGR < r1) {
+      issue(st ^ 1, rb + kGR);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    switch (warp) {
+      case 0: gram_tiles<NB, 0, H, 0, H>(xs, ys, lane, st, acc); break;
+      case 1: gram_tiles<NB, 0, H, H, H + M>(xs, ys, lane, st, acc); break;
+      case 2: gram_tiles<NB, 0, H, H + M, NB>(xs, ys, lane, st, acc); break;
+      default: gram_tiles<NB, H, NB, H, NB>(xs, ys, lane, st, acc); break;
+    }
+    __syncthreads();
+  }
+  switch (warp) {
+    case 0: gram_store<NB, 0, H, 0, H>(part, lane, acc); break;
+    case 1: gram_store<NB, 0, H, H, H + M>(part, lane, acc); break;
+    case 2: gram_store<NB, 0, H, H + M, NB>(part, lane, acc); break;
+    default: gram_store<NB, H, NB, H, NB>(part, lane, acc); break;
+  }
+}
+
 // G[row, col] (column-major, k x k) from the partials of tile t, in a fixed
 // order over chunks; the upper triangle is mirrored.
 __global__ void gram_sym_reduce_kernel(const double* __restrict__ part, int P, int k, double* __restrict__ G) {
@@ -193,7 +304,23 @@ void gram(Ctx& ctx, int k1, int k2, const double* X, long long ldx, const double
                                      static_cast<int>(smem)));
       configured = true;
     }
-    gram_sym_kernel<<<Pn, kGThreads, smem, ctx.stream>>>(X, ldx, Y, ldy, k1, n, chunk, part);
+    const int nbk = (k1 + kGB - 1) / kGB;
+    static const bool generic = [] {
+      const char* e = std::getenv("PARO_GRAM_GENERIC");  // experiment knob: the predicated kernel only
+      return e && e[0] == '1';
+    }();
+    if (!generic && (nbk == 10 || nbk == 8)) {
+      auto kern = nbk == 10 ? gram_sym_fixed_kernel<10> : gram_sym_fixed_kernel<8>;
+      static bool conf_fixed[2] = {false, false};
+      bool& cf = conf_fixed[nbk == 10 ? 1 : 0];
+      if (!cf) {
+        PARO_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        cf = true;
+      }
+      kern<<<Pn, kGThreads, smem, ctx.stream>>>(X, ldx, Y, ldy, k1, n, chunk, part);
+    } else {
+      gram_sym_kernel<<<Pn, kGThreads, smem, ctx.stream>>>(X, ldx, Y, ldy, k1, n, chunk, part);
+    }
     const int nb = (k1 + kGB - 1) / kGB;
     gram_sym_reduce_kernel<<<nb * (nb + 1) / 2, kGB * kGB, 0, ctx.stream>>>(part, Pn, k1, G);
     PARO_CUDA(cudaGetLastError());
