@@ -257,6 +257,7 @@ class ParoRun:
         self.probe_hits = 0      # Step-3 attempts decided by the probe alone
         self._fail_attempts = 0  # NotSpd attempts of the last Step 3 (the probe runs for that many)
         self._chunks = None      # step_host: (c0, c1, copy event) of the local Step-3 columns
+        self._waited = set()     # step_host: ids of the chunk events the compute stream already waits on
         self._out = None         # step_host: (copy stream, host orbitals) filled after Step 4
         self._copy_stream = None
         self.timeline = None     # profiling: list of (label, CUDA event) marks, or None
@@ -309,8 +310,7 @@ class ParoRun:
                 first[c - c0], final[c - c0], iters[c - c0] = f, g, i
             failed = False
             for k0, k1, ev in chunks:
-                if ev is not None and attempt == 0:
-                    torch.cuda.current_stream(be.device).wait_event(ev)
+                self._wait_chunk(ev)
                 if failed:  # the first NotSpd ends the attempt like the batch abort (other columns report OK)
                     continue
                 # contiguous runs of this chunk's columns the probe has not solved
@@ -340,6 +340,8 @@ class ParoRun:
                 raise N.ERRORS.get(code, N.Error)(f"source_solve_step: orbital {col} failed")
             self._fail_attempts = attempt
             break
+        # every chunk has landed before Step 4 writes the new orbitals into self.orb
+        self._wait_chunks()
         all_iters = d.allgather_ints(iters, counts, self._idev())
         d.allgather_columns(local, counts, self.half)
         return sigma, all_iters
@@ -354,10 +356,9 @@ class ParoRun:
         mine = [c for c in self._notspd_probe if c0 <= c < c1]
         hit, done = 0, {}
         if mine:
-            if attempt == 0:  # step_host: the probe columns' copies must have landed
-                for k0, k1, ev in chunks:
-                    if ev is not None and any(k0 <= c < k1 for c in mine):
-                        torch.cuda.current_stream(be.device).wait_event(ev)
+            for k0, k1, ev in chunks:  # step_host: the probe columns' copies must have landed
+                if any(k0 <= c < k1 for c in mine):
+                    self._wait_chunk(ev)
             # device-side gather (a host->device index upload would queue on the
             # copy engine behind step_host's orbital transfer)
             u = torch.stack([self.orb[c] for c in mine])
@@ -371,6 +372,17 @@ class ParoRun:
                 done = {c: (f[q], g[q], i[q]) for q, c in enumerate(mine)}
         hits = d.allgather_ints([hit], [1] * d.world, self._idev())
         return any(h == 1 for h in hits), done
+
+    def _wait_chunk(self, ev):
+        """step_host: make the compute stream wait for one column chunk's host
+        copy (once per step, whichever attempt or probe first needs it)."""
+        if ev is not None and id(ev) not in self._waited:
+            torch.cuda.current_stream(self.be.device).wait_event(ev)
+            self._waited.add(id(ev))
+
+    def _wait_chunks(self):
+        for _, _, ev in self._chunks or ():
+            self._wait_chunk(ev)
 
     def _local(self, k):
         if self._half_local is None or self._half_local.shape[0] < k:
@@ -453,6 +465,7 @@ class ParoRun:
                 evs.append(cs.record_event())
                 self._mark(f"h2d_cols_{k0}_{k1}", cs)
         self._chunks = [(k0, k1, ev) for (k0, k1), ev in zip(ranges, evs)]
+        self._waited = set()
         self._out = (cs, h_orb)
         try:
             tr = self.step(it)
@@ -472,6 +485,8 @@ class ParoRun:
         vh_in = be.hartree(self.rho_in, out=self.vh)
         # Step 2 on a fixed mesh: the estimator only feeds eta_total (paro.cpp:521-538)
         t2 = time.perf_counter()
+        if self.estimate:
+            self._wait_chunks()  # step_host: the estimator reads every orbital
         eta = be.estimate(self.orb[:N_], self.lambdas[:N_], self.rho_in, vh_in) if self.estimate else None
         t_meshgen = time.perf_counter() - t2
         a_in, cl = be.ks_form(self.rho_in, vh_in, "in")
@@ -513,6 +528,8 @@ class ParoRun:
         w, be = self.w, self.be
         t0 = time.perf_counter()
         N_ = w.n_orbitals
+        if self.estimate:
+            self._wait_chunks()
         eta = be.estimate(self.orb[:N_], self.lambdas[:N_]) if self.estimate else None  # paro.cpp:306-315
         t_meshgen = time.perf_counter() - t0
         sigma, iters = self.step3(be.form, it)
