@@ -172,6 +172,47 @@ int paro_dense_sym_geneig(paro_ctx* ctx, int m, const double* a, const double* b
 /* fix_sign (linalg.cpp:229-241) on k device columns. */
 int paro_fix_sign(paro_ctx* ctx, int k, double* v, long long ld);
 
+/* ---- Step 4 (rayleigh_ritz, paro.cpp:121-177) as building blocks on row
+ * ranges [r0, r1) of column blocks: what a Step 4 sharded over row slabs
+ * combines across ranks (Grams summed, fix_sign pieces by max / min / max).
+ * Matrices g, c, y are device buffers, column-major. */
+/* y = A x on the rows of planes [z0, z1); x must be valid on planes z0-1 .. z1 */
+int paro_op_apply_planes(paro_ctx* ctx, const paro_op* a, int k, const double* x, long long ld, double* y, int z0,
+                         int z1);
+/* g (k x k) = x^T y over rows [r0, r1) for a symmetric product (y = B x, A x) */
+int paro_gram_sym(paro_ctx* ctx, int k, const double* x, long long ldx, const double* y, long long ldy, long long r0,
+                  long long r1, double* g);
+/* g (k1 x k2) = x^T y over rows [r0, r1), k1 <= 80, k2 <= 16 */
+int paro_gram_rect(paro_ctx* ctx, int k1, const double* x, long long ldx, int k2, const double* y, long long ldy,
+                   long long r0, long long r1, double* g);
+/* z = x c over rows [r0, r1), k1, k2 <= 80; mode 1: z -= x c, 4: z += x c,
+ * 2: c is zero below its diagonal shifted by k1 - k2 (skips those products) */
+int paro_rotate(paro_ctx* ctx, int k1, const double* x, long long ldx, const double* c, int ldc, int k2, double* z,
+                long long ldz, long long r0, long long r1, int mode);
+/* ordered Cholesky with the MGS drop rule of the raw Gram g (K x K) -> basis change c1 (K x k_out) */
+int paro_ritz_ortho(paro_ctx* ctx, int K, const double* g, double drop_tol, double* c1, int* k_out,
+                    double* min_ratio);
+/* second Cholesky-QR pass: g2 -> c2 = L2^{-T}, bt = L2^{-1} g2 L2^{-T}; PARO_PENCIL if not SPD */
+int paro_ritz_second_pass(paro_ctx* ctx, int k, const double* g2, double* c2, double* bt);
+/* the k x k pencil: gb == NULL: in the Q basis from (ga, c2, bt); else directly
+ * (ga, gb). Eigenvalues to host `vals`, lift coefficients to device y (k x k). */
+int paro_ritz_pencil(paro_ctx* ctx, int k, const double* ga, const double* c2, const double* bt, const double* gb,
+                     double* vals, double* y);
+/* gram_defect (paro.cpp:50-61) of an assembled Gram g: max_{j<=i} |g_ij - d_ij| */
+int paro_gram_defect(paro_ctx* ctx, int k, const double* g, double* out);
+/* fix_sign (linalg.cpp:229-241) pieces: init (amax = 0, first = LLONG_MAX),
+ * colmax (max |v| per column, combine by max), first_above (first global row
+ * with |v| > 1e-12 amax, combine by min), sign_flags (1 where this range holds
+ * that row and it is negative, combine by max), negate_columns. */
+int paro_sign_init(paro_ctx* ctx, int k, double* amax, long long* first);
+int paro_colmax(paro_ctx* ctx, int k, const double* v, long long ld, long long r0, long long r1, double* amax);
+int paro_first_above(paro_ctx* ctx, int k, const double* v, long long ld, long long r0, long long r1,
+                     const double* amax, long long* first);
+int paro_sign_flags(paro_ctx* ctx, int k, const double* v, long long ld, long long r0, long long r1,
+                    const double* amax, const long long* first, double* flip);
+int paro_negate_columns(paro_ctx* ctx, int k, double* v, long long ld, long long r0, long long r1,
+                        const double* flip);
+
 /* ------------------------------------------------- operator assembly ----- */
 /* On the device, element by element in the reference's element order, so the
  * coefficients equal the reference CSR values. Uniform results become
@@ -202,6 +243,12 @@ int paro_ks_form(paro_ctx* ctx, const paro_op* kinetic, const paro_op* vext_mass
 int paro_density(paro_ctx* ctx, int nocc, const double* u, long long ld, const double* occ, double* rho,
                  double* raw_integral);
 /* mix_density (model.cpp:225-236) */
+/* density_from_orbitals in two halves (row-slab sharding): the nodal sum
+ * sum_i occ_i u_i^2 on rows [r0, r1) of rho, and the normalisation of a
+ * complete nodal density to sum occ (model.cpp:215-221) */
+int paro_density_rows(paro_ctx* ctx, int nocc, const double* u, long long ld, const double* occ, long long r0,
+                      long long r1, double* rho);
+int paro_density_normalize(paro_ctx* ctx, double total_occ, double* rho, double* raw_integral);
 int paro_mix_density(paro_ctx* ctx, const double* rho_in, const double* rho_out, double alpha, double* out);
 /* integrate / norm_l2 (fem.cpp:419-448), integrate_product (model.cpp:306-327); results: host */
 int paro_integrate(paro_ctx* ctx, const double* f, double* out);

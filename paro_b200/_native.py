@@ -111,6 +111,19 @@ SIGNATURES = {
     "paro_baseline_geneig": (_I, [_P, _P, _P, _I, _SZ, C.c_ulonglong, _DP, _P, _LL, C.POINTER(_I)]),
     "paro_b_orthonormalize": (_I, [_P, _P, _I, _P, _D, _P, C.POINTER(_I), C.POINTER(_I)]),
     "paro_fix_sign": (_I, [_P, _I, _P, _LL]),
+    "paro_op_apply_planes": (_I, [_P, _P, _I, _P, _LL, _P, _I, _I]),
+    "paro_gram_sym": (_I, [_P, _I, _P, _LL, _P, _LL, _LL, _LL, _P]),
+    "paro_gram_rect": (_I, [_P, _I, _P, _LL, _I, _P, _LL, _LL, _LL, _P]),
+    "paro_rotate": (_I, [_P, _I, _P, _LL, _P, _I, _I, _P, _LL, _LL, _LL, _I]),
+    "paro_ritz_ortho": (_I, [_P, _I, _P, _D, _P, C.POINTER(_I), _DP]),
+    "paro_ritz_second_pass": (_I, [_P, _I, _P, _P, _P]),
+    "paro_ritz_pencil": (_I, [_P, _I, _P, _P, _P, _P, _DP, _P]),
+    "paro_gram_defect": (_I, [_P, _I, _P, _DP]),
+    "paro_sign_init": (_I, [_P, _I, _P, _P]),
+    "paro_colmax": (_I, [_P, _I, _P, _LL, _LL, _LL, _P]),
+    "paro_first_above": (_I, [_P, _I, _P, _LL, _LL, _LL, _P, _P]),
+    "paro_sign_flags": (_I, [_P, _I, _P, _LL, _LL, _LL, _P, _P, _P]),
+    "paro_negate_columns": (_I, [_P, _I, _P, _LL, _LL, _LL, _P]),
     "paro_assemble_mass": (_I, [_P, C.POINTER(_P)]),
     "paro_assemble_stiffness": (_I, [_P, _D, C.POINTER(_P)]),
     "paro_assemble_vext": (_I, [_P, _I, _DP, _DP, _D, C.POINTER(_P)]),
@@ -125,6 +138,8 @@ SIGNATURES = {
     "paro_ks_form": (_I, [_P, _P, _P, _P, _P, _I, _P, C.POINTER(_LL)]),
     "paro_density": (_I, [_P, _I, _P, _LL, _DP, _P, _DP]),
     "paro_mix_density": (_I, [_P, _P, _P, _D, _P]),
+    "paro_density_rows": (_I, [_P, _I, _P, _LL, _DP, _LL, _LL, _P]),
+    "paro_density_normalize": (_I, [_P, _D, _P, _DP]),
     "paro_integrate": (_I, [_P, _P, _DP]),
     "paro_norm_l2": (_I, [_P, _P, _DP]),
     "paro_integrate_product": (_I, [_P, _P, _P, _DP]),

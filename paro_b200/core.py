@@ -612,3 +612,115 @@ def csr_source_solve_step(a: CsrOperator, b: CsrOperator, u_prev: torch.Tensor, 
         report.update(iterations=list(it), residual=list(res))
     ctx.check(st)
     return y
+
+
+# ----------------------------------------------------------------------------
+# Step 4 building blocks on row ranges (row-slab sharded rayleigh_ritz,
+# paro_b200/step4.py). Vectors are [k, n] device tensors with column stride
+# n; small matrices are flat device tensors in column-major order.
+
+def _ld(X: torch.Tensor, n: int) -> int:
+    return X.stride(0) if X.dim() == 2 and X.shape[0] > 1 else n
+
+
+def apply_planes(op: Operator, X: torch.Tensor, k: int, Y: torch.Tensor, z0: int, z1: int):
+    """Y = A X on the rows of planes [z0, z1); X valid on planes z0-1 .. z1."""
+    ctx = op.ctx
+    ctx.check(N.lib().paro_op_apply_planes(ctx.h, op.h, int(k), _ptr(X), _ld(X, ctx.n), _ptr(Y), int(z0), int(z1)))
+
+
+def gram_sym(ctx: Context, X: torch.Tensor, Y: torch.Tensor, k: int, r0: int, r1: int, out=None) -> torch.Tensor:
+    """X[:k]^T Y[:k] over rows [r0, r1) of a symmetric product (k x k, column-major)."""
+    G = out if out is not None else torch.empty(k * k, dtype=torch.float64, device=ctx.device)
+    ctx.check(N.lib().paro_gram_sym(ctx.h, int(k), _ptr(X), _ld(X, ctx.n), _ptr(Y), _ld(Y, ctx.n), int(r0), int(r1),
+                                    _ptr(G)))
+    return G
+
+
+def gram_rect(ctx: Context, X: torch.Tensor, k1: int, Y: torch.Tensor, k2: int, r0: int, r1: int,
+              out=None) -> torch.Tensor:
+    """X[:k1]^T Y[:k2] over rows [r0, r1) (k1 x k2, column-major; k1 <= 80, k2 <= 16)."""
+    G = out if out is not None else torch.empty(k1 * k2, dtype=torch.float64, device=ctx.device)
+    ctx.check(N.lib().paro_gram_rect(ctx.h, int(k1), _ptr(X), _ld(X, ctx.n), int(k2), _ptr(Y), _ld(Y, ctx.n),
+                                     int(r0), int(r1), _ptr(G)))
+    return G
+
+
+def rotate(ctx: Context, X: torch.Tensor, k1: int, Cm: torch.Tensor, ldc: int, k2: int, Z: torch.Tensor, r0: int,
+           r1: int, mode: int = 0):
+    """Z[:k2] = X[:k1] C over rows [r0, r1) (mode 1: Z -= X C, 4: Z += X C, 2: C triangular)."""
+    ctx.check(N.lib().paro_rotate(ctx.h, int(k1), _ptr(X), _ld(X, ctx.n), _ptr(Cm), int(ldc), int(k2), _ptr(Z),
+                                  _ld(Z, ctx.n), int(r0), int(r1), int(mode)))
+
+
+def ritz_ortho(ctx: Context, G: torch.Tensor, K: int, drop_tol: float, C1: torch.Tensor):
+    """Ordered Cholesky with the MGS drop rule of the raw Gram -> (k, min pivot ratio); C1 = K x k basis change."""
+    k = C.c_int(0)
+    rmin = C.c_double(0.0)
+    ctx.check(N.lib().paro_ritz_ortho(ctx.h, int(K), _ptr(G), float(drop_tol), _ptr(C1), C.byref(k), C.byref(rmin)))
+    return k.value, rmin.value
+
+
+def ritz_second_pass(ctx: Context, G2: torch.Tensor, k: int, C2: torch.Tensor, Bt: torch.Tensor) -> bool:
+    st = N.lib().paro_ritz_second_pass(ctx.h, int(k), _ptr(G2), _ptr(C2), _ptr(Bt))
+    if st == 6:  # PencilError: the pass is not positive definite -> the caller falls back to CGS2
+        return False
+    ctx.check(st)
+    return True
+
+
+def ritz_pencil(ctx: Context, GA: torch.Tensor, C2, Bt, GB, k: int, Y: torch.Tensor) -> list:
+    """The k x k pencil (in the Q basis from GA, C2, Bt, or directly from GA, GB) -> eigenvalues; Y = lift."""
+    vals = (C.c_double * k)()
+    ctx.check(N.lib().paro_ritz_pencil(ctx.h, int(k), _ptr(GA), _ptr(C2) if C2 is not None else None,
+                                       _ptr(Bt) if Bt is not None else None, _ptr(GB) if GB is not None else None,
+                                       vals, _ptr(Y)))
+    return list(vals)
+
+
+def gram_defect_of(ctx: Context, G: torch.Tensor, k: int) -> float:
+    out = C.c_double(0.0)
+    ctx.check(N.lib().paro_gram_defect(ctx.h, int(k), _ptr(G), C.byref(out)))
+    return out.value
+
+
+def sign_buffers(ctx: Context, k: int):
+    amax = torch.empty(k, dtype=torch.float64, device=ctx.device)
+    first = torch.empty(k, dtype=torch.int64, device=ctx.device)
+    flip = torch.empty(k, dtype=torch.float64, device=ctx.device)
+    ctx.check(N.lib().paro_sign_init(ctx.h, int(k), _ptr(amax), _ptr(first)))
+    return amax, first, flip
+
+
+def colmax(ctx: Context, V, k, r0, r1, amax):
+    ctx.check(N.lib().paro_colmax(ctx.h, int(k), _ptr(V), _ld(V, ctx.n), int(r0), int(r1), _ptr(amax)))
+
+
+def first_above(ctx: Context, V, k, r0, r1, amax, first):
+    ctx.check(N.lib().paro_first_above(ctx.h, int(k), _ptr(V), _ld(V, ctx.n), int(r0), int(r1), _ptr(amax),
+                                       _ptr(first)))
+
+
+def sign_flags(ctx: Context, V, k, r0, r1, amax, first, flip):
+    ctx.check(N.lib().paro_sign_flags(ctx.h, int(k), _ptr(V), _ld(V, ctx.n), int(r0), int(r1), _ptr(amax),
+                                      _ptr(first), _ptr(flip)))
+
+
+def negate_columns(ctx: Context, V, k, r0, r1, flip):
+    ctx.check(N.lib().paro_negate_columns(ctx.h, int(k), _ptr(V), _ld(V, ctx.n), int(r0), int(r1), _ptr(flip)))
+
+
+def density_rows(ctx: Context, U: torch.Tensor, occupations, r0: int, r1: int, rho: torch.Tensor) -> float:
+    """Nodal sum of density_from_orbitals on rows [r0, r1) of rho; returns sum occ."""
+    nocc = len(occupations)
+    if nocc == 0 or U.shape[0] < nocc:
+        raise N.InvalidArgumentError("density: orbital/occupation count mismatch")
+    occ = (C.c_double * nocc)(*[float(f) for f in occupations])
+    ctx.check(N.lib().paro_density_rows(ctx.h, nocc, _ptr(U), _ld(U, ctx.n), occ, int(r0), int(r1), _ptr(rho)))
+    return float(sum(occupations))
+
+
+def density_normalize(ctx: Context, total_occ: float, rho: torch.Tensor) -> float:
+    raw = C.c_double(0.0)
+    ctx.check(N.lib().paro_density_normalize(ctx.h, float(total_occ), _ptr(rho), C.byref(raw)))
+    return raw.value

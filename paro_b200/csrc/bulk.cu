@@ -141,8 +141,8 @@ __global__ void __launch_bounds__(kNT, kMinCtas) bulk_kernel(const MarchArgs a) 
   const int by = (blk / a.nTX) % a.nTY;
   const int bz = blk / (a.nTX * a.nTY);
   const int x0 = bx * kTX, y0 = by * kTY;
-  const int z0 = bz * a.ZC;
-  const int z1 = min(S, z0 + a.ZC);
+  const int z0 = a.zlo + bz * a.ZC;
+  const int z1 = min(a.zhi, z0 + a.ZC);
   const int tx = tid % kTX, ty = tid / kTX;
   const int gx = x0 + tx, gy = y0 + ty;
   const bool inside = gx < S && gy < S;

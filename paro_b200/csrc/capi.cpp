@@ -14,6 +14,7 @@
 #include "fields.hpp"
 #include "ritz.hpp"
 #include "solver.hpp"
+#include "step4.hpp"
 #include "csr.hpp"
 
 struct paro_ctx {
@@ -369,6 +370,101 @@ int paro_op_apply(paro_ctx* ctx, const paro_op* a, const paro_op* shift, double 
   });
 }
 
+int paro_op_apply_planes(paro_ctx* ctx, const paro_op* a, int k, const double* x, long long ld, double* y, int z0,
+                         int z1) {
+  return guarded(ctx, [&] {
+    apply_op(ctx->c, a->o, nullptr, 0.0, k, x, ld, y, ld, z0, z1);
+    return kOk;
+  });
+}
+
+// ------------------------------------------------ Step-4 building blocks on row ranges
+int paro_gram_sym(paro_ctx* ctx, int k, const double* x, long long ldx, const double* y, long long ldy, long long r0,
+                  long long r1, double* g) {
+  return guarded(ctx, [&] {
+    if (r0 < 0 || r1 < r0) throw ParoError(kInvalidArgument, "gram_sym: bad row range");
+    gram_sym_rows(ctx->c, k, x, ldx, y, ldy, r0, r1, g);
+    return kOk;
+  });
+}
+
+int paro_gram_rect(paro_ctx* ctx, int k1, const double* x, long long ldx, int k2, const double* y, long long ldy,
+                   long long r0, long long r1, double* g) {
+  return guarded(ctx, [&] {
+    if (r0 < 0 || r1 < r0) throw ParoError(kInvalidArgument, "gram_rect: bad row range");
+    gram_rect_rows(ctx->c, k1, x, ldx, k2, y, ldy, r0, r1, g);
+    return kOk;
+  });
+}
+
+int paro_rotate(paro_ctx* ctx, int k1, const double* x, long long ldx, const double* c, int ldc, int k2, double* z,
+                long long ldz, long long r0, long long r1, int mode) {
+  return guarded(ctx, [&] {
+    if (r0 < 0 || r1 < r0) throw ParoError(kInvalidArgument, "rotate: bad row range");
+    rotate_rows(ctx->c, k1, x, ldx, c, ldc, k2, z, ldz, r0, r1, mode);
+    return kOk;
+  });
+}
+
+int paro_ritz_ortho(paro_ctx* ctx, int K, const double* g, double drop_tol, double* c1, int* k_out,
+                    double* min_ratio) {
+  return guarded(ctx, [&] { return ritz_ortho(ctx->c, K, g, drop_tol, c1, k_out, min_ratio); });
+}
+
+int paro_ritz_second_pass(paro_ctx* ctx, int k, const double* g2, double* c2, double* bt) {
+  return guarded(ctx, [&] { return ritz_second_pass(ctx->c, k, g2, c2, bt); });
+}
+
+int paro_ritz_pencil(paro_ctx* ctx, int k, const double* ga, const double* c2, const double* bt, const double* gb,
+                     double* vals, double* y) {
+  return guarded(ctx, [&] { return ritz_pencil(ctx->c, k, ga, c2, bt, gb, vals, y); });
+}
+
+int paro_gram_defect(paro_ctx* ctx, int k, const double* g, double* out) {
+  return guarded(ctx, [&] {
+    *out = ritz_defect(ctx->c, k, g);
+    return kOk;
+  });
+}
+
+int paro_sign_init(paro_ctx* ctx, int k, double* amax, long long* first) {
+  return guarded(ctx, [&] {
+    sign_init(ctx->c, k, amax, first);
+    return kOk;
+  });
+}
+
+int paro_colmax(paro_ctx* ctx, int k, const double* v, long long ld, long long r0, long long r1, double* amax) {
+  return guarded(ctx, [&] {
+    colmax_rows(ctx->c, k, v, ld, r0, r1, amax);
+    return kOk;
+  });
+}
+
+int paro_first_above(paro_ctx* ctx, int k, const double* v, long long ld, long long r0, long long r1,
+                     const double* amax, long long* first) {
+  return guarded(ctx, [&] {
+    first_rows(ctx->c, k, v, ld, r0, r1, amax, first);
+    return kOk;
+  });
+}
+
+int paro_sign_flags(paro_ctx* ctx, int k, const double* v, long long ld, long long r0, long long r1,
+                    const double* amax, const long long* first, double* flip) {
+  return guarded(ctx, [&] {
+    sign_rows(ctx->c, k, v, ld, r0, r1, amax, first, flip);
+    return kOk;
+  });
+}
+
+int paro_negate_columns(paro_ctx* ctx, int k, double* v, long long ld, long long r0, long long r1,
+                        const double* flip) {
+  return guarded(ctx, [&] {
+    negate_rows(ctx->c, k, v, ld, r0, r1, flip);
+    return kOk;
+  });
+}
+
 static void fill_report(const SolveReport& r, size_t* iters, double* resid) {
   for (size_t c = 0; c < r.iterations.size(); ++c) {
     if (iters) iters[c] = static_cast<size_t>(r.iterations[c]);
@@ -549,6 +645,22 @@ int paro_density(paro_ctx* ctx, int nocc, const double* u, long long ld, const d
                  double* raw_integral) {
   return guarded(ctx, [&] {
     const double raw = density(ctx->c, nocc, u, ld, occ, rho);
+    if (raw_integral) *raw_integral = raw;
+    return kOk;
+  });
+}
+
+int paro_density_rows(paro_ctx* ctx, int nocc, const double* u, long long ld, const double* occ, long long r0,
+                      long long r1, double* rho) {
+  return guarded(ctx, [&] {
+    density_rows(ctx->c, nocc, u, ld, occ, r0, r1, rho);
+    return kOk;
+  });
+}
+
+int paro_density_normalize(paro_ctx* ctx, double total_occ, double* rho, double* raw_integral) {
+  return guarded(ctx, [&] {
+    const double raw = density_normalize(ctx->c, total_occ, rho);
     if (raw_integral) *raw_integral = raw;
     return kOk;
   });

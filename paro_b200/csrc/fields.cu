@@ -189,9 +189,13 @@ double cell_reduce(Ctx& ctx, int mode, const double* f, const double* g, int exc
   return out;
 }
 
-double density(Ctx& ctx, int nocc, const double* U, long long ld, const double* occ_host, double* rho) {
+// the nodal sum of density_from_orbitals (model.cpp:210-214) on rows [r0, r1)
+// (rho indexed globally); returns the total occupation
+double density_rows(Ctx& ctx, int nocc, const double* U, long long ld, const double* occ_host, long long r0,
+                    long long r1, double* rho) {
   ctx.check_grid();
   if (nocc <= 0) throw ParoError(kInvalidArgument, "density: orbital/occupation count mismatch");
+  if (r0 < 0 || r1 > ctx.grid.n || r1 < r0) throw ParoError(kInvalidArgument, "density: bad row range");
   double total = 0.0;
   for (int i = 0; i < nocc; ++i) {
     if (occ_host[i] < 0.0) throw ParoError(kInvalidArgument, "density: negative occupation");
@@ -200,16 +204,30 @@ double density(Ctx& ctx, int nocc, const double* U, long long ld, const double* 
   static thread_local DevBuf occ;
   double* docc = occ.get<double>(nocc);
   small_h2d(ctx, docc, occ_host, sizeof(double) * nocc);
+  const long long n = r1 - r0;
+  if (n > 0) {
+    density_kernel<<<grid1d(n), 256, 0, ctx.stream>>>(nocc, U + r0, ld, docc, n, rho + r0);
+    ++ctx.launches;
+  }
+  PARO_CUDA(cudaGetLastError());
+  return total;
+}
+
+// the normalisation of density_from_orbitals (model.cpp:215-221); returns the raw integral
+double density_normalize(Ctx& ctx, double total_occ, double* rho) {
   const long long n = ctx.grid.n;
-  density_kernel<<<grid1d(n), 256, 0, ctx.stream>>>(nocc, U, ld, docc, n, rho);
-  ++ctx.launches;
   const double raw = cell_reduce(ctx, kCellIntegrate, rho, nullptr, 0);
-  if (total > 0.0 && raw > 0.0) {
-    scale_kernel<<<grid1d(n), 256, 0, ctx.stream>>>(rho, n, total / raw);
+  if (total_occ > 0.0 && raw > 0.0) {
+    scale_kernel<<<grid1d(n), 256, 0, ctx.stream>>>(rho, n, total_occ / raw);
     ++ctx.launches;
   }
   PARO_CUDA(cudaGetLastError());
   return raw;
+}
+
+double density(Ctx& ctx, int nocc, const double* U, long long ld, const double* occ_host, double* rho) {
+  const double total = density_rows(ctx, nocc, U, ld, occ_host, 0, ctx.grid.n, rho);
+  return density_normalize(ctx, total, rho);
 }
 
 void mix(Ctx& ctx, const double* rin, const double* rout, double alpha, double* out) {

@@ -10,6 +10,11 @@ enum CellMode : int { kCellIntegrate = 0, kCellNorm2 = 1, kCellProduct = 2, kCel
 double cell_reduce(Ctx& ctx, int mode, const double* f, const double* g, int exchange_only);
 // rho = sum_i occ_i u_i^2, normalised to sum occ; returns the raw integral
 double density(Ctx& ctx, int nocc, const double* U, long long ld, const double* occ_host, double* rho);
+// its two halves: the nodal sum on rows [r0, r1) (returns sum occ) and the
+// normalisation of a complete nodal density (returns the raw integral)
+double density_rows(Ctx& ctx, int nocc, const double* U, long long ld, const double* occ_host, long long r0,
+                    long long r1, double* rho);
+double density_normalize(Ctx& ctx, double total_occ, double* rho);
 void mix(Ctx& ctx, const double* rin, const double* rout, double alpha, double* out);
 void diff(Ctx& ctx, const double* a, const double* b, double* out);
 double norm_l2(Ctx& ctx, const double* f);

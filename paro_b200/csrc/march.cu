@@ -157,8 +157,8 @@ __global__ void __launch_bounds__(kNT, CB <= 2 && kMinCtas == 2 ? 3 : kMinCtas) 
   const int by = (b / a.nTX) % a.nTY;
   const int bz = b / (a.nTX * a.nTY);
   const int x0 = bx * kTX, y0 = by * kTY;
-  const int z0 = bz * a.ZC;
-  const int z1 = min(S, z0 + a.ZC);
+  const int z0 = a.zlo + bz * a.ZC;
+  const int z1 = min(a.zhi, z0 + a.ZC);
   const int tx = tid % kTX, ty = tid / kTX;
   const int gx = x0 + tx, gy = y0 + ty;
   const bool inside = gx < S && gy < S;
@@ -485,8 +485,8 @@ __global__ void __launch_bounds__(kNT, CB <= 2 && kMinCtas == 2 ? 3 : kMinCtas) 
   const int by = (b / a.nTX) % a.nTY;
   const int bz = b / (a.nTX * a.nTY);
   const int x0 = bx * kTX, y0 = by * kTY;
-  const int z0 = bz * a.ZC;
-  const int z1 = min(S, z0 + a.ZC);
+  const int z0 = a.zlo + bz * a.ZC;
+  const int z1 = min(a.zhi, z0 + a.ZC);
   const int tx = tid % kTX, ty = tid / kTX;
   const int gx = x0 + tx, gy = y0 + ty;
   const bool inside = gx < S && gy < S;
@@ -910,20 +910,23 @@ void launch_march(int mode, bool var, int cb, const MarchArgs& a, cudaStream_t s
 
 // Spatial decomposition: 32x8 (x,y) tiles and a z-chunk sized so that one
 // column group still yields a few CTAs per SM on 148 SMs.
-void plan_march(MarchArgs& a, int S) {
+void plan_march(MarchArgs& a, int S, int zlo, int zhi) {
   a.S = S;
+  a.zlo = zlo;
+  a.zhi = zhi < 0 ? S : zhi;
+  const int nz = a.zhi - a.zlo;
   a.n = static_cast<long long>(S) * S * S;
   a.nTX = (S + kTX - 1) / kTX;
   a.nTY = (S + kTY - 1) / kTY;
   const long long target = 148 * 4;
-  long long zc = (static_cast<long long>(S) * a.nTX * a.nTY + target - 1) / target;
+  long long zc = (static_cast<long long>(nz) * a.nTX * a.nTY + target - 1) / target;
   static const int zc_max = [] {
     const char* e = std::getenv("PARO_ZC");  // experiment knob: planes per CTA z-chunk (default 32)
     return e ? std::atoi(e) : 32;
   }();
   zc = std::max<long long>(4, std::min<long long>(zc_max, zc));
-  a.ZC = static_cast<int>(std::min<long long>(zc, S));
-  a.nZ = (S + a.ZC - 1) / a.ZC;
+  a.ZC = static_cast<int>(std::max<long long>(1, std::min<long long>(zc, nz)));
+  a.nZ = (nz + a.ZC - 1) / a.ZC;
   a.nblk = a.nTX * a.nTY * a.nZ;
 }
 

@@ -59,6 +59,7 @@ struct MarchArgs {
   int S = 0;
   long long n = 0;
   int nTX = 0, nTY = 0, nZ = 0, ZC = 0;
+  int zlo = 0, zhi = 0;          // planes [zlo, zhi) whose rows are computed (row-slab Step 4); 0, S by default
   int nblk = 0;                  // spatial blocks = nTX*nTY*nZ
   int K = 0;                     // columns in the batch
   long long ld = 0;              // column stride of every vector operand
@@ -121,6 +122,6 @@ void launch_apply_flat(bool var, int cb, const MarchArgs& a, const double* coefp
 // before its first and after its last column.
 constexpr long long kBulkPad = 64;
 void launch_bulk(int mode, bool var, int cb, const MarchArgs& a, cudaStream_t st);
-void plan_march(MarchArgs& a, int S);
+void plan_march(MarchArgs& a, int S, int zlo = 0, int zhi = -1);
 
 }  // namespace paro_b200

@@ -9,7 +9,8 @@
 // i.e. CholQR2 in place of two-pass MGS (identical in exact arithmetic,
 // SURVEY.md §8a), with the stencil applies on the plane-marching kernels, the
 // tall-skinny Grams / rotations as FP64 DGEMMs and the K x K work in
-// single-warp kernels (dense.cu).
+// single-warp kernels (dense.cu). The tall-skinny Grams and rotations are
+// hand-written DMMA kernels (this file, step4.cu); no library GEMM.
 #include <algorithm>
 #include <cstdlib>
 #include <cmath>
@@ -18,14 +19,11 @@
 #include "dense.hpp"
 #include "ritz.hpp"
 #include "solver.hpp"
+#include "step4.hpp"
 
 namespace paro_b200 {
 
 namespace {
-
-void cublas_check(cublasStatus_t s, const char* what) {
-  if (s != CUBLAS_STATUS_SUCCESS) throw ParoError(kCuda, std::string("cuBLAS failure in ") + what);
-}
 
 // ---------------------------------------------------------------------------
 // Symmetric tall-skinny Gram G = X^T Y (n x k operands, k <= kGMaxK; X^T Y is
@@ -289,59 +287,81 @@ __global__ void gram_sym_reduce_kernel(const double* __restrict__ part, int P, i
   G[col + static_cast<long long>(row) * k] = s;
 }
 
-// G (k1 x k2, column-major) = X^T Y, X: n x k1 (ldx), Y: n x k2 (ldy)
-void gram(Ctx& ctx, int k1, int k2, const double* X, long long ldx, const double* Y, long long ldy, double* G) {
-  const long long n = ctx.grid.n;
-  if (k1 == k2 && k1 <= kGMaxK) {
+}  // namespace
+
+// G (k x k, column-major) = X[r0:r1)^T Y[r0:r1) of a symmetric product
+void gram_sym_rows(Ctx& ctx, int k, const double* X, long long ldx, const double* Y, long long ldy, long long r0,
+                   long long r1, double* G) {
+  if (k <= 0) return;
+  X += r0;
+  Y += r0;
+  const long long n = std::max<long long>(0, r1 - r0);
+  if (k <= kGMaxK) {
     const int P = 148 * 4;
-    const long long chunk = ((n + P - 1) / P + kGR - 1) / kGR * kGR;
-    const int Pn = static_cast<int>((n + chunk - 1) / chunk);
+    long long chunk = ((n + P - 1) / P + kGR - 1) / kGR * kGR;
+    if (chunk <= 0) chunk = kGR;
+    const int Pn = static_cast<int>(std::max<long long>(1, (n + chunk - 1) / chunk));
     double* part = ctx.ws_gram.get<double>(static_cast<size_t>(Pn) * kGPairsMax * kGB * kGB);
     constexpr size_t smem = sizeof(double) * 4 * kGR * kGRow;
     static bool configured = false;
     if (!configured) {
       PARO_CUDA(cudaFuncSetAttribute(gram_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
+      PARO_CUDA(cudaFuncSetAttribute(gram_sym_fixed_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+      PARO_CUDA(cudaFuncSetAttribute(gram_sym_fixed_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
       configured = true;
     }
-    const int nbk = (k1 + kGB - 1) / kGB;
-    static const bool generic = [] {
-      const char* e = std::getenv("PARO_GRAM_GENERIC");  // experiment knob: the predicated kernel only
-      return e && e[0] == '1';
-    }();
-    if (!generic && (nbk == 10 || nbk == 8)) {
-      auto kern = nbk == 10 ? gram_sym_fixed_kernel<10> : gram_sym_fixed_kernel<8>;
-      static bool conf_fixed[2] = {false, false};
-      bool& cf = conf_fixed[nbk == 10 ? 1 : 0];
-      if (!cf) {
-        PARO_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        cf = true;
-      }
-      kern<<<Pn, kGThreads, smem, ctx.stream>>>(X, ldx, Y, ldy, k1, n, chunk, part);
+    const int nb = (k + kGB - 1) / kGB;
+    if (nb == 10 || nb == 8) {
+      auto kern = nb == 10 ? gram_sym_fixed_kernel<10> : gram_sym_fixed_kernel<8>;
+      kern<<<Pn, kGThreads, smem, ctx.stream>>>(X, ldx, Y, ldy, k, n, chunk, part);
     } else {
-      gram_sym_kernel<<<Pn, kGThreads, smem, ctx.stream>>>(X, ldx, Y, ldy, k1, n, chunk, part);
+      gram_sym_kernel<<<Pn, kGThreads, smem, ctx.stream>>>(X, ldx, Y, ldy, k, n, chunk, part);
     }
-    const int nb = (k1 + kGB - 1) / kGB;
-    gram_sym_reduce_kernel<<<nb * (nb + 1) / 2, kGB * kGB, 0, ctx.stream>>>(part, Pn, k1, G);
+    gram_sym_reduce_kernel<<<nb * (nb + 1) / 2, kGB * kGB, 0, ctx.stream>>>(part, Pn, k, G);
     PARO_CUDA(cudaGetLastError());
     ctx.launches += 2;
     return;
   }
-  const double one = 1.0, zero = 0.0;
-  cublas_check(cublasDgemm(ctx.cublas, CUBLAS_OP_T, CUBLAS_OP_N, k1, k2, static_cast<int>(n), &one, X,
-                           static_cast<int>(ldx), Y, static_cast<int>(ldy), &zero, G, k1),
-               "gram");
-  ++ctx.launches;
+  // wider bases (baseline_geneig blocks beyond 80 columns): 80 x 16 rectangular tiles
+  double* tile = ctx.ws_small3.get<double>(80 * 16);
+  for (int i0 = 0; i0 < k; i0 += 80) {
+    const int ki = std::min(80, k - i0);
+    for (int j0 = 0; j0 < k; j0 += 16) {
+      const int kj = std::min(16, k - j0);
+      gram_rect_rows(ctx, ki, X + i0 * ldx, ldx, kj, Y + j0 * ldy, ldy, 0, n, tile);
+      PARO_CUDA(cudaMemcpy2DAsync(G + i0 + static_cast<long long>(j0) * k, sizeof(double) * k, tile,
+                                  sizeof(double) * ki, sizeof(double) * ki, kj, cudaMemcpyDeviceToDevice, ctx.stream));
+    }
+  }
 }
 
-// Z (n x k2) = X (n x k1) C (k1 x k2, column-major, ldc)
+namespace {
+
+void gram(Ctx& ctx, int k, const double* X, long long ldx, const double* Y, long long ldy, double* G) {
+  gram_sym_rows(ctx, k, X, ldx, Y, ldy, 0, ctx.grid.n, G);
+}
+
+// Z (n x k2) = X (n x k1) C (k1 x k2, column-major, ldc); tri: C is the
+// Cholesky-QR basis change (zero below the drop-shifted diagonal)
 void rotate(Ctx& ctx, int k1, int k2, const double* X, long long ldx, const double* Cm, int ldc, double* Z,
-            long long ldz) {
-  const double one = 1.0, zero = 0.0;
-  cublas_check(cublasDgemm(ctx.cublas, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(ctx.grid.n), k2, k1, &one, X,
-                           static_cast<int>(ldx), Cm, ldc, &zero, Z, static_cast<int>(ldz)),
-               "rotate");
-  ++ctx.launches;
+            long long ldz, bool tri = false) {
+  const long long n = ctx.grid.n;
+  if (k1 <= 80 && k2 <= 80) {
+    rotate_rows(ctx, k1, X, ldx, Cm, ldc, k2, Z, ldz, 0, n, tri ? 2 : 0);
+    return;
+  }
+  // blocked over 80-column slices of C (bit 2: accumulate)
+  for (int j0 = 0; j0 < k2; j0 += 80) {
+    const int kj = std::min(80, k2 - j0);
+    for (int i0 = 0; i0 < k1; i0 += 80) {
+      const int ki = std::min(80, k1 - i0);
+      rotate_rows(ctx, ki, X + i0 * ldx, ldx, Cm + i0 + static_cast<long long>(j0) * ldc, ldc, kj,
+                  Z + j0 * ldz, ldz, 0, n, i0 == 0 ? 0 : 4);
+    }
+  }
 }
 
 __device__ __forceinline__ double block_max(double v, double* sh) {
@@ -354,67 +374,6 @@ __device__ __forceinline__ double block_max(double v, double* sh) {
     for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) v = fmax(v, sh[w]);
   __syncthreads();
   return v;
-}
-
-// fix_sign (linalg.cpp:229-241) on device columns: max |v|, first index with
-// |v_i| > 1e-12 max, negate the column if that entry is negative.
-__global__ void colmax_kernel(const double* V, long long ld, long long n, unsigned long long* amax) {
-  __shared__ double sh[32];
-  const int c = blockIdx.y;
-  double m = 0.0;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x)
-    m = fmax(m, fabs(V[c * ld + i]));
-  m = block_max(m, sh);
-  if (threadIdx.x == 0 && m > 0.0) atomicMax(amax + c, static_cast<unsigned long long>(__double_as_longlong(m)));
-}
-
-// first index with |v| > 1e-12 max|v| (fix_sign, linalg.cpp:229-241): each
-// block scans one contiguous segment, low segments first, and stops as soon as
-// a lower index is already known (the pivot is usually in the first planes)
-__global__ void firstidx_kernel(const double* V, long long ld, long long n, const unsigned long long* amax,
-                                unsigned long long* first) {
-  __shared__ int stop;
-  const int c = blockIdx.y;
-  const double thr = 1e-12 * __longlong_as_double(static_cast<long long>(amax[c]));
-  const long long seg = (n + gridDim.x - 1) / gridDim.x;
-  const long long lo = blockIdx.x * seg, hi = min(n, lo + seg);
-  for (long long base = lo; base < hi; base += blockDim.x) {
-    if (threadIdx.x == 0) stop = *reinterpret_cast<volatile const unsigned long long*>(first + c) <
-                                 static_cast<unsigned long long>(base);
-    __syncthreads();
-    if (stop) return;
-    const long long i = base + threadIdx.x;
-    const bool hit = i < hi && fabs(V[c * ld + i]) > thr;
-    if (hit) atomicMin(first + c, static_cast<unsigned long long>(i));
-    if (__syncthreads_or(hit)) return;
-  }
-}
-
-// decide every column's sign before any block negates (the pivot entry is
-// itself negated by some block, so it cannot be re-read inside negate_kernel)
-__global__ void decide_sign_kernel(const double* V, long long ld, long long n, int k, const unsigned long long* amax,
-                                   unsigned long long* first) {
-  for (int c = threadIdx.x; c < k; c += blockDim.x) {
-    const bool flip = amax[c] != 0ull && first[c] < static_cast<unsigned long long>(n) &&
-                      V[c * ld + static_cast<long long>(first[c])] < 0.0;
-    first[c] = flip ? 1ull : 0ull;
-  }
-}
-
-__global__ void negate_kernel(double* V, long long ld, long long n, const unsigned long long* flip) {
-  const int c = blockIdx.y;
-  if (flip[c] == 0ull) return;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x)
-    V[c * ld + i] = -V[c * ld + i];
-}
-
-__global__ void init_sign_kernel(int k, unsigned long long* amax, unsigned long long* first) {
-  for (int i = threadIdx.x; i < k; i += blockDim.x) {
-    amax[i] = 0ull;
-    first[i] = ~0ull;
-  }
 }
 
 // gram_defect (paro.cpp:50-61): max over j <= i of |v_i^T B v_j - delta_ij|.
@@ -431,20 +390,19 @@ __global__ void defect_kernel(int k, const double* G, double* out) {
 
 }  // namespace
 
+// fix_sign (linalg.cpp:229-241) of k device columns: the row-range pieces of
+// step4.cu over all n rows (a sharded Step 4 combines them across ranks)
 void fix_sign_columns(Ctx& ctx, double* V, long long ld, int k) {
   if (k <= 0) return;
   const long long n = ctx.grid.n;
-  auto* amax = ctx.ws_small3.get<unsigned long long>(2 * static_cast<size_t>(k));
-  unsigned long long* first = amax + k;
-  cudaStream_t st = ctx.stream;
-  init_sign_kernel<<<1, 256, 0, st>>>(k, amax, first);
-  const int bx = static_cast<int>(std::min<long long>(148 * 4, (n + 255) / 256));
-  colmax_kernel<<<dim3(bx, k), 256, 0, st>>>(V, ld, n, amax);
-  firstidx_kernel<<<dim3(bx, k), 256, 0, st>>>(V, ld, n, amax, first);
-  decide_sign_kernel<<<1, 256, 0, st>>>(V, ld, n, k, amax, first);
-  negate_kernel<<<dim3(bx, k), 256, 0, st>>>(V, ld, n, first);
-  ctx.launches += 5;
-  PARO_CUDA(cudaGetLastError());
+  double* amax = ctx.ws_small3.get<double>(3 * static_cast<size_t>(k));
+  double* flip = amax + k;
+  auto* first = reinterpret_cast<long long*>(amax + 2 * k);
+  sign_init(ctx, k, amax, first);
+  colmax_rows(ctx, k, V, ld, 0, n, amax);
+  first_rows(ctx, k, V, ld, 0, n, amax, first);
+  sign_rows(ctx, k, V, ld, 0, n, amax, first, flip);
+  negate_rows(ctx, k, V, ld, 0, n, flip);
 }
 
 namespace {
@@ -513,11 +471,9 @@ __global__ void div_kernel(double* dst, const double* src, double d, long long n
     dst[i] = src[i] / d;  // x /= nb (linalg.cpp:431)
 }
 
-double ddot(Ctx& ctx, const double* x, const double* y) {
-  double r = 0.0;
-  cublas_check(cublasDdot(ctx.cublas, static_cast<int>(ctx.grid.n), x, 1, y, 1, &r), "ddot");
-  ++ctx.launches;
-  return r;
+double ddot(Ctx& ctx, const double* x, const double* y, double* d) {
+  gram_rect_rows(ctx, 1, x, ctx.grid.n, 1, y, ctx.grid.n, 0, ctx.grid.n, d);
+  return read_double(ctx, d);
 }
 
 // b_orthonormalize (linalg.cpp:409-439) as two-pass classical Gram-Schmidt in
@@ -528,26 +484,30 @@ int cgs2_orthonormalize(Ctx& ctx, const Op& B, int K, const double* U, double dr
                         int* kout, int* accepted = nullptr) {
   const long long n = ctx.grid.n;
   cudaStream_t st = ctx.stream;
-  double* h = ctx.ws_e.get<double>(2 * static_cast<size_t>(n) + K);
+  double* h = ctx.ws_e.get<double>(2 * static_cast<size_t>(n) + K + 8);
   double* Bh = h + n;
   double* c = Bh + n;
-  const double one = 1.0, zero = 0.0, mone = -1.0;
+  double* d = c + K;
   const int blocks = static_cast<int>(std::min<long long>(148 * 8, (n + 255) / 256));
   int k = 0;
   for (int j = 0; j < K; ++j) {
     PARO_CUDA(cudaMemcpyAsync(h, U + j * n, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     apply_op(ctx, B, nullptr, 0.0, 1, h, n, Bh, n);
-    const double orig = std::sqrt(std::max(0.0, ddot(ctx, h, Bh)));
+    const double orig = std::sqrt(std::max(0.0, ddot(ctx, h, Bh, d)));
     if (!(orig > 0.0)) continue;
     for (int pass = 0; pass < 2 && k > 0; ++pass) {
-      cublas_check(cublasDgemv(ctx.cublas, CUBLAS_OP_T, static_cast<int>(n), k, &one, BQ, static_cast<int>(n), h, 1,
-                               &zero, c, 1), "cgs proj");
-      cublas_check(cublasDgemv(ctx.cublas, CUBLAS_OP_N, static_cast<int>(n), k, &mone, Q, static_cast<int>(n), c, 1,
-                               &one, h, 1), "cgs update");
-      ctx.launches += 2;
+      // c = (B Q)^T h, h -= Q c, over 80-column slices of the accepted basis
+      for (int i0 = 0; i0 < k; i0 += 80) {
+        const int ki = std::min(80, k - i0);
+        gram_rect_rows(ctx, ki, BQ + i0 * n, n, 1, h, n, 0, n, c + i0);
+      }
+      for (int i0 = 0; i0 < k; i0 += 80) {
+        const int ki = std::min(80, k - i0);
+        rotate_rows(ctx, ki, Q + i0 * n, n, c + i0, ki, 1, h, n, 0, n, 1);
+      }
     }
     apply_op(ctx, B, nullptr, 0.0, 1, h, n, Bh, n);
-    const double nb = std::sqrt(std::max(0.0, ddot(ctx, h, Bh)));
+    const double nb = std::sqrt(std::max(0.0, ddot(ctx, h, Bh, d)));
     if (nb <= drop_tol * orig) continue;
     div_kernel<<<blocks, 256, 0, st>>>(Q + k * n, h, nb, n);
     ++ctx.launches;
@@ -569,7 +529,6 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
   const long long n = ctx.grid.n;
   if (ld != n || ldv != n) throw ParoError(kInvalidArgument, "rayleigh_ritz: vectors must be contiguous (ld == n)");
   cudaStream_t st = ctx.stream;
-  cublasSetStream(ctx.cublas, st);
   struct ClearCopyout {  // the copy-out request is one-shot
     Ctx& c;
     ~ClearCopyout() { c.ritz_copyout.host = nullptr; }
@@ -607,7 +566,7 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
                                   sizeof(double) * n, cudaMemcpyDeviceToHost, co.stream));
     }
     apply_op(ctx, B, nullptr, 0.0, kk, V, ldv, W, n);
-    gram(ctx, kk, kk, V, ldv, W, n, s.G3);
+    gram(ctx, kk, V, ldv, W, n, s.G3);
     defect_kernel<<<1, 256, 0, st>>>(kk, s.G3, s.defect);
     ++ctx.launches;
     return read_double(ctx, s.defect);
@@ -617,7 +576,7 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
   if (!use_cgs) {
     // CholQR pass 1: Gram of the candidates, ordered Cholesky with drops
     apply_op(ctx, B, nullptr, 0.0, K, U, ld, W, n);
-    gram(ctx, K, K, U, ld, W, n, s.G);
+    gram(ctx, K, U, ld, W, n, s.G);
     ortho_from_gram_kernel<<<1, 32, 0, st>>>(K, s.G, drop_tol, 1, s.C1, s.acc, s.kout, s.rmin, s.w, s.status);
     ++ctx.launches;
     PARO_CUDA(cudaGetLastError());
@@ -631,17 +590,17 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
   if (!use_cgs) {
     const int cs = check_count(k);
     if (cs != kOk) return cs;
-    rotate(ctx, K, k, U, ld, s.C1, K, Q1, n);
+    rotate(ctx, K, k, U, ld, s.C1, K, Q1, n, true);
     // pass 2
     apply_op(ctx, B, nullptr, 0.0, k, Q1, n, W, n);
-    gram(ctx, k, k, Q1, n, W, n, s.G2);
+    gram(ctx, k, Q1, n, W, n, s.G2);
     second_pass_kernel<<<1, 32, 0, st>>>(k, s.G2, s.C2, s.Bt, s.w, s.status);
     ++ctx.launches;
     if (read_int(ctx, s.status) != kOk) {
       use_cgs = true;
     } else {
       apply_op(ctx, A, nullptr, 0.0, k, Q1, n, W, n);
-      gram(ctx, k, k, Q1, n, W, n, s.GA);
+      gram(ctx, k, Q1, n, W, n, s.GA);
       dense_configure();
       pencil_kernel<<<1, kDenseThreads, dense_jacobi_smem(k), st>>>(k, s.GA, s.C2, s.Bt, s.vals, s.Y, s.At, s.X, s.w, s.status);
       ++ctx.launches;
@@ -661,8 +620,8 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
     if (cs != kOk) return cs;
     double* AQ = ctx.ws_d.get<double>(static_cast<size_t>(k) * n);
     apply_op(ctx, A, nullptr, 0.0, k, Q1, n, AQ, n);
-    gram(ctx, k, k, Q1, n, AQ, n, s.GA);
-    gram(ctx, k, k, Q1, n, BQ, n, s.G2);
+    gram(ctx, k, Q1, n, AQ, n, s.GA);
+    gram(ctx, k, Q1, n, BQ, n, s.G2);
     dense_configure();
     pencil_direct_kernel<<<1, kDenseThreads, dense_jacobi_smem(k), st>>>(k, s.GA, s.G2, s.vals, s.Y, s.At, s.Bt, s.X, s.w, s.status);
     ++ctx.launches;
@@ -683,11 +642,64 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
   return kOk;
 }
 
+// ---------------------------------------------------------------------------
+// The K x K stages of rayleigh_ritz on caller buffers (device, column-major),
+// for a Step 4 orchestrated over row slabs (the Grams combined across ranks
+// before each stage; every rank then runs the same stage on the same input).
+int ritz_ortho(Ctx& ctx, int K, const double* G, double drop_tol, double* C1, int* k_out, double* min_ratio) {
+  Small s = small_buffers(ctx, K);
+  ortho_from_gram_kernel<<<1, 32, 0, ctx.stream>>>(K, G, drop_tol, 1, C1, s.acc, s.kout, s.rmin, s.w, s.status);
+  ++ctx.launches;
+  PARO_CUDA(cudaGetLastError());
+  *k_out = read_int(ctx, s.kout);
+  *min_ratio = read_double(ctx, s.rmin);
+  return kOk;
+}
+
+int ritz_second_pass(Ctx& ctx, int k, const double* G2, double* C2, double* Bt) {
+  Small s = small_buffers(ctx, k);
+  second_pass_kernel<<<1, 32, 0, ctx.stream>>>(k, G2, C2, Bt, s.w, s.status);
+  ++ctx.launches;
+  PARO_CUDA(cudaGetLastError());
+  if (read_int(ctx, s.status) != kOk) {
+    ctx.err = "rayleigh_ritz: second Cholesky-QR pass not positive definite";
+    return kPencil;
+  }
+  return kOk;
+}
+
+int ritz_pencil(Ctx& ctx, int k, const double* GA, const double* C2, const double* Bt, const double* GB,
+                double* vals_host, double* Y) {
+  Small s = small_buffers(ctx, k);
+  dense_configure();
+  if (GB == nullptr)
+    pencil_kernel<<<1, kDenseThreads, dense_jacobi_smem(k), ctx.stream>>>(k, GA, C2, Bt, s.vals, Y, s.At, s.X, s.w,
+                                                                          s.status);
+  else
+    pencil_direct_kernel<<<1, kDenseThreads, dense_jacobi_smem(k), ctx.stream>>>(k, GA, GB, s.vals, Y, s.At, s.Bt,
+                                                                                 s.X, s.w, s.status);
+  ++ctx.launches;
+  PARO_CUDA(cudaGetLastError());
+  if (read_int(ctx, s.status) != kOk) {
+    ctx.err = "pencil: B is not positive definite";
+    return kPencil;
+  }
+  small_d2h(ctx, vals_host, s.vals, sizeof(double) * k);
+  return kOk;
+}
+
+double ritz_defect(Ctx& ctx, int k, const double* G) {
+  Small s = small_buffers(ctx, k);
+  defect_kernel<<<1, 256, 0, ctx.stream>>>(k, G, s.defect);
+  ++ctx.launches;
+  PARO_CUDA(cudaGetLastError());
+  return read_double(ctx, s.defect);
+}
+
 int b_orthonormalize(Ctx& ctx, const Op& B, int K, const double* U, double drop_tol, double* Q, int* k_out,
                      int* accepted) {
   ctx.check_grid();
   const long long n = ctx.grid.n;
-  cublasSetStream(ctx.cublas, ctx.stream);
   double* BQ = ctx.ws_b.get<double>(static_cast<size_t>(K) * n);
   cgs2_orthonormalize(ctx, B, K, U, drop_tol, Q, BQ, k_out, accepted);
   PARO_CUDA(cudaStreamSynchronize(ctx.stream));

@@ -164,13 +164,18 @@ OpDev make_opdev(const Ctx& ctx, const Op& a, const Op* shift, double sigma) {
 }
 
 void apply_op(Ctx& ctx, const Op& a, const Op* shift, double sigma, int K, const double* x, long long ldx,
-              double* y, long long ldy) {
+              double* y, long long ldy, int z0, int z1) {
   ctx.check_grid();
   if (ldx != ldy) throw ParoError(kInvalidArgument, "apply: x and y must share a column stride");
   if (K <= 0) return;
   if (shift && shift->var) throw ParoError(kInvalidArgument, "apply: shift operator must be a constant stencil");
+  if (z1 < 0) z1 = ctx.grid.S;
+  if (z0 < 0 || z1 > ctx.grid.S || z0 >= z1) {
+    if (z0 == z1) return;
+    throw ParoError(kInvalidArgument, "apply: plane range outside the lattice");
+  }
   MarchArgs m;
-  plan_march(m, ctx.grid.S);
+  plan_march(m, ctx.grid.S, z0, z1);
   m.K = K;
   m.ld = ldx;
   m.op = preshift(ctx, make_opdev(ctx, a, shift, sigma));

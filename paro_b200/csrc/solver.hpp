@@ -17,8 +17,10 @@ struct SolveReport {
 
 OpDev make_opdev(const Ctx& ctx, const Op& a, const Op* shift, double sigma);
 
+// y = (A + sigma shift) x on the rows of planes [z0, z1) (default: all);
+// x must hold valid values on planes z0 - 1 .. z1 (the stencil's reach)
 void apply_op(Ctx& ctx, const Op& a, const Op* shift, double sigma, int K, const double* x, long long ldx,
-              double* y, long long ldy);
+              double* y, long long ldy, int z0 = 0, int z1 = -1);
 
 int source_solve(Ctx& ctx, const Op& a, const Op& b, double sigma, int K, const double* u, long long ld,
                  const double* lambdas, double tol, unsigned long long max_iter, double* out, SolveReport* rep);

@@ -180,8 +180,8 @@ __global__ void __launch_bounds__(kNT, kMinCtas) tma_kernel(const MarchArgs a, c
   const int by = (blk / a.nTX) % a.nTY;
   const int bz = blk / (a.nTX * a.nTY);
   const int x0 = bx * kTX, y0 = by * kTY;
-  const int z0 = bz * a.ZC;
-  const int z1 = min(S, z0 + a.ZC);
+  const int z0 = a.zlo + bz * a.ZC;
+  const int z1 = min(a.zhi, z0 + a.ZC);
   const int tx = tid % kTX, ty = tid / kTX;
   const int gx = x0 + tx, gy = y0 + ty;
   const bool inside = gx < S && gy < S;
@@ -510,8 +510,8 @@ __global__ void __launch_bounds__(kNT, CB >= 8 ? 1 : kMinCtas)
   const int by = (blk / a.nTX) % a.nTY;
   const int bz = blk / (a.nTX * a.nTY);
   const int x0 = bx * kTX, y0 = by * kTY;
-  const int z0 = bz * a.ZC;
-  const int z1 = min(S, z0 + a.ZC);
+  const int z0 = a.zlo + bz * a.ZC;
+  const int z1 = min(a.zhi, z0 + a.ZC);
   const int tx = tid % kTX, ty = tid / kTX;
   const int gx = x0 + tx, gy = y0 + ty;
   const bool inside = gx < S && gy < S;
@@ -747,8 +747,8 @@ __global__ void __launch_bounds__(kNT, kMinCtas)
   const int by = (blk / a.nTX) % a.nTY;
   const int bz = blk / (a.nTX * a.nTY);
   const int x0 = bx * kTX, y0 = by * kTY;
-  const int z0 = bz * a.ZC;
-  const int z1 = min(S, z0 + a.ZC);
+  const int z0 = a.zlo + bz * a.ZC;
+  const int z1 = min(a.zhi, z0 + a.ZC);
   const int tx = tid % kTX, ty = tid / kTX;
   const int gx = x0 + tx, gy = y0 + ty;
   const bool inside = gx < S && gy < S;
@@ -934,8 +934,8 @@ __global__ void __launch_bounds__(kNT, kMinCtas)
   const int by = (blk / a.nTX) % a.nTY;
   const int bz = blk / (a.nTX * a.nTY);
   const int x0 = bx * kTX, y0 = by * kTY;
-  const int z0 = bz * a.ZC;
-  const int z1 = min(S, z0 + a.ZC);
+  const int z0 = a.zlo + bz * a.ZC;
+  const int z1 = min(a.zhi, z0 + a.ZC);
   const int tx = tid % kTX, ty = tid / kTX;
   const int gx = x0 + tx, gy = y0 + ty;
   const bool inside = gx < S && gy < S;
@@ -1222,8 +1222,8 @@ __global__ void __launch_bounds__(kNT, VAR ? kMinCtas : 3)
   const int by = (blk / a.nTX) % a.nTY;
   const int bz = blk / (a.nTX * a.nTY);
   const int x0 = bx * kTX, y0 = by * kTY;
-  const int z0 = bz * a.ZC;
-  const int z1 = min(S, z0 + a.ZC);
+  const int z0 = a.zlo + bz * a.ZC;
+  const int z1 = min(a.zhi, z0 + a.ZC);
   const int tx = tid % kTX, ty = tid / kTX;
   const int gx = x0 + tx, gy = y0 + ty;
   const bool inside = gx < S && gy < S;

@@ -5,12 +5,16 @@ Mirrors the loop bodies of the reference drivers with the adaptive branch off
   Kohn-Sham  proj/src/paro.cpp:514-638   (Step 2 estimator omitted on both sides)
   linear     proj/src/paro.cpp:340-354
 Multi-GPU: rank r owns a contiguous block of orbital columns
-and solves its Step-3 source problems with no communication; the half-step
-orbitals are all-gathered once per iteration and every rank then runs the
-(small, deterministic) Step 4 and potential rebuild on identical inputs, so
-all ranks hold bitwise-identical orbitals, densities and energies and the
-results do not depend on the GPU count. The compute is delegated to a
-backend (GpuBackend = the native sm_100a library); the orchestration is
+and solves its Step-3 source problems with no communication. The half-step
+orbitals are then transposed (one all-to-all) into row slabs: rank r holds
+all K columns on its block of lattice planes (+ one halo plane each side),
+and Step 4 runs sharded over the slabs (step4.py): the K x K Gram partials
+are summed across ranks in rank order, the fix_sign pieces reduced, and
+every per-dof operation stays on the slab. The densities are computed on the
+slabs and all-gathered (the Hartree solve, KS form and energy stay
+replicated on the full density), and the new orbitals go back to column
+shards with a second all-to-all. The compute is delegated to a backend
+(GpuBackend = the native sm_100a library); the orchestration is
 backend-agnostic so the N > 1 path is testable with gloo on CPU.
 """
 from __future__ import annotations
@@ -22,6 +26,7 @@ import torch
 
 from . import _native as N
 from .configs import Workload, guess_vectors
+from .step4 import RowSlab, Step4
 
 OK, NOT_SPD, ITER_LIMIT = 0, 3, 4
 
@@ -81,6 +86,90 @@ class Dist:
             out[row: row + cnt].copy_(recv[r * kmax: r * kmax + cnt])
             row += cnt
         return out
+
+    # ---- Step-4 reductions (step4.py): fixed rank order, identical on every rank
+    def allsum_(self, t: torch.Tensor) -> torch.Tensor:
+        """In-place sum over ranks, added in rank order (deterministic, and
+        the same bits on every rank)."""
+        if self.world == 1:
+            return t
+        flat = t.reshape(-1)
+        buf = flat.new_empty(self.world * flat.numel())
+        self._gather(buf, flat.contiguous())
+        parts = buf.view(self.world, -1)
+        flat.copy_(parts[0])
+        for r in range(1, self.world):
+            flat.add_(parts[r])
+        return t
+
+    def allmax_(self, t: torch.Tensor) -> torch.Tensor:
+        if self.world > 1:
+            self.td.all_reduce(t, op=self.td.ReduceOp.MAX, group=self.group)
+        return t
+
+    def allmin_(self, t: torch.Tensor) -> torch.Tensor:
+        if self.world > 1:
+            self.td.all_reduce(t, op=self.td.ReduceOp.MIN, group=self.group)
+        return t
+
+    def cols_to_slabs(self, local: torch.Tensor, counts, dst: torch.Tensor, slabs):
+        """Column shards -> row slabs: this rank's columns [k_r, n] (all rows)
+        go out as the extended row range of every rank's slab; dst[:K] receives
+        every rank's columns on this rank's extended rows. One all-to-all."""
+        me = slabs[self.rank]
+        c0 = sum(counts[: self.rank])
+        if self.world == 1:
+            if local.data_ptr() != dst[c0:].data_ptr():
+                dst[c0:c0 + local.shape[0], me.e0:me.e1].copy_(local[:, me.e0:me.e1])
+            return dst
+        k = local.shape[0]
+        send = torch.cat([local[:, s.e0:s.e1].reshape(-1) for s in slabs])
+        ext = me.e1 - me.e0
+        recv = local.new_empty(sum(counts) * ext)
+        self.td.all_to_all_single(recv, send, [c * ext for c in counts], [k * (s.e1 - s.e0) for s in slabs],
+                                  group=self.group)
+        off, col = 0, 0
+        for cnt in counts:
+            dst[col:col + cnt, me.e0:me.e1].copy_(recv[off:off + cnt * ext].view(cnt, ext))
+            off += cnt * ext
+            col += cnt
+        return dst
+
+    def slabs_to_cols(self, V: torch.Tensor, counts, slabs):
+        """Row slabs -> column shards, in place: V[:K] holds every column on this
+        rank's own rows; afterwards this rank's columns hold every row."""
+        if self.world == 1:
+            return V
+        me = slabs[self.rank]
+        c0 = sum(counts[: self.rank])
+        k = counts[self.rank]
+        starts = [sum(counts[:r]) for r in range(self.world)]
+        send = torch.cat([V[starts[r]:starts[r] + counts[r], me.r0:me.r1].reshape(-1) for r in range(self.world)])
+        rows = [s.r1 - s.r0 for s in slabs]
+        recv = V.new_empty(k * sum(rows))
+        self.td.all_to_all_single(recv, send, [k * r for r in rows], [c * (me.r1 - me.r0) for c in counts],
+                                  group=self.group)
+        off = 0
+        for s, r in zip(slabs, rows):
+            if s is not me:
+                V[c0:c0 + k, s.r0:s.r1].copy_(recv[off:off + k * r].view(k, r))
+            off += k * r
+        return V
+
+    def allgather_rows(self, f: torch.Tensor, slabs):
+        """f (n) valid on this rank's own rows -> valid everywhere."""
+        if self.world == 1:
+            return f
+        m = max(s.r1 - s.r0 for s in slabs)
+        me = slabs[self.rank]
+        send = f.new_zeros(m)
+        send[: me.r1 - me.r0].copy_(f[me.r0:me.r1])
+        buf = f.new_empty(self.world * m)
+        self._gather(buf, send)
+        for r, s in enumerate(slabs):
+            if s is not me:
+                f[s.r0:s.r1].copy_(buf[r * m: r * m + (s.r1 - s.r0)])
+        return f
 
     def allgather_ints(self, values, counts, device):
         if self.world == 1:
@@ -191,6 +280,71 @@ class GpuBackend:
     def launches(self) -> int:
         return self.ctx.launches()
 
+    # ---- Step 4 building blocks on row ranges (step4.py)
+    @property
+    def S(self) -> int:
+        return self.ctx.S
+
+    def mass_op(self):
+        return self.mass
+
+    def apply_planes(self, op, X, k, Y, z0, z1):
+        self.core.apply_planes(op, X, k, Y, z0, z1)
+
+    def gram_sym(self, X, Y, k, r0, r1):
+        return self.core.gram_sym(self.ctx, X, Y, k, r0, r1)
+
+    def gram_rect(self, X, k1, Y, k2, r0, r1):
+        return self.core.gram_rect(self.ctx, X, k1, Y, k2, r0, r1)
+
+    def rotate(self, X, k1, Cm, ldc, k2, Z, r0, r1, mode):
+        self.core.rotate(self.ctx, X, k1, Cm, ldc, k2, Z, r0, r1, mode)
+
+    def kk(self, m):
+        return torch.empty(max(m, 1), dtype=torch.float64, device=self.device)
+
+    def ritz_ortho(self, G, K, drop_tol, C1):
+        return self.core.ritz_ortho(self.ctx, G, K, drop_tol, C1)
+
+    def ritz_second_pass(self, G2, k, C2, Bt):
+        return self.core.ritz_second_pass(self.ctx, G2, k, C2, Bt)
+
+    def ritz_pencil(self, GA, C2, Bt, GB, k, Y):
+        return self.core.ritz_pencil(self.ctx, GA, C2, Bt, GB, k, Y)
+
+    def gram_defect(self, G, k):
+        return self.core.gram_defect_of(self.ctx, G, k)
+
+    def sign_buffers(self, k):
+        return self.core.sign_buffers(self.ctx, k)
+
+    def colmax(self, V, k, r0, r1, amax):
+        self.core.colmax(self.ctx, V, k, r0, r1, amax)
+
+    def first_above(self, V, k, r0, r1, amax, first):
+        self.core.first_above(self.ctx, V, k, r0, r1, amax, first)
+
+    def sign_flags(self, V, k, r0, r1, amax, first, flip):
+        self.core.sign_flags(self.ctx, V, k, r0, r1, amax, first, flip)
+
+    def negate_columns(self, V, k, r0, r1, flip):
+        self.core.negate_columns(self.ctx, V, k, r0, r1, flip)
+
+    def copy_rows(self, src, dst, r0, r1):
+        dst[:, r0:r1].copy_(src[:, r0:r1])
+
+    def div_rows(self, src, d, dst, r0, r1):
+        torch.div(src[:, r0:r1], d, out=dst[:, r0:r1])  # x /= nb (linalg.cpp:431)
+
+    def to_host(self, t):
+        return t.cpu().tolist()
+
+    def density_rows(self, U, occ, r0, r1, rho):
+        return self.core.density_rows(self.ctx, U, occ, r0, r1, rho)
+
+    def density_normalize(self, total, rho):
+        return self.core.density_normalize(self.ctx, total, rho)
+
 
 @dataclass
 class Trace:
@@ -224,6 +378,14 @@ class ParoRun:
         self.half = backend.empty(K, n)
         self.orb = backend.empty(K, n)
         self._half_local = None
+        # Step 4 over row slabs of the lattice planes (one slab per rank)
+        self.slabs = RowSlab.all(backend.S, self.dist.world)
+        self.slab = self.slabs[self.dist.rank]
+        self.s4 = Step4(backend, self.dist, self.slab)
+        if estimate and self.dist.world > 1:
+            raise N.InvalidArgumentError("ParoRun: the Step-2 estimator needs every orbital row (world size 1)")
+        self._out = None         # step_host: (copy stream, host orbitals) filled after Step 4
+        self._hooked = False     # step_host: the copy-out was started inside Step 4
         # guess="baseline": the reference drivers' own start, initial_guess =
         # baseline eigenpairs of the core / linear operator (paro.cpp:278,
         # 499-505); otherwise the generator's guess columns, Ritz-projected
@@ -233,9 +395,10 @@ class ParoRun:
             cands = backend.from_host(g) if not torch.is_tensor(g) else g
 
         def start(a):
-            if baseline:
+            if baseline:  # replicated on every rank: all rows of every column
                 return backend.initial_guess(a, K, self.orb)
-            return backend.ritz(cands, a, K, w.drop_tol, self.orb)
+            orb, lam, d = self.s4.ritz(cands, a, backend.mass_op(), K, w.drop_tol, self.orb)
+            return orb, lam, d
 
         if w.kind == "ks":
             self.occ = [2.0] * (w.n_electrons // 2)
@@ -244,12 +407,14 @@ class ParoRun:
             a0 = backend.core_hamiltonian()
             # initial guess: V_H = V_xc = 0 linearisation (paro.cpp:499-505)
             orb, lam, _ = start(a0)
-            self.rho_in = backend.density(orb, self.occ, out=backend.empty(n))
+            self.rho_in = self._density(orb[: w.n_orbitals], backend.empty(n))
             self.rho_half = backend.empty(n)
             self.rho_out = backend.empty(n)
             self.vh = backend.empty(n)
         else:
             orb, lam, _ = start(backend.form)
+        if not baseline:
+            self.dist.slabs_to_cols(self.orb, self.dist.shard(orb.shape[0])[2], self.slabs)
         self.k = orb.shape[0]
         self.lambdas = lam
         self.clamped = 0
@@ -258,7 +423,6 @@ class ParoRun:
         self._fail_attempts = 0  # NotSpd attempts of the last Step 3 (the probe runs for that many)
         self._chunks = None      # step_host: (c0, c1, copy event) of the local Step-3 columns
         self._waited = set()     # step_host: ids of the chunk events the compute stream already waits on
-        self._out = None         # step_host: (copy stream, host orbitals) filled after Step 4
         self._copy_stream = None
         self.timeline = None     # profiling: list of (label, CUDA event) marks, or None
 
@@ -343,7 +507,7 @@ class ParoRun:
         # every chunk has landed before Step 4 writes the new orbitals into self.orb
         self._wait_chunks()
         all_iters = d.allgather_ints(iters, counts, self._idev())
-        d.allgather_columns(local, counts, self.half)
+        d.cols_to_slabs(local, counts, self.half, self.slabs)
         return sigma, all_iters
 
     def _probe(self, a, chunks, c0, c1, sigma, tol, attempt, local):
@@ -401,17 +565,45 @@ class ParoRun:
             return self._ks_step(it)
         return self._linear_step(it)
 
-    def _arm_copy_out(self):
-        """step_host: the library copies this rank's block of the new orbitals
-        to the host on the side stream as soon as Step 4 has them final
-        (before its Gram certificate)."""
-        if self._out is None or not hasattr(self.be, "ritz_copyout"):
-            return False
+    def _density(self, U, out):
+        """density_from_orbitals (model.cpp:192-223): the nodal sum on this
+        rank's slab rows, all-gathered, then normalised on the full density."""
+        be = self.be
+        total = be.density_rows(U, self.occ, self.slab.r0, self.slab.r1, out)
+        self.dist.allgather_rows(out, self.slabs)
+        be.density_normalize(total, out)
+        return out
+
+    def _final_hook(self):
+        """step_host at world size 1: Step 4 starts the host copy-out of the new
+        orbitals as soon as they are final (before its Gram certificate)."""
+        self._hooked = False
+        if self._out is None or self.dist.world > 1:
+            return None
         cs, h_orb = self._out
-        o0, o1, _ = self.dist.shard(self.k)
-        self._mark("d2h_armed", cs)
-        self.be.ritz_copyout(cs, h_orb, o0, o1)
-        return True
+        main = torch.cuda.current_stream(self.be.device)
+
+        def hook(V, k):
+            o0, o1, _ = self.dist.shard(k)
+            cs.wait_stream(main)
+            with torch.cuda.stream(cs):
+                self._mark("d2h_start", cs)
+                h_orb[o0:o1].copy_(V[o0:o1], non_blocking=True)
+                ev = cs.record_event()
+                self._mark("d2h_end", cs)
+            self._hooked = True
+            return lambda: main.wait_event(ev)
+
+        return hook
+
+    def _to_columns(self):
+        """Step 4's row slabs back to column shards for the next Step 3 (one
+        all-to-all), and step_host's copy-out of this rank's block if Step 4
+        did not start it."""
+        d = self.dist
+        d.slabs_to_cols(self.orb, d.shard(self.k)[2], self.slabs)
+        if self._out is not None and not self._hooked:
+            self._copy_out(self.orb[: self.k])
 
     def _copy_out(self, orb):
         """step_host: this rank's block of the new orbitals to the host (side stream)."""
@@ -499,21 +691,18 @@ class ParoRun:
         t_source = time.perf_counter() - ts
         tp = time.perf_counter()
         half = self.half[: self.k]
-        rho_half = be.density(half[:N_], self.occ, out=self.rho_half)
+        rho_half = self._density(half[:N_], self.rho_half)
         vh_half = be.hartree(rho_half, out=self.vh)
         a_half, cl = be.ks_form(rho_half, vh_half, "half")
         self.clamped += cl
-        armed = self._arm_copy_out()
-        orb, lam, defect = be.ritz(half, a_half, N_, w.drop_tol, self.orb)
+        orb, lam, defect = self.s4.ritz(half, a_half, be.mass_op(), N_, w.drop_tol, self.orb,
+                                        on_final=self._final_hook())
         self._mark("ritz_end")
-        if self._out is not None and not armed:  # step_host: the orbitals leave while the density work runs
-            self._copy_out(orb)
-        if self._out is not None and orb.shape[0] != self.k:
-            self._copy_out(orb)  # a dropped candidate changed the shard: copy the final block explicitly
+        self.k, self.lambdas = orb.shape[0], lam
+        self._to_columns()
         self._sync()
         t_project = time.perf_counter() - tp
-        self.k, self.lambdas = orb.shape[0], lam
-        rho_out = be.density(orb[:N_], self.occ, out=self.rho_out)
+        rho_out = self._density(orb[:N_], self.rho_out)
         vh_out = be.hartree(rho_out, out=self.vh)
         e_tot = be.energy(lam, self.occ, rho_out, vh_out)
         res = be.rho_residual(rho_out, self.rho_in)
@@ -536,12 +725,11 @@ class ParoRun:
         self._sync()
         t_source = time.perf_counter() - t0
         tp = time.perf_counter()
-        armed = self._arm_copy_out()
-        orb, lam, defect = be.ritz(self.half[: self.k], be.form, w.n_orbitals, w.drop_tol, self.orb)
-        if self._out is not None and (not armed or orb.shape[0] != self.k):
-            self._copy_out(orb)
-        self._sync()
+        orb, lam, defect = self.s4.ritz(self.half[: self.k], be.form, be.mass_op(), w.n_orbitals, w.drop_tol,
+                                        self.orb, on_final=self._final_hook())
         self.k, self.lambdas = orb.shape[0], lam
+        self._to_columns()
+        self._sync()
         return Trace(it + 1, lam[: w.n_orbitals], None, None, sigma, defect, iters, t_source,
                      time.perf_counter() - tp, time.perf_counter() - t0, eta, t_meshgen, be.n)
 
