@@ -172,6 +172,11 @@ int paro_dense_sym_geneig(paro_ctx* ctx, int m, const double* a, const double* b
 /* fix_sign (linalg.cpp:229-241) on k device columns. */
 int paro_fix_sign(paro_ctx* ctx, int k, double* v, long long ld);
 
+/* ---- run artifacts (runner.cpp:92-121): Mesh::dump (mesh.cpp:198-217) of the
+ * uniform Kuhn box mesh [lo, hi]^3 with `subdivisions` cells per axis, byte
+ * for byte the reference's mesh.txt; no GPU or context needed */
+int paro_mesh_dump(int subdivisions, double lo, double hi, const char* path);
+
 /* ---- Step 4 (rayleigh_ritz, paro.cpp:121-177) as building blocks on row
  * ranges [r0, r1) of column blocks: what a Step 4 sharded over row slabs
  * combines across ranks (Grams summed, fix_sign pieces by max / min / max).

@@ -13,9 +13,12 @@
 // (SURVEY.md §8c "Oracle harness contract"); paro.cpp is therefore left out of
 // the object list in the Makefile.
 #include "paro.cpp"  // NOLINT: unity build of the reference driver (proj/src/paro.cpp)
+#include "paro/runconfig.hpp"
+#include "paro/runner.hpp"
 
 #include <cstring>
 #include <exception>
+#include <fstream>
 #include <string>
 
 using namespace paro;
@@ -733,3 +736,52 @@ void ref_lin_state_get(void* sv, int which, double* out) {
 std::size_t ref_lin_state_k(void* s) { return static_cast<LinState*>(s)->orbitals.count(); }
 
 }  // extern "C"
+
+// ------------------------------------------------------------- run_experiment ----
+// The reference runner on a key = value config file (runconfig.cpp, runner.cpp),
+// writing trace.csv / eigenvalues.txt / mesh.txt / summary.txt into out_dir;
+// returns the exit code the reference CLI would (tools/main.cpp:46-67).
+extern "C" int ref_run_config(const char* config_path, const char* out_dir, int workers, char* summary, int cap) {
+  try {
+    RunConfig config = parse_run_config_file(config_path);
+    if (workers > 0) config.paro.workers = workers;
+    if (out_dir && *out_dir) config.out_dir = out_dir;
+    const RunArtifacts a = run_experiment(config);
+    if (summary && cap > 0) std::snprintf(summary, cap, "%s", a.summary.c_str());
+    return a.converged ? 0 : 1;
+  } catch (const ParseError& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const InvalidArgumentError& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const NotSpdError& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const IterationLimitError& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const CapacityError& e) {
+    g_err = e.what();
+    return 4;
+  } catch (const ScfDivergenceError& e) {
+    g_err = e.what();
+    return 5;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 6;
+  }
+}
+
+// Mesh::dump of the space's mesh (mesh.cpp:198-217)
+extern "C" int ref_space_dump(void* h, const char* path) {
+  try {
+    std::ofstream os(path, std::ios::binary);
+    static_cast<SpaceH*>(h)->space->mesh().dump(os);
+    return os ? 0 : 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+

@@ -92,6 +92,8 @@ def lib():
             "ref_space_free": (None, [_P]),
             "ref_space_dofs": (_SZ, [_P]),
             "ref_space_elements": (_SZ, [_P]),
+            "ref_space_dump": (C.c_int, [_P, C.c_char_p]),
+            "ref_run_config": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.c_char_p, C.c_int]),
             "ref_op_mass": (_P, [_P]),
             "ref_op_stiffness": (_P, [_P, _D]),
             "ref_op_wmass_coulomb": (_P, [_P, C.c_int, _DP, _DP, _D]),
@@ -145,7 +147,9 @@ def lib():
             "ref_lin_state_k": (_SZ, [_P]),
         }
         for name, (res, args) in sig.items():
-            f = getattr(L, name)
+            f = getattr(L, name, None)
+            if f is None:  # an older build of the harness: that entry point fails when called
+                continue
             f.restype = res
             f.argtypes = args
         _lib = L
@@ -535,6 +539,20 @@ class LinLoop:
         out = np.zeros((self.k, self.sp.n)) if idx == 0 else np.zeros(self.k)
         lib().ref_lin_state_get(self.h, idx, _dp(out))
         return out
+
+
+def space_dump(sp: "Space", path) -> None:
+    """Mesh::dump (mesh.cpp:198-217) of the space's mesh into `path`."""
+    if lib().ref_space_dump(sp.h, str(path).encode()) != 0:
+        raise RefError(lib().ref_last_error().decode())
+
+
+def run_config(config_path, out_dir, workers: int = 0):
+    """The reference runner (run_experiment, runner.cpp:67-121) on a config file:
+    returns (exit code as tools/main.cpp maps it, summary line, error text)."""
+    buf = C.create_string_buffer(512)
+    rc = lib().ref_run_config(str(config_path).encode(), str(out_dir).encode(), int(workers), buf, 512)
+    return rc, buf.value.decode(), (lib().ref_last_error() or b"").decode()
 
 
 def workers_default() -> int:

@@ -70,8 +70,21 @@ class CudaError(Error):
     code = 20
 
 
+class ScfDivergenceError(Error):
+    """paro::ScfDivergenceError (errors.hpp): raised by the run-level stop test, not the library."""
+
+    code = 30
+
+
+class ParseError(Error):
+    """paro::ParseError (errors.hpp): run configuration / molecule file syntax."""
+
+    code = 31
+
+
 ERRORS = {c.code: c for c in (Error, InvalidArgumentError, NotSpdError, IterationLimitError, DegenerateSpanError,
-                              PencilError, EmptyBasisError, CapacityError, LineageError, CudaError)}
+                              PencilError, EmptyBasisError, CapacityError, LineageError, CudaError,
+                              ScfDivergenceError, ParseError)}
 
 # name -> (restype, argtypes)
 SIGNATURES = {
@@ -111,6 +124,7 @@ SIGNATURES = {
     "paro_baseline_geneig": (_I, [_P, _P, _P, _I, _SZ, C.c_ulonglong, _DP, _P, _LL, C.POINTER(_I)]),
     "paro_b_orthonormalize": (_I, [_P, _P, _I, _P, _D, _P, C.POINTER(_I), C.POINTER(_I)]),
     "paro_fix_sign": (_I, [_P, _I, _P, _LL]),
+    "paro_mesh_dump": (_I, [_I, _D, _D, C.c_char_p]),
     "paro_op_apply_planes": (_I, [_P, _P, _I, _P, _LL, _P, _I, _I]),
     "paro_gram_sym": (_I, [_P, _I, _P, _LL, _P, _LL, _LL, _LL, _P]),
     "paro_gram_rect": (_I, [_P, _I, _P, _LL, _I, _P, _LL, _LL, _LL, _P]),

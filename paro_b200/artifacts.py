@@ -5,6 +5,10 @@ this driver can be diffed against `paro --config` output:
                    header iter,dofs,lambda_1..N[,e_tot],eta_total,t_meshgen,t_source,t_project;
                    values "%.12g", times "%.6f", missing values "nan"
   eigenvalues.txt  proj/src/runner.cpp:97-101   "<i> <lambda_i %.15g>" per line
+  mesh.txt         Mesh::dump proj/src/mesh.cpp:198-217 of the uniform Kuhn box
+                   mesh (C ABI paro_mesh_dump, streamed by the native library)
+  summary.txt      proj/src/runner.cpp:107-121  "<converged|failed>, <n> iterations,
+                   E_tot = %.12g | lambda_1 = %.12g, <dofs> DOFs"
 """
 from __future__ import annotations
 
@@ -45,9 +49,37 @@ def eigenvalues_txt(lambdas) -> str:
     return "".join(f"{i + 1} {_fmt(v, '%.15g')}\n" for i, v in enumerate(lambdas))
 
 
-def write_run(out_dir, traces, final_lambdas, n_lambdas: int, kohn_sham: bool) -> None:
-    """trace.csv + eigenvalues.txt under out_dir (run_experiment, runner.cpp:79-101)."""
+def summary_line(converged: bool, iterations: int, kohn_sham: bool, e_tot, lambda_1, dofs: int) -> str:
+    """run_experiment's summary (runner.cpp:107-116)."""
+    s = f"{'converged' if converged else 'failed'}, {iterations} iterations, "
+    s += f"E_tot = {_fmt(e_tot or 0.0)}" if kohn_sham else f"lambda_1 = {_fmt(lambda_1 or 0.0)}"
+    return s + f", {dofs} DOFs"
+
+
+def mesh_dump(path, subdivisions: int, lo: float, hi: float) -> None:
+    """mesh.txt: Mesh::dump of create_box_mesh([lo, hi]^3, subdivisions)."""
+    from . import _native as N
+
+    st = N.lib().paro_mesh_dump(int(subdivisions), float(lo), float(hi), str(path).encode())
+    if st != 0:
+        raise N.ERRORS.get(st, N.Error)((N.lib().paro_ctx_last_error(None) or b"").decode())
+
+
+def write_run(out_dir, traces, final_lambdas, n_lambdas: int, kohn_sham: bool, *, converged: bool | None = None,
+              mesh=None) -> str | None:
+    """The run_experiment artifacts (runner.cpp:79-121) under out_dir:
+    trace.csv + eigenvalues.txt, and with mesh = (subdivisions, lo, hi)
+    mesh.txt, with `converged` given summary.txt. Returns the summary line."""
     d = Path(out_dir)
     d.mkdir(parents=True, exist_ok=True)
     (d / "trace.csv").write_text(trace_csv(traces, n_lambdas, kohn_sham))
     (d / "eigenvalues.txt").write_text(eigenvalues_txt(final_lambdas))
+    if mesh is not None:
+        mesh_dump(d / "mesh.txt", *mesh)
+    if converged is None:
+        return None
+    last = traces[-1] if traces else None
+    line = summary_line(converged, len(traces), kohn_sham, last.e_tot if last else None,
+                        final_lambdas[0] if len(final_lambdas) else None, last.dofs if last else 0)
+    (d / "summary.txt").write_text(line + "\n")
+    return line

@@ -68,6 +68,9 @@ class Workload:
     cg_max_iter: int = 100000
     mixing_alpha: float = 0.3
     drop_tol: float = 1e-8
+    tol_energy: float = 1e-6       # ParoConfig::tol_energy (paro.hpp:39): the stop tests' threshold
+    tol_estimator: float = 0.0     # ParoConfig::tol_estimator: 0 disables the estimator stop test
+    diffusion: float = 0.5         # linear: the stiffness scale (1 for laplace-cube)
 
     @property
     def K(self) -> int:

@@ -1,11 +1,12 @@
 // C ABI (include/paro_b200.h) over the device implementation.
 #include "paro_b200.h"
 
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "ctx.hpp"
@@ -70,8 +71,6 @@ int paro_ctx_create(int device, void* stream, paro_ctx** out) {
     ctx->c.device = device;
     PARO_CUDA(cudaSetDevice(device));
     ctx->c.stream = static_cast<cudaStream_t>(stream);
-    if (cublasCreate(&ctx->c.cublas) != CUBLAS_STATUS_SUCCESS) throw ParoError(kCuda, "cublasCreate failed");
-    cublasSetStream(ctx->c.cublas, ctx->c.stream);
     PARO_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->c.pinned_count), sizeof(int), cudaHostAllocMapped));
     PARO_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->c.pinned_count_dev), ctx->c.pinned_count, 0));
     *out = ctx;
@@ -88,7 +87,6 @@ int paro_ctx_destroy(paro_ctx* ctx) {
                     &ctx->c.ws_small, &ctx->c.ws_small2, &ctx->c.dst_tab, &ctx->c.wtab, &ctx->c.shifted, &ctx->c.coefp, &ctx->c.csr_ws, &ctx->c.csr_ws2, &ctx->c.csr_io, &ctx->c.pcg_x, &ctx->c.ws_gram,
                     &ctx->c.ws_small3})
     b->release();
-  if (ctx->c.cublas) cublasDestroy(ctx->c.cublas);
   if (ctx->c.pinned_count) cudaFreeHost(ctx->c.pinned_count);
   paro_b200::xfer_release(ctx->c);
   delete ctx;
@@ -98,7 +96,6 @@ int paro_ctx_destroy(paro_ctx* ctx) {
 int paro_ctx_set_stream(paro_ctx* ctx, void* stream) {
   return guarded(ctx, [&] {
     ctx->c.stream = static_cast<cudaStream_t>(stream);
-    cublasSetStream(ctx->c.cublas, ctx->c.stream);
     return kOk;
   });
 }
@@ -743,6 +740,81 @@ int paro_total_energy(paro_ctx* ctx, int n_lambdas, const double* lambdas, int n
 int paro_fix_sign(paro_ctx* ctx, int k, double* v, long long ld) {
   return guarded(ctx, [&] {
     fix_sign_columns(ctx->c, v, ld, k);
+    return kOk;
+  });
+}
+
+// ------------------------------------------------ run artifacts
+// Mesh::dump (mesh.cpp:198-217) of the uniform Kuhn box mesh create_box_mesh
+// builds (mesh.cpp:411-478): "3 nv ne", vertices "%.17g %.17g %.17g" in vertex
+// id order (k(s+1)+j)(s+1)+i, then one line per tetrahedron in the reference's
+// element order: four vertex ids, the refinement-edge index 2 and type 0.
+int paro_mesh_dump(int subdivisions, double lo, double hi, const char* path) {
+  return guarded(nullptr, [&] {
+    const int n = subdivisions;
+    if (n < 1) throw ParoError(kInvalidArgument, "create_box_mesh: subdivisions must be >= 1");
+    if (!(hi - lo > 0.0)) throw ParoError(kInvalidArgument, "create_box_mesh: box has non-positive edge length");
+    FILE* f = std::fopen(path, "wb");
+    if (!f) throw ParoError(kInvalidArgument, std::string("mesh dump: cannot open ") + path);
+    std::vector<char> buf(1 << 22);
+    size_t used = 0;
+    auto flush = [&] {
+      if (used && std::fwrite(buf.data(), 1, used, f) != used) {
+        std::fclose(f);
+        throw ParoError(kError, "mesh dump: write failed");
+      }
+      used = 0;
+    };
+    auto put = [&](const char* p, size_t len) {
+      if (used + len > buf.size()) flush();
+      std::memcpy(buf.data() + used, p, len);
+      used += len;
+    };
+    const long long nv = static_cast<long long>(n + 1) * (n + 1) * (n + 1);
+    const long long ne = 6LL * n * n * n;
+    char line[160];
+    put(line, static_cast<size_t>(std::snprintf(line, sizeof line, "3 %lld %lld\n", nv, ne)));
+    std::vector<std::string> c(n + 1);
+    for (int i = 0; i <= n; ++i) {
+      std::snprintf(line, sizeof line, "%.17g", lo + (hi - lo) * i / n);
+      c[i] = line;
+    }
+    for (int k = 0; k <= n; ++k)
+      for (int j = 0; j <= n; ++j)
+        for (int i = 0; i <= n; ++i) {
+          const std::string l = c[i] + ' ' + c[j] + ' ' + c[k] + '\n';
+          put(l.data(), l.size());
+        }
+    auto vid = [&](int i, int j, int k) {
+      return static_cast<unsigned>((k * (n + 1) + j) * (n + 1) + i);
+    };
+    auto utoa = [](unsigned v, char* out) {
+      char tmp[12];
+      int len = 0;
+      do {
+        tmp[len++] = static_cast<char>('0' + v % 10);
+        v /= 10;
+      } while (v);
+      for (int q = 0; q < len; ++q) out[q] = tmp[len - 1 - q];
+      return len;
+    };
+    constexpr int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    for (int k = 0; k < n; ++k)
+      for (int j = 0; j < n; ++j)
+        for (int i = 0; i < n; ++i)
+          for (const auto& perm : perms) {
+            int cc[3] = {i, j, k};
+            int len = utoa(vid(cc[0], cc[1], cc[2]), line);
+            for (int step = 0; step < 3; ++step) {
+              cc[perm[step]] += 1;
+              line[len++] = ' ';
+              len += utoa(vid(cc[0], cc[1], cc[2]), line + len);
+            }
+            std::memcpy(line + len, " 2 0\n", 5);
+            put(line, static_cast<size_t>(len + 5));
+          }
+    flush();
+    if (std::fclose(f) != 0) throw ParoError(kError, "mesh dump: close failed");
     return kOk;
   });
 }

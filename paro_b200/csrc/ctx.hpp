@@ -1,7 +1,6 @@
 // Host-side context: device, stream, grid, operators and grow-only workspace.
 #pragma once
 
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <string>
@@ -50,7 +49,6 @@ constexpr int kXferSlots = 32;
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cublasHandle_t cublas = nullptr;
   Grid grid;
   bool grid_set = false;
   std::string err;

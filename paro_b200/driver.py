@@ -207,10 +207,11 @@ class GpuBackend:
             self.forms = {"in": c.Operator.variable_empty(self.ctx), "half": c.Operator.variable_empty(self.ctx)}
             self.scratch = self.ctx.empty(self.n)
         else:
-            a = c.assemble_stiffness(self.ctx, 0.5)
+            # LinearProblem::elliptic / potential_well (runner.cpp:30-47): diffusion stiffness + reaction mass
+            a = c.assemble_stiffness(self.ctx, workload.diffusion)
             if workload.potential == "harmonic":
                 c.add_scaled(a, c.assemble_harmonic(self.ctx, 0.5))
-            else:
+            elif workload.potential != "none":
                 c.add_scaled(a, c.assemble_vext(self.ctx, workload.charges, workload.positions, workload.eps))
             self.form = a
 
@@ -242,7 +243,7 @@ class GpuBackend:
 
     def initial_guess(self, a, count, out):
         """initial_guess (paro.cpp:63-79) on the device: baseline eigenpairs of a."""
-        og = self.core.initial_guess(a, self.mass, count)
+        og = self.core.initial_guess(a, self.mass, count, seed=self.w.seed)
         out[:count].copy_(og.orbitals)
         return out[:count], list(og.lambdas), og.gram_defect
 
@@ -272,10 +273,11 @@ class GpuBackend:
         if w.kind == "ks":
             return self.core.estimate_eta(self.ctx, U, lambdas, reaction="ks", charges=w.charges,
                                           positions=w.positions, eps=w.eps, rho=rho, vh=vh)
-        if w.potential == "harmonic":
-            return self.core.estimate_eta(self.ctx, U, lambdas, reaction="harmonic", c=0.5)
-        return self.core.estimate_eta(self.ctx, U, lambdas, reaction="well", charges=w.charges,
-                                      positions=w.positions, eps=w.eps)
+        if w.potential in ("harmonic", "none"):
+            return self.core.estimate_eta(self.ctx, U, lambdas, diffusion=w.diffusion, reaction="harmonic",
+                                          c=0.5 if w.potential == "harmonic" else 0.0)
+        return self.core.estimate_eta(self.ctx, U, lambdas, diffusion=w.diffusion, reaction="well",
+                                      charges=w.charges, positions=w.positions, eps=w.eps)
 
     def launches(self) -> int:
         return self.ctx.launches()
@@ -361,6 +363,53 @@ class Trace:
     eta_total: float | None = None   # Step 2 (estimate=True): combine_max(estimate_eigen_residual).total()
     t_meshgen: float = 0.0           # Step 2 wall time (the reference's t_meshgen column)
     dofs: int = 0
+    # what the reference driver's stop tests decide after this iteration
+    # (fixed mesh: mesh_frozen = true), logged while the harness runs on:
+    stable_count: int = 0            # KS: |dE| < tol_energy streak (paro.cpp:624); linear: lambdas_stable (:358-362)
+    increase_count: int = 0          # KS: rising energy with a stalled density residual (paro.cpp:615-617)
+    converged: bool = False          # the reference would stop here, converged (paro.cpp:632-635 / :365-369)
+    diverged: bool = False           # the reference would throw ScfDivergenceError here (paro.cpp:618-622)
+
+
+class StopTests:
+    """The reference drivers' convergence control on a fixed mesh, evaluated
+    on the harness's trace rows without changing the run:
+      Kohn-Sham  paro.cpp:605-635  energy-stability streak >= 3 converges;
+                 5 consecutive energy rises without density-residual progress
+                 is an SCF divergence;
+      linear     paro.cpp:358-369  lambdas_stable (:240-246) streak >= 2, or
+                 eta_total <= tol_estimator when that test is enabled."""
+
+    def __init__(self, w: Workload):
+        self.w = w
+        self.stable = 0
+        self.increase = 0
+        self.e_prev = None
+        self.res_prev = None
+        self.lam_prev = None
+
+    def update(self, tr: "Trace") -> "Trace":
+        w = self.w
+        if w.kind == "ks":
+            if self.e_prev is not None:
+                rising = tr.e_tot > self.e_prev + 1e-14
+                stalled = tr.rho_residual >= self.res_prev * (1.0 - 1e-12)
+                self.increase = self.increase + 1 if (rising and stalled) else 0
+                tr.diverged = self.increase >= 5
+                self.stable = self.stable + 1 if abs(tr.e_tot - self.e_prev) < w.tol_energy else 0
+            self.res_prev, self.e_prev = tr.rho_residual, tr.e_tot
+            tr.converged = self.stable >= 3 and not tr.diverged
+        else:
+            lam = list(tr.lambdas)
+            prev = self.lam_prev
+            stable = prev is not None and len(prev) == len(lam) and all(
+                abs(a - b) <= w.tol_energy * (1.0 + abs(a)) for a, b in zip(lam, prev))
+            self.stable = self.stable + 1 if stable else 0
+            self.lam_prev = lam
+            est_ok = w.tol_estimator > 0.0 and tr.eta_total is not None and tr.eta_total <= w.tol_estimator
+            tr.converged = self.stable >= 2 or est_ok
+        tr.stable_count, tr.increase_count = self.stable, self.increase
+        return tr
 
 
 class ParoRun:
@@ -421,6 +470,7 @@ class ParoRun:
         self._notspd_probe = []  # orbitals that met NotSpd in the last failing Step-3 attempt
         self.probe_hits = 0      # Step-3 attempts decided by the probe alone
         self._fail_attempts = 0  # NotSpd attempts of the last Step 3 (the probe runs for that many)
+        self.stops = StopTests(w)  # the reference's stop decisions, logged per Trace row
         self._chunks = None      # step_host: (c0, c1, copy event) of the local Step-3 columns
         self._waited = set()     # step_host: ids of the chunk events the compute stream already waits on
         self._copy_stream = None
@@ -561,9 +611,8 @@ class ParoRun:
         return torch.device("cpu")
 
     def step(self, it: int) -> Trace:
-        if self.w.kind == "ks":
-            return self._ks_step(it)
-        return self._linear_step(it)
+        tr = self._ks_step(it) if self.w.kind == "ks" else self._linear_step(it)
+        return self.stops.update(tr)
 
     def _density(self, U, out):
         """density_from_orbitals (model.cpp:192-223): the nodal sum on this
@@ -733,5 +782,19 @@ class ParoRun:
         return Trace(it + 1, lam[: w.n_orbitals], None, None, sigma, defect, iters, t_source,
                      time.perf_counter() - tp, time.perf_counter() - t0, eta, t_meshgen, be.n)
 
-    def run(self, iterations: int | None = None):
-        return [self.step(i) for i in range(iterations if iterations is not None else self.w.iterations)]
+    def run(self, iterations: int | None = None, stop: bool = False):
+        """`iterations` outer iterations (default: the workload's count). With
+        stop=True the reference's own control applies (max_outer = iterations):
+        return at the first converged row, raise ScfDivergenceError at a
+        divergent one (paro.cpp:618-635)."""
+        out = []
+        for i in range(iterations if iterations is not None else self.w.iterations):
+            tr = self.step(i)
+            out.append(tr)
+            if stop and tr.diverged:
+                raise N.ScfDivergenceError(
+                    "kohn-sham: total energy increased for 5 consecutive iterations without density-residual "
+                    "progress; consider a smaller mixing_alpha")
+            if stop and tr.converged:
+                break
+        return out

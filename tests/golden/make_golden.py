@@ -81,12 +81,12 @@ def stencils():
 # 40), and configs[2..4] on 65^3 meshes of the same generators (SURVEY 8d:
 # "run configs 4 and 5 scaled down (same generators at s = 64) fully on both
 # sides").  python tests/golden/make_golden.py full
+# The Kohn-Sham configs at these sizes (h2, water@s64, cluster32@s64, and
+# water at its full 129^3) have traces with stored reference densities:
+# tests/golden/make_golden_big.py.
 FULL = {
-    "h2": ("ks", 20),
     "oscillator": ("linear", 40),
-    "water@s64": ("ks", 6),
     "source64@s64": ("linear", 1),
-    "cluster32@s64": ("ks", 3),
 }
 
 

@@ -68,10 +68,29 @@ def run(name: str, workers: int):
     return fx
 
 
+SKETCH_ROWS = 32
+SKETCH_SEED = 20261020
+
+
+def sketch_matrix(n: int) -> np.ndarray:
+    """[SKETCH_ROWS, n] uniform[-1, 1) rows (configs.SplitMix64, seeded): for a
+    difference d, mean((S d)^2) * 3 estimates ||d||_2^2 (E s^2 = 1/3)."""
+    rng = configs.SplitMix64(SKETCH_SEED)
+    return rng.sym_array(SKETCH_ROWS * n).reshape(SKETCH_ROWS, n)
+
+
 def pack(name: str, keep):
-    """Commit step: the trace json plus the rho vectors of iterations `keep`."""
+    """Commit step: the trace json (plus a 32-row sketch of every iteration's
+    rho_out) and the full rho vectors of iterations `keep`."""
     tag = name.replace("@", "_")
     fx = json.loads((SCRATCH / f"big_{tag}.json").read_text())
+    n = configs.get(name).n
+    S = sketch_matrix(n)
+    for row in fx["trace"]:
+        rho = np.load(SCRATCH / f"{tag}_rho_{row['iter']:02d}.npy")
+        row["rho_sketch"] = (S @ rho).tolist()
+    fx["rho_vectors"] = list(keep)
+    fx["sketch"] = {"rows": SKETCH_ROWS, "seed": SKETCH_SEED, "dist": "uniform[-1,1) SplitMix64"}
     (OUT / f"big_{tag}.json").write_text(json.dumps(fx, indent=1))
     arrs = {f"it{k:02d}": shuffle(np.load(SCRATCH / f"{tag}_rho_{k:02d}.npy")) for k in keep}
     np.savez_compressed(OUT / f"big_{tag}_rho.npz", **arrs)

@@ -1,9 +1,11 @@
 """GPU runs of the BASELINE generators (scaled meshes) against the committed
 golden fixtures produced by the compiled reference (tests/golden/make_golden.py).
-North-star tolerances: eigenvalues 1e-8 relative (with a 1e-10 Ha absolute
-floor for eigenvalues near zero, a hundredth of the energy bar), energy
-1e-8 Ha; the density is compared through its size-independent checksums
-(integral, L2 norm)."""
+North-star tolerances: eigenvalues 1e-8 relative (for |lambda| < 1e-2 a 1e-10 Ha
+absolute floor, a hundredth of the energy bar, replaces it), energy 1e-8 Ha.
+These fixtures carry only the density's checksums (integral, L2 norm, the
+residual ||rho_out - rho_in||); the density difference itself is bounded in
+test_gpu_driver.py (live reference, small meshes) and test_gpu_golden_big.py
+(stored reference vectors and sketches at the config sizes)."""
 import json
 from pathlib import Path
 
@@ -12,6 +14,13 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+def check_lambdas(got, ref):
+    got, ref = np.asarray(got), np.asarray(ref)
+    small = np.abs(ref) < 1e-2
+    np.testing.assert_allclose(got[~small], ref[~small], rtol=1e-8, atol=0)
+    np.testing.assert_allclose(got[small], ref[small], rtol=0, atol=1e-10)
 
 
 @pytest.mark.parametrize("name", ["h2_s16", "water_s24", "cluster32_s24", "oscillator_s16", "source64_s24"])
@@ -25,7 +34,7 @@ def test_gpu_matches_golden_trace(name):
     np.testing.assert_allclose(run.lambdas[: len(fx["lambdas0"])], fx["lambdas0"], rtol=1e-10)
     for row in fx["trace"]:
         tr = run.step(row["iter"] - 1)
-        np.testing.assert_allclose(tr.lambdas, row["lambdas"], rtol=1e-8, atol=1e-10)
+        check_lambdas(tr.lambdas, row["lambdas"])
         assert tr.sigma == pytest.approx(row["sigma"], rel=1e-12, abs=1e-14)
         if "e_tot" in row:
             assert abs(tr.e_tot - row["e_tot"]) <= 1e-8
@@ -35,12 +44,13 @@ def test_gpu_matches_golden_trace(name):
             assert abs(tr.rho_residual - row["rho_residual"]) <= 1e-7
 
 
+# the Kohn-Sham configs at full size have stored reference densities (big_*.json)
 FULL = sorted(p.stem for p in GOLDEN.glob("full_*.json"))
 
 
 @pytest.mark.parametrize("name", FULL)
 def test_gpu_matches_golden_trace_full_size(name):
-    """BASELINE configs[0] and [1] at their full sizes and iteration counts
-    (H2 33^3 x 20, oscillator 65^3 x 40), configs[2..4] on 65^3 meshes of the
-    same generators (tests/golden/make_golden.py full)."""
+    """BASELINE configs[1] at its full size and iteration count (oscillator
+    65^3 x 40) and configs[3]'s generator on a 65^3 mesh (source64, noise
+    start: the Gram-Schmidt path of Step 4); tests/golden/make_golden.py full."""
     test_gpu_matches_golden_trace(name)

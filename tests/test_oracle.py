@@ -209,3 +209,35 @@ def test_port_estimator_matches_reference(ref):
     tot_r = ref.lin_eta_total(sp, U, lam, 0.5, "harmonic", c=0.5)
     tot_p, _ = port.estimate_eta(U, lam, s, lo, hi, harm)
     assert abs(tot_p - tot_r) <= 1e-10 * tot_r
+
+
+def test_big_golden_fixtures_are_consistent():
+    """The committed config-size rho vectors reproduce their trace's checksums
+    (integral, L2 norm) and sketches, so the GPU parity test compares against
+    what the reference produced (tests/golden/make_golden_big.py)."""
+    import json
+    import sys
+    from pathlib import Path
+
+    import numpy as np
+
+    from oracle import port as P
+    from paro_b200 import configs
+
+    gold = Path(__file__).resolve().parent / "golden"
+    sys.path.insert(0, str(gold))
+    from make_golden_big import sketch_matrix, unshuffle
+
+    for js in sorted(gold.glob("big_*.json")):
+        fx = json.loads(js.read_text())
+        w = configs.get(fx["workload"])
+        vecs = np.load(js.with_name(js.stem + "_rho.npz"))
+        S = sketch_matrix(w.n)
+        rows = {r["iter"]: r for r in fx["trace"]}
+        assert len(rows) == w.iterations
+        for key in vecs.files:
+            rho = unshuffle(vecs[key])
+            r = rows[int(key[2:])]
+            assert P.integrate(rho, w.subdivisions, w.lo, w.hi) == pytest.approx(r["rho_integral"], rel=1e-12)
+            assert P.norm_l2(rho, w.subdivisions, w.lo, w.hi) == pytest.approx(r["rho_l2"], rel=1e-12)
+            np.testing.assert_allclose(S @ rho, r["rho_sketch"], rtol=1e-12, atol=1e-12)
