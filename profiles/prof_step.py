@@ -52,7 +52,7 @@ def main():
     torch.cuda.synchronize()
     torch.cuda.nvtx.range_push("prof")
     if a.phase == "ritz":
-        run.be.ritz(half, a_half, w.n_orbitals, w.drop_tol, run.orb)
+        run.s4.ritz(half, a_half, run.be.mass, w.n_orbitals, w.drop_tol, run.orb)
     else:
         run.step(1)
     torch.cuda.synchronize()
