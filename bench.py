@@ -117,6 +117,13 @@ def cpu_sample_rate(workload: str, sample_s: int, steps: int = 1, workers: int |
     return times, factor, workers, w
 
 
+def ref_sample_subdivisions(full, override: int = 0) -> int:
+    """The reduced mesh both CPU legs time the reference on (the reference
+    cannot build the 257^3 Kuhn mesh in the host RAM budget: its face map
+    alone is ~4e8 std::map entries); full size below 128 subdivisions."""
+    return override or (48 if full.subdivisions >= 128 else full.subdivisions)
+
+
 def run_reference(args):
     """--impl reference: the reference's CPU implementation on the host cores."""
     rank = int(os.environ.get("RANK", "0"))
@@ -125,7 +132,7 @@ def run_reference(args):
     from paro_b200 import configs
 
     full = configs.get(args.workload)
-    s = args.ref_sample or (48 if full.subdivisions >= 128 else full.subdivisions)
+    s = ref_sample_subdivisions(full, args.ref_sample)
     times, factor, workers, w = cpu_sample_rate(args.workload, s, steps=args.warmup + args.steps)
     timed = times[args.warmup:] or times
     per = sum(timed) / len(timed)
@@ -287,11 +294,17 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            s = 24 if w.subdivisions >= 128 else max(8, w.subdivisions // 2)
-            times, factor, workers, ws = cpu_sample_rate(args.workload, s, steps=1)
-            cpu = {"value": 1.0 / (times[0] * factor), "unit": UNIT, "cores": workers, "kind": "reference",
-                   "sample": f"{ws.name}: 1 full reference outer iteration in {times[0]:.2f} s on {workers} threads, "
-                             f"extrapolated x{factor:.1f} to {w.name} (DOF ratio x 1/h growth of CG iterations)"}
+            # the --impl reference leg's sample and model, bounded: the reference
+            # runs outer iterations 0 .. W on the reduced mesh and iteration W
+            # (the first timed index of this run) is the sample
+            s = ref_sample_subdivisions(w, args.ref_sample)
+            times, factor, workers, ws = cpu_sample_rate(args.workload, s, steps=args.warmup + 1)
+            per = times[-1]
+            cpu = {"value": 1.0 / (per * factor), "unit": UNIT, "cores": workers, "kind": "reference",
+                   "sample": f"{ws.name}: reference outer iteration {args.warmup} in {per:.2f} s on {workers} threads "
+                             f"(after {args.warmup} untimed), extrapolated x{factor:.1f} to {w.name} (DOF ratio x "
+                             f"mesh-refinement growth of the CG iteration count); same sample and model as "
+                             f"--impl reference"}
         except Exception as exc:  # the oracle build is test/baseline infrastructure only
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {exc}"}
 

@@ -81,6 +81,11 @@ int paro_malloc(paro_ctx* ctx, size_t bytes, void** dev);
 int paro_free(paro_ctx* ctx, void* dev);
 int paro_memcpy_h2d(paro_ctx* ctx, void* dev, const void* host, size_t bytes);
 int paro_memcpy_d2h(paro_ctx* ctx, void* host, const void* dev, size_t bytes);
+/* k host vectors of n doubles (e.g. the reference's std::vector columns) <->
+ * a device block [k][ld], through a pinned double-buffered staging ring
+ * (host copies overlap the DMA); synchronous on return */
+int paro_upload_columns(paro_ctx* ctx, int k, const double* const* host, size_t n, double* dev, long long ld);
+int paro_download_columns(paro_ctx* ctx, int k, const double* dev, long long ld, size_t n, double* const* host);
 
 /* Uniform box mesh [lo,hi]^3 with `subdivisions` cells per axis
  * (create_box_mesh + FeSpace::create, mesh.cpp:411-478, fem.cpp:13-30). */

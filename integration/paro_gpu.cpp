@@ -2,9 +2,18 @@
 // Host vectors in, host vectors out (the drop-in contract); each call moves its
 // operands to the device, runs the sm_100a kernels and maps the status code
 // back to the reference's exception type. See paro_gpu.hpp / INTEGRATION.md.
+//
+// Operators are converted once: the device form of a SparseOperator (the
+// stencil operator of the bound lattice, or the general CSR form for adapted
+// meshes) is cached per operator, keyed by its value array, dimension, nnz and
+// a signature of 4096 sampled values, so the mass / stiffness / KS form of a
+// call sequence cross the PCIe bus once (at 257^3 a KS form is 3 GB of CSR).
+// Orbital blocks move through the library's pinned staging ring
+// (paro_upload_columns / paro_download_columns).
 #include "paro_gpu.hpp"
 
 #include <cmath>
+#include <cstdint>
 #include <cstring>
 #include <string>
 
@@ -23,6 +32,25 @@ struct State {
   std::uint64_t mesh_id = 0;
 };
 thread_local State g;
+
+struct CachedOp {
+  const double* vals = nullptr;
+  std::size_t n = 0, nnz = 0;
+  std::uint64_t sig = 0;
+  bool lattice = false;
+  paro_op* op = nullptr;   // stencil form (lattice operators)
+  paro_csr* csr = nullptr; // general CSR form (adapted meshes)
+  std::uint64_t used = 0;
+};
+constexpr std::size_t kCacheSize = 8;
+thread_local std::vector<CachedOp> g_cache;
+thread_local std::uint64_t g_tick = 0;
+
+void drop(CachedOp& c) {
+  if (c.op) paro_op_destroy(c.op);
+  if (c.csr) paro_csr_destroy(c.csr);
+  c = CachedOp{};
+}
 
 [[noreturn]] void rethrow(int st) {
   const std::string msg = paro_ctx_last_error(g.ctx);
@@ -64,32 +92,71 @@ struct DevVec {
   }
 };
 
-struct DevOp {
-  paro_op* op = nullptr;
-  explicit DevOp(const SparseOperator& a) {
-    check(paro_op_from_csr(g.ctx, a.dimension(), a.row_offsets().data(), a.col_indices().data(), a.values().data(),
-                           &op));
+std::uint64_t signature(const SparseOperator& a) {
+  const auto& v = a.values();
+  std::uint64_t h = 1469598103934665603ull ^ v.size();
+  const std::size_t step = std::max<std::size_t>(1, v.size() / 4096);
+  for (std::size_t i = 0; i < v.size(); i += step) {
+    std::uint64_t bits;
+    std::memcpy(&bits, &v[i], sizeof bits);
+    h = (h ^ bits) * 1099511628211ull;
   }
-  ~DevOp() {
-    if (op) paro_op_destroy(op);
+  if (!v.empty()) {
+    std::uint64_t bits;
+    std::memcpy(&bits, &v.back(), sizeof bits);
+    h = (h ^ bits) * 1099511628211ull;
   }
-  DevOp(const DevOp&) = delete;
-  DevOp& operator=(const DevOp&) = delete;
-};
+  return h;
+}
 
-// general CSR operator on the device (adapted meshes)
-struct DevCsr {
-  paro_csr* op = nullptr;
-  explicit DevCsr(const SparseOperator& a) {
+void ensure_ctx();
+
+// the cached device form of `a` (converted on first use; LRU of kCacheSize)
+CachedOp& device_op(const SparseOperator& a) {
+  ensure_ctx();
+  const std::uint64_t sig = signature(a);
+  for (auto& c : g_cache)
+    if (c.vals == a.values().data() && c.n == a.dimension() && c.nnz == a.values().size() && c.sig == sig) {
+      c.used = ++g_tick;
+      return c;
+    }
+  if (g_cache.size() >= kCacheSize) {
+    auto lru = std::min_element(g_cache.begin(), g_cache.end(),
+                                [](const CachedOp& x, const CachedOp& y) { return x.used < y.used; });
+    drop(*lru);
+    g_cache.erase(lru);
+  }
+  CachedOp c;
+  c.vals = a.values().data();
+  c.n = a.dimension();
+  c.nnz = a.values().size();
+  c.sig = sig;
+  c.used = ++g_tick;
+  // the stencil form exists for operators of the bound lattice with the P1/Kuhn pattern
+  if (g.n == a.dimension()) {
+    const int st = paro_op_from_csr(g.ctx, a.dimension(), a.row_offsets().data(), a.col_indices().data(),
+                                    a.values().data(), &c.op);
+    if (st != PARO_OK && st != PARO_INVALID_ARGUMENT) check(st);
+    c.lattice = st == PARO_OK;
+  }
+  g_cache.push_back(c);
+  return g_cache.back();
+}
+
+paro_op* lattice_op(const SparseOperator& a) {
+  CachedOp& c = device_op(a);
+  if (!c.lattice)
+    throw InvalidArgumentError("paro::gpu: operator is not a P1/Kuhn stencil of the bound grid");
+  return c.op;
+}
+
+paro_csr* csr_op(const SparseOperator& a) {
+  CachedOp& c = device_op(a);
+  if (!c.csr)
     check(paro_csr_create(g.ctx, a.dimension(), a.row_offsets().data(), a.col_indices().data(), a.values().data(),
-                          &op));
-  }
-  ~DevCsr() {
-    if (op) paro_csr_destroy(op);
-  }
-  DevCsr(const DevCsr&) = delete;
-  DevCsr& operator=(const DevCsr&) = delete;
-};
+                          &c.csr));
+  return c.csr;
+}
 
 void ensure_ctx() {
   if (!g.ctx && paro_ctx_create(0, nullptr, &g.ctx) != PARO_OK) throw Error(paro_ctx_last_error(nullptr));
@@ -98,16 +165,7 @@ void ensure_ctx() {
 // The stencil kernels serve operators of the bound uniform lattice whose
 // pattern is the P1/Kuhn stencil; everything else (adapted meshes) takes the
 // general CSR kernels.
-bool on_lattice(const SparseOperator& a) {
-  if (!g.ctx || g.n != a.dimension()) return false;
-  paro_op* op = nullptr;
-  const int st = paro_op_from_csr(g.ctx, a.dimension(), a.row_offsets().data(), a.col_indices().data(),
-                                  a.values().data(), &op);
-  if (op) paro_op_destroy(op);
-  if (st == PARO_INVALID_ARGUMENT) return false;
-  check(st);
-  return true;
-}
+bool on_lattice(const SparseOperator& a) { return g.ctx && device_op(a).lattice; }
 
 void need(std::size_t n) {
   if (!g.ctx || g.n != n)
@@ -117,16 +175,20 @@ void need(std::size_t n) {
 
 DevVec pack(const std::vector<std::vector<double>>& cols, std::size_t n) {
   DevVec d(cols.empty() ? 1 : cols.size() * n);
+  std::vector<const double*> ptr(cols.size());
   for (std::size_t c = 0; c < cols.size(); ++c) {
     if (cols[c].size() != n) throw InvalidArgumentError("paro::gpu: vector dimension mismatch");
-    d.up(cols[c].data(), n, c * n);
+    ptr[c] = cols[c].data();
   }
+  check(paro_upload_columns(g.ctx, static_cast<int>(cols.size()), ptr.data(), n, d.p, static_cast<long long>(n)));
   return d;
 }
 
 std::vector<std::vector<double>> unpack(const DevVec& d, std::size_t k, std::size_t n) {
   std::vector<std::vector<double>> out(k, std::vector<double>(n));
-  for (std::size_t c = 0; c < k; ++c) d.down(out[c].data(), n, c * n);
+  std::vector<double*> ptr(k);
+  for (std::size_t c = 0; c < k; ++c) ptr[c] = out[c].data();
+  check(paro_download_columns(g.ctx, static_cast<int>(k), d.p, static_cast<long long>(n), n, ptr.data()));
   return out;
 }
 
@@ -146,6 +208,7 @@ void bind(const FeSpace& space, int device) {
   if (!g.ctx) {
     if (paro_ctx_create(device, nullptr, &g.ctx) != PARO_OK) throw Error(paro_ctx_last_error(nullptr));
   }
+  invalidate();  // stencil forms belong to the previous grid
   check(paro_grid_init(g.ctx, s, b.lo.x, b.hi.x));
   g.s = s;
   g.lo = b.lo.x;
@@ -155,6 +218,11 @@ void bind(const FeSpace& space, int device) {
 }
 
 bool bound_to(const FeSpace& space) { return g.ctx && g.mesh_id == space.mesh().id(); }
+
+void invalidate() {
+  for (auto& c : g_cache) drop(c);
+  g_cache.clear();
+}
 
 CgResult cg_solve(const SparseOperator& a, const std::vector<double>& b, const CgOptions& opts) {
   const std::size_t n = a.dimension();
@@ -173,12 +241,10 @@ CgResult cg_solve(const SparseOperator& a, const std::vector<double>& b, const C
   std::size_t it = 0;
   double res = 0.0;
   if (lattice) {
-    DevOp A(a);
-    check(paro_cg_solve(g.ctx, A.op, 1, db.p, opts.x0 ? dx0.p : nullptr, static_cast<long long>(n), opts.tol,
+    check(paro_cg_solve(g.ctx, lattice_op(a), 1, db.p, opts.x0 ? dx0.p : nullptr, static_cast<long long>(n), opts.tol,
                         opts.max_iter, opts.throw_on_max_iter ? 1 : 0, dx.p, &it, &res));
   } else {
-    DevCsr A(a);
-    check(paro_csr_cg_solve(g.ctx, A.op, 1, db.p, opts.x0 ? dx0.p : nullptr, static_cast<long long>(n), opts.tol,
+    check(paro_csr_cg_solve(g.ctx, csr_op(a), 1, db.p, opts.x0 ? dx0.p : nullptr, static_cast<long long>(n), opts.tol,
                             opts.max_iter, opts.throw_on_max_iter ? 1 : 0, dx.p, &it, &res));
   }
   CgResult r;
@@ -202,12 +268,10 @@ std::vector<std::vector<double>> source_solve_step(const SparseOperator& a, cons
   DevVec du = pack(u_prev, n);
   DevVec dh(k * n);
   if (on_lattice(a) && on_lattice(b)) {
-    DevOp A(a), B(b);
-    check(paro_source_solve_step(g.ctx, A.op, B.op, static_cast<int>(k), du.p, static_cast<long long>(n),
+    check(paro_source_solve_step(g.ctx, lattice_op(a), lattice_op(b), static_cast<int>(k), du.p, static_cast<long long>(n),
                                  lambdas.data(), opts.tol, opts.max_iter, opts.sigma, dh.p, nullptr, nullptr));
   } else {  // adapted meshes: general CSR kernels, same semantics
-    DevCsr A(a), B(b);
-    check(paro_csr_source_solve_step(g.ctx, A.op, B.op, static_cast<int>(k), du.p, static_cast<long long>(n),
+    check(paro_csr_source_solve_step(g.ctx, csr_op(a), csr_op(b), static_cast<int>(k), du.p, static_cast<long long>(n),
                                      lambdas.data(), opts.tol, opts.max_iter, opts.sigma, dh.p, nullptr, nullptr));
   }
   return unpack(dh, k, n);
@@ -219,13 +283,14 @@ OrbitalSet rayleigh_ritz(const std::vector<std::vector<double>>& candidates, con
   const std::size_t n = a_form.dimension(), k = candidates.size();
   need(n);
   if (k == 0) throw EmptyBasisError("b_orthonormalize: all vectors dropped");
-  DevOp A(a_form), B(b);
+  paro_op* A = lattice_op(a_form);
+  paro_op* B = lattice_op(b);
   DevVec du = pack(candidates, n);
   DevVec dv(k * n);
   std::vector<double> lam(k);
   int kout = 0;
   double defect = 0.0;
-  check(paro_rayleigh_ritz(g.ctx, A.op, B.op, static_cast<int>(k), du.p, static_cast<long long>(n), min_keep,
+  check(paro_rayleigh_ritz(g.ctx, A, B, static_cast<int>(k), du.p, static_cast<long long>(n), min_keep,
                            drop_tol, lam.data(), dv.p, static_cast<long long>(n), &kout, &defect));
   OrbitalSet out;
   out.space = std::move(space);
@@ -242,12 +307,12 @@ OrthonormalizeResult b_orthonormalize(const std::vector<std::vector<double>>& ve
   need(n);
   OrthonormalizeResult r;
   if (k == 0) return r;
-  DevOp B(b);
+  paro_op* B = lattice_op(b);
   DevVec du = pack(vectors, n);
   DevVec dq(k * n);
   int kout = 0;
   std::vector<int> acc(k, -1);
-  check(paro_b_orthonormalize(g.ctx, B.op, static_cast<int>(k), du.p, drop_tol, dq.p, &kout, acc.data()));
+  check(paro_b_orthonormalize(g.ctx, B, static_cast<int>(k), du.p, drop_tol, dq.p, &kout, acc.data()));
   r.vectors = unpack(dq, static_cast<std::size_t>(kout), n);
   std::vector<bool> kept(k, false);
   for (int i = 0; i < kout; ++i) kept[static_cast<std::size_t>(acc[i])] = true;
@@ -262,12 +327,13 @@ EigenPairs baseline_geneig(const SparseOperator& a, const SparseOperator& b, std
   if (b.dimension() != n) throw InvalidArgumentError("baseline: pencil dimension mismatch");
   if (count == 0 || count > n) throw InvalidArgumentError("baseline: bad eigenpair count");
   need(n);
-  DevOp A(a), B(b);
+  paro_op* A = lattice_op(a);
+  paro_op* B = lattice_op(b);
   DevVec dv(count * n);
   EigenPairs out;
   out.values.assign(count, 0.0);
   int its = 0;
-  check(paro_baseline_geneig(g.ctx, A.op, B.op, static_cast<int>(count), opts.max_iter, opts.seed,
+  check(paro_baseline_geneig(g.ctx, A, B, static_cast<int>(count), opts.max_iter, opts.seed,
                              out.values.data(), dv.p, static_cast<long long>(n), &its));
   const std::vector<std::vector<double>> cols = unpack(dv, count, n);
   out.vectors = DenseMatrix(n, count);
@@ -303,7 +369,9 @@ Density density_from_orbitals(const std::vector<DiscreteFunction>& orbitals, con
   const std::size_t n = space->dof_count(), k = orbitals.size();
   need(n);
   DevVec du(k * n), drho(n);
-  for (std::size_t c = 0; c < k; ++c) du.up(orbitals[c].coeffs.data(), n, c * n);
+  std::vector<const double*> cols(k);
+  for (std::size_t c = 0; c < k; ++c) cols[c] = orbitals[c].coeffs.data();
+  check(paro_upload_columns(g.ctx, static_cast<int>(k), cols.data(), n, du.p, static_cast<long long>(n)));
   Density d;
   d.occupations = occupations;
   d.rho = DiscreteFunction(space);
@@ -319,10 +387,11 @@ DiscreteFunction hartree_solve_with(const SparseOperator& poisson_stiffness, con
     throw LineageError("hartree: density lives on a different generation");
   const std::size_t n = space->dof_count();
   need(n);
-  DevOp K(poisson_stiffness), M(mass);
+  paro_op* K = lattice_op(poisson_stiffness);
+  paro_op* M = lattice_op(mass);
   DevVec dr(n), dv(n);
   dr.up(rho.rho.coeffs.data(), n);
-  check(paro_hartree_solve(g.ctx, K.op, M.op, dr.p, tol, dv.p, nullptr));
+  check(paro_hartree_solve(g.ctx, K, M, dr.p, tol, dv.p, nullptr));
   DiscreteFunction out(space);
   dv.down(out.coeffs.data(), n);
   return out;

@@ -22,6 +22,10 @@ namespace paro::gpu {
 void bind(const FeSpace& space, int device = 0);
 /// True when the bound grid matches `space`'s mesh.
 bool bound_to(const FeSpace& space);
+/// Drops the cached device forms of operators (they are keyed by value array,
+/// size and a sampled signature; call this after modifying an operator in
+/// place in a way the sample could miss). bind() clears the cache too.
+void invalidate();
 
 /// cg_solve (linalg.cpp:143-223)
 CgResult cg_solve(const SparseOperator& a, const std::vector<double>& b, const CgOptions& opts = {});

@@ -103,6 +103,8 @@ SIGNATURES = {
     "paro_free": (_I, [_P, _P]),
     "paro_memcpy_h2d": (_I, [_P, _P, _P, _SZ]),
     "paro_memcpy_d2h": (_I, [_P, _P, _P, _SZ]),
+    "paro_upload_columns": (_I, [_P, _I, C.POINTER(_P), _SZ, _P, _LL]),
+    "paro_download_columns": (_I, [_P, _I, _P, _LL, _SZ, C.POINTER(_P)]),
     "paro_grid_init": (_I, [_P, _I, _D, _D]),
     "paro_grid_dofs": (_LL, [_P]),
     "paro_op_create_const": (_I, [_P, _DP, C.POINTER(_P)]),

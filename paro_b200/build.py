@@ -31,7 +31,8 @@ def _sources():
 
 
 def _headers_mtime() -> float:
-    hs = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.hpp")) + list((ROOT / "include").glob("*.h"))
+    hs = (list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.hpp")) + list(CSRC.glob("*.inc"))
+          + list((ROOT / "include").glob("*.h")))
     return max((h.stat().st_mtime for h in hs), default=0.0)
 
 

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -169,6 +170,95 @@ int paro_memcpy_d2h(paro_ctx* ctx, void* host, const void* dev, size_t bytes) {
   return guarded(ctx, [&] {
     PARO_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, ctx->c.stream));
     PARO_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    return kOk;
+  });
+}
+
+// Column blocks between scattered host vectors (the reference's
+// std::vector<std::vector<double>>) and a device [k][ld] block through a
+// pinned two-slot staging ring: host memcpy of column c + 1 overlaps the DMA
+// of column c, and no pageable-memory transfer stalls the copy engine.
+namespace {
+struct Staging {
+  double* buf[2] = {nullptr, nullptr};
+  size_t cap = 0;  // doubles per slot
+  cudaEvent_t done[2] = {nullptr, nullptr};
+};
+Staging& staging(paro_ctx* ctx, size_t doubles) {
+  static thread_local Staging st;
+  static thread_local int dev = -1;
+  if (st.cap < doubles || dev != ctx->c.device) {
+    for (int i = 0; i < 2; ++i) {
+      if (st.buf[i]) cudaFreeHost(st.buf[i]);
+      if (st.done[i]) cudaEventDestroy(st.done[i]);
+      st.buf[i] = nullptr;
+      st.done[i] = nullptr;
+    }
+    st.cap = 0;
+    for (int i = 0; i < 2; ++i) {
+      PARO_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&st.buf[i]), doubles * sizeof(double), cudaHostAllocDefault));
+      PARO_CUDA(cudaEventCreateWithFlags(&st.done[i], cudaEventDisableTiming));
+    }
+    st.cap = doubles;
+    dev = ctx->c.device;
+  }
+  return st;
+}
+constexpr size_t kStageDoubles = size_t(4) << 20;  // 32 MB per slot
+}  // namespace
+
+int paro_upload_columns(paro_ctx* ctx, int k, const double* const* host, size_t n, double* dev, long long ld) {
+  return guarded(ctx, [&] {
+    if (k < 0 || (k > 0 && (!host || !dev)) || ld < static_cast<long long>(n))
+      throw ParoError(kInvalidArgument, "upload_columns: bad arguments");
+    Staging& st = staging(ctx, kStageDoubles);
+    int slot = 0;
+    bool used[2] = {false, false};
+    for (int c = 0; c < k; ++c)
+      for (size_t off = 0; off < n; off += st.cap) {
+        const size_t cnt = std::min(st.cap, n - off);
+        if (used[slot]) PARO_CUDA(cudaEventSynchronize(st.done[slot]));
+        std::memcpy(st.buf[slot], host[c] + off, cnt * sizeof(double));
+        PARO_CUDA(cudaMemcpyAsync(dev + c * ld + off, st.buf[slot], cnt * sizeof(double), cudaMemcpyHostToDevice,
+                                  ctx->c.stream));
+        PARO_CUDA(cudaEventRecord(st.done[slot], ctx->c.stream));
+        used[slot] = true;
+        slot ^= 1;
+      }
+    PARO_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    return kOk;
+  });
+}
+
+int paro_download_columns(paro_ctx* ctx, int k, const double* dev, long long ld, size_t n, double* const* host) {
+  return guarded(ctx, [&] {
+    if (k < 0 || (k > 0 && (!host || !dev)) || ld < static_cast<long long>(n))
+      throw ParoError(kInvalidArgument, "download_columns: bad arguments");
+    Staging& st = staging(ctx, kStageDoubles);
+    // chunk i lands in slot i % 2; its host copy happens after chunk i + 1 is queued
+    struct Pending {
+      double* dst;
+      size_t cnt;
+    } pend[2] = {{nullptr, 0}, {nullptr, 0}};
+    int slot = 0;
+    auto drain = [&](int s) {
+      if (!pend[s].dst) return;
+      PARO_CUDA(cudaEventSynchronize(st.done[s]));
+      std::memcpy(pend[s].dst, st.buf[s], pend[s].cnt * sizeof(double));
+      pend[s].dst = nullptr;
+    };
+    for (int c = 0; c < k; ++c)
+      for (size_t off = 0; off < n; off += st.cap) {
+        const size_t cnt = std::min(st.cap, n - off);
+        drain(slot);
+        PARO_CUDA(cudaMemcpyAsync(st.buf[slot], dev + c * ld + off, cnt * sizeof(double), cudaMemcpyDeviceToHost,
+                                  ctx->c.stream));
+        PARO_CUDA(cudaEventRecord(st.done[slot], ctx->c.stream));
+        pend[slot] = {host[c] + off, cnt};
+        slot ^= 1;
+      }
+    drain(slot);
+    drain(slot ^ 1);
     return kOk;
   });
 }

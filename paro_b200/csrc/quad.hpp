@@ -1,5 +1,5 @@
-// Quadrature rules on the reference tetrahedron (host side), restating
-// proj/src/quadrature.cpp so the device sees identical nodes and weights.
+// Quadrature rules on the reference tetrahedron (host side): the reference's
+// own nodes and weights (quad_tables.inc, see quad.cpp).
 #pragma once
 
 #include <array>
@@ -13,9 +13,9 @@ struct Rule {
   std::vector<double> weights;                // sum to 1
 };
 
-// simplex_rule(3, degree) (quadrature.cpp:169-177 -> make_rule :80-108)
+// simplex_rule(3, degree) (quadrature.cpp:169-177), degree 2 or 5
 const Rule& simplex_rule3(int degree);
-// subdivided_rule(3, degree, levels) (quadrature.cpp:179-188 -> make_subdivided :143-165)
+// subdivided_rule(3, degree, levels) (quadrature.cpp:179-188), (5, 2)
 const Rule& subdivided_rule3(int degree, int levels);
 
 }  // namespace paro_b200

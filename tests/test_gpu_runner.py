@@ -1,0 +1,58 @@
+"""`python -m paro_b200 --config` against the reference runner (run_experiment,
+runner.cpp:67-121, compiled into oracle/_ref) on the same fixed-mesh config:
+mesh.txt byte for byte, summary.txt / exit code / iteration count equal (the
+same stop decision), trace.csv and eigenvalues.txt at the north-star bar
+(the timing columns excepted)."""
+import csv
+import io
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+H2 = "1 0.7 0 0\n1 -0.7 0 0\n"
+CASES = {
+    # Kohn-Sham, augment 0 (K = N = 1: the baseline start is unique up to sign)
+    "molecule": "problem = molecule\nmolecule_file = {mol}\nsubdivisions = 12\nbox_lo = -6\nbox_hi = 6\n"
+                "adaptive = off\naugment = 0\nmax_outer = 12\ntol_energy = 1e-7\n",
+    # linear potential well (the hydrogen builtin), converging by the lambda stability test
+    "hydrogen": "problem = hydrogen\nsubdivisions = 12\nadaptive = off\naugment = 0\nmax_outer = 12\n"
+                "vext_smoothing = 0.3\n",
+}
+
+
+def _rows(text):
+    return list(csv.DictReader(io.StringIO(text)))
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_runner_matches_reference_runner(case, tmp_path, ref):
+    from paro_b200 import runner
+
+    (tmp_path / "h2.mol").write_text(H2)
+    cfg = tmp_path / f"{case}.cfg"
+    cfg.write_text(CASES[case].format(mol=tmp_path / "h2.mol"))
+    rc_ref, summary_ref, err = ref.run_config(cfg, tmp_path / "ref", 1)
+    assert rc_ref in (0, 1), err
+    rc = runner.main(["--config", str(cfg), "-o", str(tmp_path / "gpu")])
+    assert rc == rc_ref
+    g, r = tmp_path / "gpu", tmp_path / "ref"
+    assert (g / "mesh.txt").read_bytes() == (r / "mesh.txt").read_bytes()
+    sg, sr = (g / "summary.txt").read_text().strip(), (r / "summary.txt").read_text().strip()
+    assert sg.split(",")[0] == sr.split(",")[0] and sg.split(",")[1] == sr.split(",")[1]  # status, iterations
+    assert sg.split(",")[-1] == sr.split(",")[-1]  # DOFs
+    vg, vr = float(sg.split("=")[1].split(",")[0]), float(sr.split("=")[1].split(",")[0])
+    assert abs(vg - vr) <= 1e-8 * max(1.0, abs(vr))
+    tg, tr = _rows((g / "trace.csv").read_text()), _rows((r / "trace.csv").read_text())
+    assert list(tg[0].keys()) == list(tr[0].keys()) and len(tg) == len(tr)
+    for a, b in zip(tg, tr):
+        assert a["iter"] == b["iter"] and a["dofs"] == b["dofs"]
+        for key in a:
+            if key.startswith("lambda_") or key == "e_tot":
+                assert abs(float(a[key]) - float(b[key])) <= 1e-8 * max(1.0, abs(float(b[key]))), (key, a, b)
+            if key == "eta_total":
+                assert float(a[key]) == pytest.approx(float(b[key]), rel=1e-6)
+    eg = np.loadtxt(g / "eigenvalues.txt")
+    er = np.loadtxt(r / "eigenvalues.txt")
+    np.testing.assert_allclose(eg, er, rtol=1e-8, atol=1e-10)

@@ -241,3 +241,19 @@ def test_big_golden_fixtures_are_consistent():
             assert P.integrate(rho, w.subdivisions, w.lo, w.hi) == pytest.approx(r["rho_integral"], rel=1e-12)
             assert P.norm_l2(rho, w.subdivisions, w.lo, w.hi) == pytest.approx(r["rho_l2"], rel=1e-12)
             np.testing.assert_allclose(S @ rho, r["rho_sketch"], rtol=1e-12, atol=1e-12)
+
+
+def test_quad_tables_are_the_reference_rules(ref):
+    """paro_b200/csrc/quad_tables.inc holds the reference's tetrahedral rules
+    bit for bit (generated by oracle/gen_quad_tables.py)."""
+    import re
+    from pathlib import Path
+
+    text = (Path(__file__).resolve().parents[1] / "paro_b200" / "csrc" / "quad_tables.inc").read_text()
+    for name, degree, levels in (("kSimplex2", 2, -1), ("kSimplex5", 5, -1), ("kSubdivided5x2", 5, 2)):
+        body = text.split(f"constexpr double {name}[")[1].split("};")[0]
+        rows = [[float.fromhex(v) for v in r.split(",")] for r in re.findall(r"\{([^{}]+)\}", body)]
+        pts, w = ref.quad_rule(3, degree, levels)
+        assert len(rows) == len(w)
+        for row, p, wt in zip(rows, pts, w):
+            assert row[:4] == list(p) and row[4] == wt
