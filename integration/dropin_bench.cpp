@@ -51,7 +51,7 @@ int main(int argc, char** argv) {
   SourceSolveOptions so;
   so.tol = 1e-10;
   so.max_iter = 100000;
-  so.sigma = std::max(0.0, 0.5 - orb.lambdas[0]) + 1.0;
+  so.sigma = 3.0;  // the weighted-mass field is >= -2: A + 3 M is SPD
   so.workers = workers;
   std::vector<double> occ(std::min<std::size_t>(K, 8), 2.0);
 

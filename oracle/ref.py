@@ -549,10 +549,17 @@ def space_dump(sp: "Space", path) -> None:
 
 def run_config(config_path, out_dir, workers: int = 0):
     """The reference runner (run_experiment, runner.cpp:67-121) on a config file:
-    returns (exit code as tools/main.cpp maps it, summary line, error text)."""
-    buf = C.create_string_buffer(512)
-    rc = lib().ref_run_config(str(config_path).encode(), str(out_dir).encode(), int(workers), buf, 512)
-    return rc, buf.value.decode(), (lib().ref_last_error() or b"").decode()
+    returns (exit code as tools/main.cpp maps it, summary line, error text).
+    Runs in a subprocess without numpy (oracle/run_config.py)."""
+    import subprocess
+    import sys
+
+    r = subprocess.run([sys.executable, str(HERE / "run_config.py"), str(config_path), str(out_dir), str(int(workers))],
+                       capture_output=True, text=True, timeout=3600)
+    if r.returncode != 0:
+        raise RefError(f"reference runner crashed (rc {r.returncode}): {r.stderr[-500:]}")
+    rc, summary, err = r.stdout.rstrip("\n").split("\t")
+    return int(rc), summary, err
 
 
 def workers_default() -> int:

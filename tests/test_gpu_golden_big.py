@@ -76,9 +76,12 @@ def test_config_size_trace_and_density(tag):
         e_bar = max(1e-8, AMPLIFY * sk.get("abs_e_tot", 0.0))
         rho_bar = max(1e-7, AMPLIFY * sk.get("rho_l2_est", 0.0))
         assert abs(tr.e_tot - row["e_tot"]) <= e_bar, (row["iter"], tr.e_tot, row["e_tot"])
-        # sigma = max(0, 0.5 - lambda_1) escalated by the NotSpd policy: the same
-        # escalation count, the value within the eigenvalue bar
-        assert tr.sigma == pytest.approx(row["sigma"], rel=1e-9, abs=1e-12)
+        # sigma = max(0, 0.5 - lambda_1 of the previous iteration) escalated by
+        # the NotSpd policy: the same escalation count, the value within the
+        # eigenvalue bar of the iteration it comes from
+        s_prev = sens.get(row["iter"] - 1, {}).get("max_rel_lambda", 0.0)
+        assert tr.sigma == pytest.approx(row["sigma"], rel=max(1e-9, AMPLIFY * max(s_prev, sk.get("max_rel_lambda", 0.0))),
+                                         abs=1e-12)
         d_sketch = (S @ run.rho_out).cpu().numpy() - np.asarray(row["rho_sketch"])
         est = math.sqrt(3.0 * float(np.mean(d_sketch ** 2)))  # ~ ||d||_2
         assert hh * est <= 0.5 * rho_bar, (row["iter"], hh * est)

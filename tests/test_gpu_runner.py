@@ -14,10 +14,10 @@ pytestmark = pytest.mark.gpu
 H2 = "1 0.7 0 0\n1 -0.7 0 0\n"
 CASES = {
     # Kohn-Sham, augment 0 (K = N = 1: the baseline start is unique up to sign)
-    "molecule": "problem = molecule\nmolecule_file = {mol}\nsubdivisions = 12\nbox_lo = -6\nbox_hi = 6\n"
+    "molecule": "problem = molecule\nmolecule_file = {mol}\nsubdivisions = 8\nbox_lo = -6\nbox_hi = 6\n"
                 "adaptive = off\naugment = 0\nmax_outer = 12\ntol_energy = 1e-7\n",
     # linear potential well (the hydrogen builtin), converging by the lambda stability test
-    "hydrogen": "problem = hydrogen\nsubdivisions = 12\nadaptive = off\naugment = 0\nmax_outer = 12\n"
+    "hydrogen": "problem = hydrogen\nsubdivisions = 8\nadaptive = off\naugment = 0\nmax_outer = 12\n"
                 "vext_smoothing = 0.3\n",
 }
 
