@@ -99,19 +99,24 @@ def cpu_sample_rate(workload: str, sample_s: int, steps: int = 1, workers: int |
     sp = ref.Space(w.subdivisions, w.lo, w.hi)
     g = configs.guess_vectors(w)
     times = []
-    if w.kind == "ks":
-        ks = ref.KsSystem(sp, w.charges, w.positions, w.n_electrons, w.eps)
-        loop = ref.KsLoop(ks, g, w.cg_tol_start, w.cg_tol, w.cg_tol_factor, w.cg_max_iter, w.mixing_alpha,
-                          w.drop_tol, workers)
-    else:
+
+    def make_loop():
+        if w.kind == "ks":
+            ks = ref.KsSystem(sp, w.charges, w.positions, w.n_electrons, w.eps)
+            return ks, ref.KsLoop(ks, g, w.cg_tol_start, w.cg_tol, w.cg_tol_factor, w.cg_max_iter, w.mixing_alpha,
+                                  w.drop_tol, workers)
         a = ref.Op.stiffness(sp, 0.5)
         a.add_scaled(ref.Op.wmass_harmonic(sp, 0.5) if w.potential == "harmonic"
                      else ref.Op.wmass_coulomb(sp, w.charges, w.positions, w.eps))
-        loop = ref.LinLoop(sp, a, ref.Op.mass(sp), g, w.n_orbitals, w.cg_tol_start, w.cg_tol, w.cg_tol_factor,
-                           w.cg_max_iter, w.drop_tol, workers)
+        return a, ref.LinLoop(sp, a, ref.Op.mass(sp), g, w.n_orbitals, w.cg_tol_start, w.cg_tol, w.cg_tol_factor,
+                              w.cg_max_iter, w.drop_tol, workers)
+
+    keep, loop = make_loop()
     for it in range(steps):
+        if full.iterations == 1 and it > 0:  # single-pass workload: every step is the pass from the start
+            keep, loop = make_loop()
         t0 = time.perf_counter()
-        loop.step(it)
+        loop.step(0 if full.iterations == 1 else it)
         times.append(time.perf_counter() - t0)
     factor = (full.n / w.n) * (full.subdivisions / w.subdivisions)
     return times, factor, workers, w
@@ -165,7 +170,8 @@ def pcg_traffic():
 
 def workload_config(w, world):
     return {"workload": f"BASELINE configs: {w.name} ({w.kind}, {w.subdivisions + 1}^3 nodes, n={w.n}, K={w.K}, "
-                        f"box [{w.lo},{w.hi}]^3)",
+                        f"box [{w.lo},{w.hi}]^3)" + (", one Step-3 + Step-4 pass from the initial state per step"
+                                                     if w.iterations == 1 else ""),
             "n_dofs": w.n, "orbitals": w.K, "subdivisions": w.subdivisions,
             "parallelism": f"orbital-sharded x{world}" if world > 1 else "single GPU",
             "l2": "inputs larger than L2 (K x n x 8 B per orbital set)"}
@@ -225,8 +231,25 @@ def main():
     run = ParoRun(w, be, dist, timers=False)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t_setup
+    # a single-pass workload (configs[3]: "one Step-3 + Step-4 pass") is timed
+    # as that pass repeated from its initial state, restored outside the timed
+    # intervals; every other workload runs consecutive outer iterations
+    single = w.iterations == 1
+    init = (run.orb[: run.k].clone(), list(run.lambdas), run.k) if single else None
+
+    def restore():
+        if single:
+            run.orb[: init[2]].copy_(init[0])
+            run.k, run.lambdas = init[2], list(init[1])
+            run._notspd_probe, run._fail_attempts = [], 0
+            run.stops = type(run.stops)(w)
+
+    def it_index(i):
+        return 0 if single else i
+
     for it in range(args.warmup):
-        run.step(it)
+        restore()
+        run.step(it_index(it))
     torch.cuda.synchronize()
 
     # state before the timed steps: the end-to-end pass below replays exactly
@@ -241,14 +264,27 @@ def main():
         td.barrier()
     torch.cuda.synchronize()
     torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" selects the timed region
-    ev0.record()
-    traces = [run.step(args.warmup + i) for i in range(args.steps)]
-    ev1.record()
+    if single:
+        pairs, traces = [], []
+        for i in range(args.steps):
+            restore()
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record()
+            traces.append(run.step(0))
+            b_.record()
+            pairs.append((a_, b_))
+    else:
+        ev0.record()
+        traces = [run.step(args.warmup + i) for i in range(args.steps)]
+        ev1.record()
     torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     if world > 1:
         td.barrier()
-    ms = ev0.elapsed_time(ev1) / args.steps
+    if single:
+        ms = sum(a_.elapsed_time(b_) for a_, b_ in pairs) / args.steps
+    else:
+        ms = ev0.elapsed_time(ev1) / args.steps
     launches = be.launches() - launches0
     st = be.ctx.stats()
     clk = clocks.stop() if clocks else None
@@ -275,12 +311,25 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if world > 1:
             td.barrier()
-        e0.record()
-        for i in range(args.steps):
-            tr = run.step_host(args.warmup + i, h_orb, h_rho, chunks=args.e2e_chunks)
-        e1.record()
-        torch.cuda.synchronize()
-        e_ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda", dtype=torch.float64)
+        if single:
+            e_tot_ms = 0.0
+            for i in range(args.steps):
+                restore()
+                h_orb.copy_(init[0])  # the pass's host input, restored outside the timed interval
+                torch.cuda.synchronize()
+                e0.record()
+                tr = run.step_host(0, h_orb, h_rho, chunks=args.e2e_chunks)
+                e1.record()
+                torch.cuda.synchronize()
+                e_tot_ms += e0.elapsed_time(e1)
+            e_ms = torch.tensor([e_tot_ms / args.steps], device="cuda", dtype=torch.float64)
+        else:
+            e0.record()
+            for i in range(args.steps):
+                tr = run.step_host(args.warmup + i, h_orb, h_rho, chunks=args.e2e_chunks)
+            e1.record()
+            torch.cuda.synchronize()
+            e_ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda", dtype=torch.float64)
         if world > 1:
             td.all_reduce(e_ms, op=td.ReduceOp.MAX)
         c0, c1, _ = dist.shard(K0)
