@@ -197,9 +197,12 @@ int baseline_geneig(Ctx& ctx, const Op& A, const Op& B, int count, unsigned long
     // random columns, as the reference tops the basis up (linalg.cpp:569-575)
     int k = 0, rs = kOk;
     double defect = 0.0;
+    // baseline_subspace (linalg.cpp:568-596) has no orthonormality certificate
+    RitzInfo no_cert;
+    no_cert.certify = false;
     for (int tries = 0; tries < 8; ++tries) {
       rs = rayleigh_ritz(ctx, A, B, block, Y, n, static_cast<size_t>(block), 1e-14, lam.data(), X, n, &k, &defect,
-                         nullptr);
+                         &no_cert);
       if (rs != kDegenerateSpan && rs != kEmptyBasis) break;
       noise(Y + static_cast<long long>(block - 1 - tries % block) * n, n);
     }

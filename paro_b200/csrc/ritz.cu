@@ -550,12 +550,15 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
     }
     return kOk;
   };
+  bool copy_pending = false;  // a host copy-out of V is queued on the copy stream
   auto finish = [&](const double* Qb, int kk) -> double {
+    auto& co = ctx.ritz_copyout;
+    // a CGS2 retry rewrites V: the copy-out queued by the first finish must have read it
+    if (copy_pending) PARO_CUDA(cudaStreamWaitEvent(st, co.ready, 0));
     // lift, sign convention, certificate (paro.cpp:157-174)
     rotate(ctx, kk, kk, Qb, n, s.Y, kk, V, ldv);
     fix_sign_columns(ctx, V, ldv, kk);
     // final orbitals: a pending host copy-out starts now, overlapping the certificate
-    auto& co = ctx.ritz_copyout;
     if (co.host != nullptr) {
       if (co.ready == nullptr) PARO_CUDA(cudaEventCreateWithFlags(&co.ready, cudaEventDisableTiming));
       PARO_CUDA(cudaEventRecord(co.ready, st));
@@ -564,6 +567,8 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
       for (int c = co.c0; c < c1; ++c)
         PARO_CUDA(cudaMemcpyAsync(co.host + static_cast<long long>(c) * co.ldh, V + static_cast<long long>(c) * ldv,
                                   sizeof(double) * n, cudaMemcpyDeviceToHost, co.stream));
+      PARO_CUDA(cudaEventRecord(co.ready, co.stream));  // reused: "the copies have read V"
+      copy_pending = true;
     }
     apply_op(ctx, B, nullptr, 0.0, kk, V, ldv, W, n);
     gram(ctx, kk, V, ldv, W, n, s.G3);
@@ -635,7 +640,7 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
   small_d2h(ctx, lambdas, s.vals, sizeof(double) * k);
   *k_out = k;
   *defect = d;
-  if (d > 1e-8) {
+  if (d > 1e-8 && (!info || info->certify)) {
     ctx.err = "rayleigh_ritz: orthonormality certificate violated (defect " + std::to_string(d) + ")";
     return kError;
   }

@@ -9,6 +9,7 @@ struct RitzInfo {
   double min_ratio = 0.0;  // smallest projected/original B-norm ratio of the candidates
   int k = 0;
   bool cgs2 = false;       // the explicit Gram-Schmidt path was used
+  bool certify = true;     // in: fail on max |V^T B V - I| > 1e-8 (paro.cpp:171-174); baseline_subspace has no such test
 };
 
 int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, long long ld, size_t min_keep,
