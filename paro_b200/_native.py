@@ -10,8 +10,6 @@ import os
 from pathlib import Path
 
 _LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libparo_b200.so"
-if os.environ.get("PARO_LIB"):  # experiment knob: A/B against another in-tree build of the same library
-    _LIB_PATH = Path(os.environ["PARO_LIB"]).resolve()
 
 _P = C.c_void_p
 _D = C.c_double

@@ -22,8 +22,6 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NO_FMA = {"dense.cu", "assemble.cu", "fields.cu"}
 CFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{ROOT / 'include'}", f"-I{CSRC}",
           "--expt-relaxed-constexpr"]
-if os.environ.get("PARO_TILE_Y"):  # experiment knob: stencil tile height (8 default, 16)
-    CFLAGS.append(f"-DPARO_TILE_Y={int(os.environ['PARO_TILE_Y'])}")
 
 
 def _sources():

@@ -844,20 +844,12 @@ void launch_s(const MarchArgs& a, cudaStream_t st) {
   PARO_CUDA(cudaGetLastError());
 }
 
-bool use_v2() {
-  static const bool v2 = [] {
-    const char* e = std::getenv("PARO_MARCH_V2");  // experiment knob: previous kernel generation
-    return e && e[0] == '1';
-  }();
-  return v2;
-}
-
 template <int MODE, bool VAR, int CB>
 void launch_t(const MarchArgs& a, cudaStream_t st) {
   {
     // the streaming kernel takes constant shift / rhs-mass stencils; variable
     // ones (inexact mesh spacing) stay on the v2 kernel
-    if (!use_v2() && a.op.mcoef == nullptr && a.mwcoef == nullptr) {
+    if (a.op.mcoef == nullptr && a.mwcoef == nullptr) {
       if (VAR && a.op.sigma != 0.0) throw ParoError(kInvalidArgument, "march: shifted variable operator not preshifted");
       return launch_s<MODE, VAR, CB>(a, st);
     }
@@ -877,11 +869,6 @@ void launch_t(const MarchArgs& a, cudaStream_t st) {
 
 template <int MODE, bool VAR>
 void launch_cb(int cb, const MarchArgs& a, cudaStream_t st) {
-  static const int forced = [] {
-    const char* e = std::getenv("PARO_MARCH_CB");  // experiment knob: column-group width
-    return e ? std::atoi(e) : 0;
-  }();
-  if (forced > 0 && cb > forced) cb = forced;
   switch (cb) {
     case 1: launch_t<MODE, VAR, 1>(a, st); break;
     case 2: launch_t<MODE, VAR, 2>(a, st); break;
@@ -920,10 +907,7 @@ void plan_march(MarchArgs& a, int S, int zlo, int zhi) {
   a.nTY = (S + kTY - 1) / kTY;
   const long long target = 148 * 4;
   long long zc = (static_cast<long long>(nz) * a.nTX * a.nTY + target - 1) / target;
-  static const int zc_max = [] {
-    const char* e = std::getenv("PARO_ZC");  // experiment knob: planes per CTA z-chunk (default 32)
-    return e ? std::atoi(e) : 32;
-  }();
+  constexpr long long zc_max = 32;  // planes per CTA z-chunk (48 / 64 measured no faster)
   zc = std::max<long long>(4, std::min<long long>(zc_max, zc));
   a.ZC = static_cast<int>(std::max<long long>(1, std::min<long long>(zc, nz)));
   a.nZ = (nz + a.ZC - 1) / a.ZC;

@@ -78,7 +78,6 @@ struct MarchArgs {
   double* partials = nullptr;    // [K][3][nblk]
   int with_dot = 0;              // Apply: accumulate x.y
   long long ldw = 0;             // Setup: stride of the x, r outputs (0: ld)
-  int bulk = 0;                  // K1/K2: operands in padded solver buffers -> bulk-copy kernel
   int xmode = 2;                 // K2 x update: 2 every iteration; deferred pairs (k2c): 0 none, 1 x += a' p' + a p
   int P = 0;                     // row length of the row-padded solver layout (0: dense S);
                                  // Setup writes x, r there, the TMA passes read/write it
@@ -117,11 +116,10 @@ void launch_march(int mode, bool var, int cb, const MarchArgs& a, cudaStream_t s
 // operands qualify (otherwise the apply stays on stream_kernel).
 bool apply_flat_ok(bool var, const MarchArgs& a);
 void launch_apply_flat(bool var, int cb, const MarchArgs& a, const double* coefp, long long ldi, cudaStream_t st);
-// K1/K2 on padded solver buffers (bulk.cu): every vector operand is 16-byte
-// aligned, has an even column stride and at least kBulkPad readable elements
-// before its first and after its last column.
+// padded solver buffers: every vector operand is 16-byte aligned, has an even
+// column stride and at least kBulkPad readable elements before its first and
+// after its last column
 constexpr long long kBulkPad = 64;
-void launch_bulk(int mode, bool var, int cb, const MarchArgs& a, cudaStream_t st);
 void plan_march(MarchArgs& a, int S, int zlo = 0, int zhi = -1);
 
 }  // namespace paro_b200

@@ -244,11 +244,8 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
   if (!var && op.mcoef) throw ParoError(kInvalidArgument, "pcg: a variable shift needs a variable operator");
   const int cb = pick_cb(K);
   // TMA-tensor passes (tma.cu) unless the shift stencil varies per point
-  static const bool no_tma = [] {
-    const char* e = std::getenv("PARO_NO_TMA");  // experiment knob: previous (bulk/LDGSTS) passes
-    return e && e[0] == '1';
-  }();
-  const bool use_tma = !no_tma && op.mcoef == nullptr;
+  // (inexact mesh spacings: the LDGSTS march kernels take the per-point shift)
+  const bool use_tma = op.mcoef == nullptr;
   const int P = use_tma ? padded_row(g.S) : g.S;
   const long long np = static_cast<long long>(g.S) * g.S * P;  // elements per column in the solver layout
 
@@ -321,11 +318,7 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
   m.P = use_tma ? P : 0;
   m.scale = dscale;
   m.rhs = rhs;
-  static const bool no_tma_setup = [] {
-    const char* e = std::getenv("PARO_NO_TMA_SETUP");  // experiment knob: setup on the LDGSTS kernel
-    return e && e[0] == '1';
-  }();
-  if (use_tma && var && warm && rhs == nullptr && m.mwcoef == nullptr && !no_tma_setup) {
+  if (use_tma && var && warm && rhs == nullptr && m.mwcoef == nullptr) {
     // x0 = u copied into the solver layout, then r0 = (M u) scale - A u on TMA planes of x
     pad_cols_kernel<<<dim3(148 * 2, K), 256, 0, st>>>(src, ld, xi, ldi, g.S, P);
     PARO_CUDA(cudaGetLastError());
@@ -343,10 +336,6 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
   // iteration chunks captured once into a CUDA graph (PARO_NO_GRAPH=1 launches
   // them directly, e.g. for ncu)
   const int chunk = n >= (1 << 22) ? 4 : n >= (1 << 18) ? 8 : 16;  // even: ping-pong parity repeats
-  static const bool k1_bulk = [] {
-    const char* e = std::getenv("PARO_K1_BULK");  // experiment knob
-    return e && e[0] == '1';
-  }();
   // x updates in pairs of iterations on the k2c pass (half the x traffic):
   // even iterations leave x, odd ones apply both updates; a column stopping
   // after an even iteration gets its last update at the copy-out
@@ -358,11 +347,9 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
       k1.pold = (it & 1) ? p1 : p0;
       k1.dst = (it & 1) ? p0 : p1;
       k1.r = r;
-      // previous generation (PARO_NO_TMA=1): K1 on the LDGSTS streaming
-      // kernel, K2 on the bulk-copy kernel
+      // a per-point shift stencil runs on the LDGSTS march kernels
       if (use_tma) launch_tma(kK1, var, cb, k1, tmaps, (it & 1) == 0, s);
-      else if (op.mcoef || !k1_bulk) launch_march(kK1, var, cb, k1, s);
-      else launch_bulk(kK1, var, cb, k1, s);
+      else launch_march(kK1, var, cb, k1, s);
       fin_kernel<<<K, kFinThreads, 0, s>>>(kFinK1, dcols, partials, m.nblk, flag);
       MarchArgs k2 = m;
       k2.ld = ldi;
@@ -372,8 +359,7 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
       k2.xmode = deferred ? (it & 1) : 2;  // chunk is even: it has the global iteration's parity
       k2.pold = k1.pold;                   // p of the previous iteration
       if (use_tma) launch_tma(kK2, var, cb, k2, tmaps, (it & 1) != 0, s);
-      else if (op.mcoef || K < 4) launch_march(kK2, var, cb, k2, s);  // narrow batches: LDGSTS kernel
-      else launch_bulk(kK2, var, cb, k2, s);
+      else launch_march(kK2, var, cb, k2, s);
       fin_kernel<<<K, kFinThreads, 0, s>>>(kFinK2, dcols, partials, m.nblk, flag);
     }
     count_active_kernel<<<1, 256, 0, s>>>(dcols, K, ctx.pinned_count_dev);

@@ -1,20 +1,20 @@
 // TMA-tensor variant of the two fused Jacobi-PCG stencil passes (K1, K2) on
 // the row-padded solver layout (march.cuh: padded_row).
 //
-// Same streaming row sums as stream_kernel / bulk_kernel, but every operand
+// Same streaming row sums as stream_kernel (march.cu), but every operand
 // plane is moved by the TMA engine from a 4-D tensor map (x, y, z, column):
 // one elected thread issues one cp.async.bulk.tensor per (array, column) and
 // plane, completion is counted on an mbarrier per ring slot, and the engine's
 // out-of-bounds zero fill supplies the Dirichlet halo (fem.cpp:21-28), so no
 // thread spends issue slots on per-row copies, edge fix-ups or zero planes
-// (the per-thread bulk copies of bulk_kernel compiled to a uniform-register
+// (per-thread bulk copies, the previous generation, compiled to a uniform-register
 // waterfall on 4 of the 8 warps, which then gated every barrier).
 //
 // K2 also writes x and r back with TMA tensor stores: the own-point rows of
 // x and r land in a 4-slot ring, are updated in place, fenced to the async
 // proxy and stored by the elected thread one step later.
 //
-// Arithmetic is identical to bulk_kernel (same FMA row sums, same update
+// Arithmetic is identical to the march kernels (same FMA row sums, same update
 // formulas, linalg.cpp:179, 202-210), so results do not depend on the variant.
 #include <cudaTypedefs.h>
 
@@ -1103,11 +1103,6 @@ void launch_k(const MarchArgs& a, const Maps& m, cudaStream_t st) {
 
 template <int MODE, bool VAR>
 void launch_cb(int cb, const MarchArgs& a, const Maps& m, cudaStream_t st) {
-  static const int forced = [] {
-    const char* e = std::getenv("PARO_MARCH_CB");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (forced > 0 && cb > forced) cb = forced;
   switch (cb) {
     case 1: launch_k<MODE, VAR, 1>(a, m, st); break;
     case 2: launch_k<MODE, VAR, 2>(a, m, st); break;
@@ -1471,12 +1466,8 @@ void tma_plan(PcgTma& t, int S, long long ldi, int K, const double* r, const dou
 }
 
 bool apply_flat_ok(bool var, const MarchArgs& a) {
-  static const bool off = [] {
-    const char* e = std::getenv("PARO_NO_FLAT_APPLY");  // experiment knob: apply on stream_kernel
-    return e && e[0] == '1';
-  }();
   const int S = a.S;
-  if (off || (S & 1) == 0 || a.ld != a.n || a.with_dot || a.op.mcoef != nullptr) return false;
+  if ((S & 1) == 0 || a.ld != a.n || a.with_dot || a.op.mcoef != nullptr) return false;
   if (var && a.op.sigma != 0.0) return false;
   if ((reinterpret_cast<uintptr_t>(a.src) & 15) != 0) return false;
   const long long rows = static_cast<long long>(a.K) * S * S;  // lattice rows of all columns
@@ -1518,11 +1509,7 @@ void launch_apply_flat(bool var, int cb, const MarchArgs& a, const double* coefp
   }
   if (var) encode(mc, coefp, S, ldi, kSlots, kRW, kTY + 1, kSlots);
   else mc = mx;
-  static const int forced = [] {
-    const char* e = std::getenv("PARO_MARCH_CB");
-    return e ? std::atoi(e) : 0;
-  }();
-  const int c = forced > 0 && cb > forced ? forced : cb;
+  const int c = cb;
   if (var) {
     if (c == 1) launch_k3f<true, 1>(a, mx, mc, st);
     else if (c == 2) launch_k3f<true, 2>(a, mx, mc, st);
@@ -1534,13 +1521,7 @@ void launch_apply_flat(bool var, int cb, const MarchArgs& a, const double* coefp
   }
 }
 
-bool tma_k2c_active() {
-  static const bool no_k2c = [] {
-    const char* e = std::getenv("PARO_NO_K2C");  // experiment knob: coefficients by per-thread loads
-    return e && e[0] == '1';
-  }();
-  return !no_k2c;
-}
+bool tma_k2c_active() { return true; }
 
 void launch_tma_setup(int cb, const MarchArgs& a, const PcgTma& t, cudaStream_t st) {
   if (!t.has_coef) throw ParoError(kInvalidArgument, "tma setup: needs the padded coefficients");
@@ -1550,11 +1531,7 @@ void launch_tma_setup(int cb, const MarchArgs& a, const PcgTma& t, cudaStream_t 
   m.a = t.x_halo;
   m.b = t.coef_box;
   m.c = t.invd_own;
-  static const int forced = [] {
-    const char* e = std::getenv("PARO_MARCH_CB");
-    return e ? std::atoi(e) : 0;
-  }();
-  const int c = forced > 0 && cb > forced ? forced : cb;
+  const int c = cb;
   if (c == 1) launch_k0c<1>(a, m, st);
   else if (c == 2) launch_k0c<2>(a, m, st);
   else launch_k0c<4>(a, m, st);
@@ -1566,16 +1543,8 @@ void launch_tma(int mode, bool var, int cb, const MarchArgs& a, const PcgTma& t,
   if (var && a.op.sigma != 0.0) throw ParoError(kInvalidArgument, "tma: shifted variable operator not preshifted");
   if (a.op.mcoef != nullptr) throw ParoError(kInvalidArgument, "tma: variable shift stencil unsupported");
   Maps m;
-  static const bool no_k1f = [] {
-    const char* e = std::getenv("PARO_NO_K1F");  // experiment knob: K1 on the full row-sum kernel
-    return e && e[0] == '1';
-  }();
-  if (mode == kK1 && !no_k1f) {
-    static const int forced = [] {
-      const char* e = std::getenv("PARO_MARCH_CB");
-      return e ? std::atoi(e) : 0;
-    }();
-    const int c = forced > 0 && cb > forced ? forced : cb;
+  if (mode == kK1) {
+    const int c = cb;
     const CUtensorMap& po = p_is_p0 ? t.p0_fwd : t.p1_fwd;
     if (var) {
       if (c == 1) launch_k1f<true, 1>(a, t.r_fwd, po, t.invd_fwd, st);
@@ -1586,12 +1555,6 @@ void launch_tma(int mode, bool var, int cb, const MarchArgs& a, const PcgTma& t,
       else if (c == 2) launch_k1f<false, 2>(a, t.r_fwd, po, t.invd_fwd, st);
       else launch_k1f<false, 4>(a, t.r_fwd, po, t.invd_fwd, st);
     }
-  } else if (mode == kK1) {
-    m.a = t.r_halo;
-    m.b = p_is_p0 ? t.p0_halo : t.p1_halo;
-    m.c = t.invd_halo;
-    if (var) launch_cb<kK1, true>(cb, a, m, st);
-    else launch_cb<kK1, false>(cb, a, m, st);
   } else if (mode == kK2) {
     m.a = p_is_p0 ? t.p0_halo : t.p1_halo;
     m.b = t.x_own;
@@ -1599,18 +1562,9 @@ void launch_tma(int mode, bool var, int cb, const MarchArgs& a, const PcgTma& t,
     if (var && t.has_coef && tma_k2c_active()) {
       m.b = t.coef_box;
       m.c = t.invd_own;
-      static const int forced = [] {
-        const char* e = std::getenv("PARO_MARCH_CB");
-        return e ? std::atoi(e) : 0;
-      }();
-      static const bool cb8 = [] {
-        const char* e = std::getenv("PARO_K2C_CB8");  // experiment knob: 8 columns per CTA, one CTA per SM
-        return e && e[0] == '1';
-      }();
-      const int c = forced > 0 && cb > forced ? forced : cb;
+      const int c = cb;
       if (c == 1) launch_k2c<1>(a, m, st);
       else if (c == 2) launch_k2c<2>(a, m, st);
-      else if (c >= 8 && cb8) launch_k2c<8>(a, m, st);
       else launch_k2c<4>(a, m, st);
     } else if (a.xmode != 2) {
       throw ParoError(kInvalidArgument, "tma: deferred x updates need the k2c pass");
