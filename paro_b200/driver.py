@@ -47,13 +47,16 @@ def step3_outcome(first, final):
 class Dist:
     """torch.distributed plumbing (NCCL on GPUs, gloo on CPU); world 1 = no-op."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, collectives: bool = False):
+        """collectives=True runs every exchange through the process group even
+        at world size 1 (a single-rank NCCL check of the N > 1 code path)."""
         import torch.distributed as td
 
         self.td = td if td.is_available() and td.is_initialized() else None
         self.group = group
         self.world = self.td.get_world_size(group) if self.td else 1
         self.rank = self.td.get_rank(group) if self.td else 0
+        self.solo = self.world == 1 and not (collectives and self.td is not None)
 
     def _gather(self, out: torch.Tensor, inp: torch.Tensor):
         """all_gather_into_tensor (NCCL); list all_gather on backends without it (gloo)."""
@@ -70,7 +73,7 @@ class Dist:
 
     def allgather_columns(self, local: torch.Tensor, counts, out: torch.Tensor):
         """[k_r, n] blocks -> out[:K] in rank order (padded to max(counts))."""
-        if self.world == 1:
+        if self.solo:
             if local.data_ptr() != out.data_ptr():
                 out[: local.shape[0]].copy_(local)
             return out
@@ -91,7 +94,7 @@ class Dist:
     def allsum_(self, t: torch.Tensor) -> torch.Tensor:
         """In-place sum over ranks, added in rank order (deterministic, and
         the same bits on every rank)."""
-        if self.world == 1:
+        if self.solo:
             return t
         flat = t.reshape(-1)
         buf = flat.new_empty(self.world * flat.numel())
@@ -103,12 +106,12 @@ class Dist:
         return t
 
     def allmax_(self, t: torch.Tensor) -> torch.Tensor:
-        if self.world > 1:
+        if not self.solo:
             self.td.all_reduce(t, op=self.td.ReduceOp.MAX, group=self.group)
         return t
 
     def allmin_(self, t: torch.Tensor) -> torch.Tensor:
-        if self.world > 1:
+        if not self.solo:
             self.td.all_reduce(t, op=self.td.ReduceOp.MIN, group=self.group)
         return t
 
@@ -118,7 +121,7 @@ class Dist:
         every rank's columns on this rank's extended rows. One all-to-all."""
         me = slabs[self.rank]
         c0 = sum(counts[: self.rank])
-        if self.world == 1:
+        if self.solo:
             if local.data_ptr() != dst[c0:].data_ptr():
                 dst[c0:c0 + local.shape[0], me.e0:me.e1].copy_(local[:, me.e0:me.e1])
             return dst
@@ -138,7 +141,7 @@ class Dist:
     def slabs_to_cols(self, V: torch.Tensor, counts, slabs):
         """Row slabs -> column shards, in place: V[:K] holds every column on this
         rank's own rows; afterwards this rank's columns hold every row."""
-        if self.world == 1:
+        if self.solo:
             return V
         me = slabs[self.rank]
         c0 = sum(counts[: self.rank])
@@ -158,7 +161,7 @@ class Dist:
 
     def allgather_rows(self, f: torch.Tensor, slabs):
         """f (n) valid on this rank's own rows -> valid everywhere."""
-        if self.world == 1:
+        if self.solo:
             return f
         m = max(s.r1 - s.r0 for s in slabs)
         me = slabs[self.rank]
@@ -172,7 +175,7 @@ class Dist:
         return f
 
     def allgather_ints(self, values, counts, device):
-        if self.world == 1:
+        if self.solo:
             return list(values)
         kmax = max(counts)
         t = torch.full((kmax,), -1, dtype=torch.int64, device=device)
@@ -606,7 +609,7 @@ class ParoRun:
     def _idev(self):
         """Device for the small status all-gathers: the GPU under NCCL, else CPU."""
         d = self.dist
-        if d.world > 1 and d.td.get_backend(d.group) == "nccl":
+        if not d.solo and d.td.get_backend(d.group) == "nccl":
             return self.be.device
         return torch.device("cpu")
 
