@@ -348,20 +348,7 @@ void gram(Ctx& ctx, int k, const double* X, long long ldx, const double* Y, long
 // Cholesky-QR basis change (zero below the drop-shifted diagonal)
 void rotate(Ctx& ctx, int k1, int k2, const double* X, long long ldx, const double* Cm, int ldc, double* Z,
             long long ldz, bool tri = false) {
-  const long long n = ctx.grid.n;
-  if (k1 <= 80 && k2 <= 80) {
-    rotate_rows(ctx, k1, X, ldx, Cm, ldc, k2, Z, ldz, 0, n, tri ? 2 : 0);
-    return;
-  }
-  // blocked over 80-column slices of C (bit 2: accumulate)
-  for (int j0 = 0; j0 < k2; j0 += 80) {
-    const int kj = std::min(80, k2 - j0);
-    for (int i0 = 0; i0 < k1; i0 += 80) {
-      const int ki = std::min(80, k1 - i0);
-      rotate_rows(ctx, ki, X + i0 * ldx, ldx, Cm + i0 + static_cast<long long>(j0) * ldc, ldc, kj,
-                  Z + j0 * ldz, ldz, 0, n, i0 == 0 ? 0 : 4);
-    }
-  }
+  rotate_rows(ctx, k1, X, ldx, Cm, ldc, k2, Z, ldz, 0, ctx.grid.n, tri ? 2 : 0);
 }
 
 __device__ __forceinline__ double block_max(double v, double* sh) {

@@ -309,7 +309,20 @@ int grid_for(long long rows, int per_sm) {
 void rotate_rows(Ctx& ctx, int k1, const double* X, long long ldx, const double* C, int ldc, int k2, double* Z,
                  long long ldz, long long r0, long long r1, int mode) {
   if (k1 <= 0 || k2 <= 0 || r1 <= r0) return;
-  if (k1 > kRotMaxK || k2 > kRotMaxK) throw ParoError(kInvalidArgument, "rotate: at most 80 columns");
+  if (k1 > kRotMaxK || k2 > kRotMaxK) {
+    // wider bases: 80 x 80 blocks of C; the first input block of an assigning
+    // rotation assigns, the others accumulate (the triangular skip is dropped)
+    for (int j0 = 0; j0 < k2; j0 += kRotMaxK) {
+      const int kj = std::min(kRotMaxK, k2 - j0);
+      for (int i0 = 0; i0 < k1; i0 += kRotMaxK) {
+        const int ki = std::min(kRotMaxK, k1 - i0);
+        const int m = (mode & 1) ? 1 : (mode & 4) ? 4 : (i0 == 0 ? 0 : 4);
+        rotate_rows(ctx, ki, X + i0 * ldx, ldx, C + i0 + static_cast<long long>(j0) * ldc, ldc, kj, Z + j0 * ldz,
+                    ldz, r0, r1, m);
+      }
+    }
+    return;
+  }
   static bool configured = false;
   if (!configured) {
     PARO_CUDA(cudaFuncSetAttribute(rotate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -27,7 +27,7 @@ def _rand(shape, seed):
     return torch.rand(shape, generator=g, dtype=torch.float64).mul_(2).sub_(1).cuda()
 
 
-@pytest.mark.parametrize("k1,k2", [(76, 76), (5, 3), (80, 17), (33, 1)])
+@pytest.mark.parametrize("k1,k2", [(76, 76), (5, 3), (80, 17), (33, 1), (100, 90), (81, 7)])
 def test_rotate_matches_torch(k1, k2):
     from paro_b200 import core
 
