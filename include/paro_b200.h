@@ -204,6 +204,9 @@ int paro_ritz_ortho(paro_ctx* ctx, int K, const double* g, double drop_tol, doub
                     double* min_ratio);
 /* second Cholesky-QR pass: g2 -> c2 = L2^{-T}, bt = L2^{-1} g2 L2^{-T}; PARO_PENCIL if not SPD */
 int paro_ritz_second_pass(paro_ctx* ctx, int k, const double* g2, double* c2, double* bt);
+/* one-pass basis change (well-conditioned candidates, no drops): bt = sym(c1^T sym(g) c1), the
+ * B-Gram of U c1 in k x k arithmetic; the pencil then runs on (ga = U^T A U, c1, bt) */
+int paro_ritz_congruence(paro_ctx* ctx, int k, const double* g, const double* c1, double* bt);
 /* the k x k pencil: gb == NULL: in the Q basis from (ga, c2, bt); else directly
  * (ga, gb). Eigenvalues to host `vals`, lift coefficients to device y (k x k). */
 int paro_ritz_pencil(paro_ctx* ctx, int k, const double* ga, const double* c2, const double* bt, const double* gb,

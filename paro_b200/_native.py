@@ -131,6 +131,7 @@ SIGNATURES = {
     "paro_rotate": (_I, [_P, _I, _P, _LL, _P, _I, _I, _P, _LL, _LL, _LL, _I]),
     "paro_ritz_ortho": (_I, [_P, _I, _P, _D, _P, C.POINTER(_I), _DP]),
     "paro_ritz_second_pass": (_I, [_P, _I, _P, _P, _P]),
+    "paro_ritz_congruence": (_I, [_P, _I, _P, _P, _P]),
     "paro_ritz_pencil": (_I, [_P, _I, _P, _P, _P, _P, _DP, _P]),
     "paro_gram_defect": (_I, [_P, _I, _P, _DP]),
     "paro_sign_init": (_I, [_P, _I, _P, _P]),

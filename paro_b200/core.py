@@ -101,8 +101,9 @@ class Context:
         return self
 
     def set_ritz_mode(self, mode: str) -> "Context":
-        """'cholqr': Cholesky-QR twice with Gram-Schmidt fallback; 'cgs2': always Gram-Schmidt."""
-        self.check(N.lib().paro_ctx_set_ritz_mode(self.h, {"cholqr": 0, "cgs2": 1}[mode]))
+        """'cholqr': Cholesky-QR (one K x K pass for well-conditioned candidates, else twice) with
+        Gram-Schmidt fallback; 'cholqr2': always twice; 'cgs2': always Gram-Schmidt."""
+        self.check(N.lib().paro_ctx_set_ritz_mode(self.h, {"cholqr": 0, "cgs2": 1, "cholqr2": 2}[mode]))
         return self
 
     def empty(self, *shape) -> torch.Tensor:
@@ -667,6 +668,11 @@ def ritz_second_pass(ctx: Context, G2: torch.Tensor, k: int, C2: torch.Tensor, B
         return False
     ctx.check(st)
     return True
+
+
+def ritz_congruence(ctx: Context, G: torch.Tensor, C1: torch.Tensor, k: int, Bt: torch.Tensor):
+    """Bt = sym(C1^T sym(G) C1): the B-Gram of U C1 in k x k arithmetic (one-pass Step 4)."""
+    ctx.check(N.lib().paro_ritz_congruence(ctx.h, int(k), _ptr(G), _ptr(C1), _ptr(Bt)))
 
 
 def ritz_pencil(ctx: Context, GA: torch.Tensor, C2, Bt, GB, k: int, Y: torch.Tensor) -> list:

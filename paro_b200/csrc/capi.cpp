@@ -136,6 +136,7 @@ int paro_ctx_set_ritz_copyout(paro_ctx* ctx, void* copy_stream, double* host, lo
 int paro_ctx_set_ritz_mode(paro_ctx* ctx, int mode) {
   return guarded(ctx, [&] {
     ctx->c.force_cgs2 = mode == 1;
+    ctx->c.two_pass_only = mode == 2;
     return kOk;
   });
 }
@@ -500,6 +501,10 @@ int paro_ritz_ortho(paro_ctx* ctx, int K, const double* g, double drop_tol, doub
 
 int paro_ritz_second_pass(paro_ctx* ctx, int k, const double* g2, double* c2, double* bt) {
   return guarded(ctx, [&] { return ritz_second_pass(ctx->c, k, g2, c2, bt); });
+}
+
+int paro_ritz_congruence(paro_ctx* ctx, int k, const double* g, const double* c1, double* bt) {
+  return guarded(ctx, [&] { return ritz_congruence(ctx->c, k, g, c1, bt); });
 }
 
 int paro_ritz_pencil(paro_ctx* ctx, int k, const double* ga, const double* c2, const double* bt, const double* gb,

@@ -58,6 +58,7 @@ struct Ctx {
   DevBuf partials, cols, scale, invd, pbuf0, pbuf1, flag;
   DevBuf ws_a, ws_b, ws_c, ws_d, ws_e, ws_small, ws_small2, ws_small3;
   bool force_cgs2 = false;           // Step 4: skip the Cholesky-QR path
+  bool two_pass_only = false;        // Step 4: always form the intermediate basis (no one-pass basis change)
   struct {                           // one-shot host copy-out of the next Ritz orbitals
     cudaStream_t stream = nullptr;
     double* host = nullptr;

@@ -399,6 +399,32 @@ __global__ void second_pass_kernel(int k, const double* G2, double* C2, double* 
   if (lane == 0) *status = kOk;
 }
 
+// One-pass basis change: Bt = sym(C^T sym(G) C) (row-major k x k) for the raw
+// Gram G = U^T B U and C = L^{-T} of its ordered Cholesky (both column-major
+// k x k): the B-Gram of Q = U C formed in K x K arithmetic, which is as
+// accurate as forming Q when the candidates are well conditioned (step4.py).
+__global__ void congruence_kernel(int k, const double* G, const double* Cm, double* Bt, DenseScratch w) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int idx = tid; idx < k * k; idx += nt) {
+    const int i = idx / k, j = idx % k;
+    double s = 0.0;
+    for (int m = 0; m < k; ++m) s += 0.5 * (G[i + m * k] + G[m + i * k]) * Cm[m + j * k];
+    w.w[i * k + j] = s;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < k * k; idx += nt) {
+    const int i = idx / k, j = idx % k;
+    double s = 0.0;
+    for (int m = 0; m < k; ++m) s += Cm[m + i * k] * w.w[m * k + j];
+    w.c[i * k + j] = s;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < k * k; idx += nt) {
+    const int i = idx / k, j = idx % k;
+    Bt[i * k + j] = i == j ? w.c[idx] : 0.5 * (w.c[i * k + j] + w.c[j * k + i]);
+  }
+}
+
 // Pencil in an explicitly orthonormalised basis Q (paro.cpp:143-150):
 // At = sym(Q^T A Q), Bt = sym(Q^T B Q) (column-major inputs), then
 // dense_sym_geneig; Y (column-major k x k) = X.

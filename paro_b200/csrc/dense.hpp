@@ -28,6 +28,7 @@ __global__ void geneig_kernel(int n, const double* A, const double* B, double* v
 __global__ void ortho_from_gram_kernel(int K, const double* G, double drop_tol, int allow_drop, double* C, int* acc,
                                        int* kout, double* min_ratio, DenseScratch w, int* status);
 __global__ void second_pass_kernel(int k, const double* G2, double* C2, double* Bt, DenseScratch w, int* status);
+__global__ void congruence_kernel(int k, const double* G, const double* Cm, double* Bt, DenseScratch w);
 __global__ void pencil_direct_kernel(int k, const double* GA, const double* GB, double* vals, double* Y, double* At,
                                      double* Bt, double* X, DenseScratch w, int* status);
 __global__ void pencil_kernel(int k, const double* GA, const double* C2, const double* Bt, double* vals, double* Y,

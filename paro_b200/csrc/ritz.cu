@@ -508,6 +508,10 @@ int cgs2_orthonormalize(Ctx& ctx, const Op& B, int K, const double* U, double dr
 
 }  // namespace
 
+// smallest pivot ratio of the candidates' ordered Cholesky for which the basis
+// change stays in K x K arithmetic (one pass; step4.py ONE_PASS_RATIO)
+constexpr double kOnePassRatio = 0.5;
+
 int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, long long ld, size_t min_keep,
                   double drop_tol, double* lambdas, double* V, long long ldv, int* k_out, double* defect,
                   RitzInfo* info) {
@@ -564,7 +568,7 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
     return read_double(ctx, s.defect);
   };
 
-  double d = 0.0;
+  double d = 0.0, rmin = 0.0;
   if (!use_cgs) {
     // CholQR pass 1: Gram of the candidates, ordered Cholesky with drops
     apply_op(ctx, B, nullptr, 0.0, K, U, ld, W, n);
@@ -573,13 +577,37 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
     ++ctx.launches;
     PARO_CUDA(cudaGetLastError());
     k = read_int(ctx, s.kout);
-    const double rmin = read_double(ctx, s.rmin);
+    rmin = read_double(ctx, s.rmin);
     if (info) info->min_ratio = rmin;
     // Cholesky pivots lose ~eps/ratio^2 relative accuracy: near-dependent
     // candidates (and every drop decision) go through the CGS2 path instead
     if (rmin < 1e-5) use_cgs = true;
   }
-  if (!use_cgs) {
+  bool one_pass = false;
+  const bool aliased = V < U + static_cast<long long>(K) * ld && U < V + static_cast<long long>(K) * ldv;
+  if (!use_cgs && k == K && rmin >= kOnePassRatio && !aliased && !ctx.two_pass_only) {
+    // well-conditioned candidates (the steady state of the outer iteration:
+    // the Step-3 solutions are nearly B-orthonormal): the basis change stays
+    // in K x K arithmetic -- At = C1^T (U^T A U) C1, Bt = C1^T (U^T B U) C1,
+    // both Grams of the actual candidates -- and the lift is V = U (C1 X);
+    // no intermediate basis is formed (one rotation, apply and Gram less).
+    // The certificate below still measures the actual V.
+    const int cs = check_count(k);
+    if (cs != kOk) return cs;
+    congruence_kernel<<<1, kDenseThreads, 0, st>>>(k, s.G, s.C1, s.Bt, s.w);
+    ++ctx.launches;
+    apply_op(ctx, A, nullptr, 0.0, k, U, ld, W, n);
+    gram(ctx, k, U, ld, W, n, s.GA);
+    dense_configure();
+    pencil_kernel<<<1, kDenseThreads, dense_jacobi_smem(k), st>>>(k, s.GA, s.C1, s.Bt, s.vals, s.Y, s.At, s.X, s.w, s.status);
+    ++ctx.launches;
+    if (read_int(ctx, s.status) == kOk) {
+      d = finish(U, k);
+      one_pass = d <= 1e-8;
+    }
+    // a failed pencil or certificate falls through to the two-pass path
+  }
+  if (!use_cgs && !one_pass) {
     const int cs = check_count(k);
     if (cs != kOk) return cs;
     rotate(ctx, K, k, U, ld, s.C1, K, Q1, n, true);
@@ -657,6 +685,14 @@ int ritz_second_pass(Ctx& ctx, int k, const double* G2, double* C2, double* Bt) 
     ctx.err = "rayleigh_ritz: second Cholesky-QR pass not positive definite";
     return kPencil;
   }
+  return kOk;
+}
+
+int ritz_congruence(Ctx& ctx, int k, const double* G, const double* C1, double* Bt) {
+  Small s = small_buffers(ctx, k);
+  congruence_kernel<<<1, kDenseThreads, 0, ctx.stream>>>(k, G, C1, Bt, s.w);
+  ++ctx.launches;
+  PARO_CUDA(cudaGetLastError());
   return kOk;
 }
 

@@ -31,6 +31,8 @@ void fix_sign_columns(Ctx& ctx, double* V, long long ld, int k);
 // lift Y (k x k); the certificate max |G - I| (lower triangle).
 int ritz_ortho(Ctx& ctx, int K, const double* G, double drop_tol, double* C1, int* k_out, double* min_ratio);
 int ritz_second_pass(Ctx& ctx, int k, const double* G2, double* C2, double* Bt);
+// one-pass variant: Bt = sym(C1^T sym(G) C1) from the raw Gram and its basis change (k x k, no drops)
+int ritz_congruence(Ctx& ctx, int k, const double* G, const double* C1, double* Bt);
 int ritz_pencil(Ctx& ctx, int k, const double* GA, const double* C2, const double* Bt, const double* GB,
                 double* vals_host, double* Y);
 double ritz_defect(Ctx& ctx, int k, const double* G);

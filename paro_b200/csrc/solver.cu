@@ -421,6 +421,11 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
     }
     PARO_CUDA(cudaEventSynchronize(ev[cur]));
     remaining = *hcount;
+    if (trace.on) {
+      const auto tn = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[pcg]   chunk done at %8.3f ms, active %d\n",
+                   std::chrono::duration<double, std::milli>(tn - trace.t0).count(), remaining);
+    }
     if (!more) {
       PARO_CUDA(cudaStreamSynchronize(st));
       remaining = *hcount;
@@ -473,6 +478,8 @@ void batched_pcg(Ctx& ctx, const OpDev& op_in, bool var, int K, const double* sr
       col_iters += static_cast<double>(cols[c].it);
       batch_iters = std::max(batch_iters, static_cast<double>(cols[c].it));
     }
+  if (trace.on)
+    std::fprintf(stderr, "[pcg] K=%d col_iters=%.0f batch_iters=%.0f loop %.3f ms\n", K, col_iters, batch_iters, ms);
   const int base = var ? 0 : 3;
   ctx.stats[base + 0] += ms * 1e-3;
   ctx.stats[base + 1] += static_cast<double>(n) * (88.0 * col_iters + (var ? 64.0 : 0.0) * batch_iters);

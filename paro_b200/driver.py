@@ -314,6 +314,9 @@ class GpuBackend:
     def ritz_second_pass(self, G2, k, C2, Bt):
         return self.core.ritz_second_pass(self.ctx, G2, k, C2, Bt)
 
+    def ritz_congruence(self, G, C1, k, Bt):
+        self.core.ritz_congruence(self.ctx, G, C1, k, Bt)
+
     def ritz_pencil(self, GA, C2, Bt, GB, k, Y):
         return self.core.ritz_pencil(self.ctx, GA, C2, Bt, GB, k, Y)
 

@@ -33,6 +33,7 @@ from dataclasses import dataclass
 CERT_TOL = 1e-8          # paro.cpp:171
 CGS_RATIO = 1e-5         # pivot/original ratio below which Cholesky-QR hands over to CGS2
 CGS_BLOCK = 8            # candidates per CGS2 block
+ONE_PASS_RATIO = 0.5     # pivot ratio from which the basis change stays in K x K arithmetic (ritz.cu kOnePassRatio)
 
 
 class Step4Error(RuntimeError):
@@ -86,6 +87,7 @@ class RitzInfo:
     k: int = 0
     min_ratio: float = 0.0
     cgs2: bool = False
+    one_pass: bool = False
 
 
 class Step4:
@@ -98,6 +100,7 @@ class Step4:
         self.slab = slab
         self._ws = {}
         self.force_cgs2 = False
+        self.two_pass_only = False
         self.info = RitzInfo()
 
     # work buffers [k, n] reused across calls
@@ -166,7 +169,29 @@ class Step4:
             # Cholesky pivots lose ~eps/ratio^2 relative accuracy: near-dependent
             # candidates (and every drop decision) go through CGS2 instead
             use_cgs = rmin < CGS_RATIO
-        if not use_cgs:
+        one_pass = False
+        if not use_cgs and k == K and rmin >= ONE_PASS_RATIO and not self.two_pass_only \
+                and U.data_ptr() != V.data_ptr():
+            # well-conditioned candidates (the steady state: Step-3 solutions are nearly
+            # B-orthonormal): the basis change stays in K x K arithmetic. Both Grams are those of
+            # the actual candidates, At = C1^T (U^T A U) C1, Bt = C1^T (U^T B U) C1, and the lift is
+            # V = U (C1 X): one rotation, one apply and one Gram less than forming Q1. The
+            # certificate still measures the actual V; a failure falls back to the two-pass path.
+            self._check_count(k, min_keep)
+            Bt = be.kk(k * k)
+            be.ritz_congruence(G, C1, k, Bt)
+            self._apply(A, U, k, W)
+            GA = self._gram(U, W, k)
+            Y = be.kk(k * k)
+            try:
+                lam = be.ritz_pencil(GA, C1, Bt, None, k, Y)
+            except N.PencilError:
+                lam = None
+            if lam is not None:
+                d = self._finish(U, Y, k, V, W, B, on_final)
+                one_pass = d <= CERT_TOL
+        info.one_pass = one_pass
+        if not use_cgs and not one_pass:
             self._check_count(k, min_keep)
             be.rotate(U, K, C1, K, k, Q1, s.e0, s.e1, 2)
             self._apply(B, Q1, k, W)

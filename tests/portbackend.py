@@ -199,6 +199,13 @@ class PortBackend:
         Bt[: k * k] = self._flat(b)
         return True
 
+    def ritz_congruence(self, G, C1, k, Bt):
+        g = self._mat(G, k, k)
+        g = 0.5 * (g + g.T)
+        c = self._mat(C1, k, k)
+        b = c.T @ g @ c
+        Bt[: k * k] = self._flat(0.5 * (b + b.T))
+
     def ritz_pencil(self, GA, C2, Bt, GB, k, Y):
         ga = self._mat(GA, k, k)
         ga = 0.5 * (ga + ga.T)

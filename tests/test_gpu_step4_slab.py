@@ -170,3 +170,41 @@ def test_orchestrated_ritz_equals_monolithic(force_cgs2):
         np.testing.assert_allclose(lam1, r.lambdas, rtol=1e-11)
         torch.testing.assert_close(orb1, r.orbitals, rtol=0, atol=1e-8 * r.orbitals.abs().max().item())
         assert d1 <= 1e-8
+
+
+def test_one_pass_ritz_matches_two_pass():
+    """Well-conditioned candidates (Step-3 solutions of a running KS iteration,
+    pivot ratios ~1) take the one-pass basis change (K x K congruence, lift
+    from the candidates themselves): same Ritz values to 1e-12 relative and the
+    same orbitals to rounding as the two-pass Cholesky-QR, bit-identical
+    between the orchestrated and the monolithic Step 4, certificate <= 1e-8."""
+    from paro_b200 import configs, core
+    from paro_b200.driver import GpuBackend, ParoRun
+
+    w = configs.get("water@s24")
+    be = GpuBackend(w)
+    run = ParoRun(w, be, timers=False)
+    for i in range(2):
+        run.step(i)
+    assert run.s4.info.one_pass and not run.s4.info.cgs2
+    K = run.k
+    half = run.half[:K].clone()
+    a_half = be.forms["half"]
+    s4 = run.s4
+    V1, V2 = be.empty(K, be.n), be.empty(K, be.n)
+    o1, l1, d1 = s4.ritz(half, a_half, be.mass, K, w.drop_tol, V1)
+    assert s4.info.one_pass and s4.info.min_ratio >= 0.5
+    s4.two_pass_only = True
+    o2, l2, d2 = s4.ritz(half, a_half, be.mass, K, w.drop_tol, V2)
+    s4.two_pass_only = False
+    assert not s4.info.one_pass
+    assert d1 <= 1e-8 and d2 <= 1e-8
+    np.testing.assert_allclose(l1, l2, rtol=1e-12, atol=1e-13)
+    torch.testing.assert_close(o1, o2, rtol=0, atol=1e-9 * o2.abs().max().item())
+    # the monolithic C-ABI Step 4 takes the same path with the same kernels
+    r = core.rayleigh_ritz(half, a_half, be.mass, K, w.drop_tol)
+    assert l1 == r.lambdas and d1 == r.gram_defect and torch.equal(o1, r.orbitals)
+    be.ctx.set_ritz_mode("cholqr2")
+    r2 = core.rayleigh_ritz(half, a_half, be.mass, K, w.drop_tol)
+    be.ctx.set_ritz_mode("cholqr")
+    assert l2 == r2.lambdas and torch.equal(o2, r2.orbitals)
