@@ -275,6 +275,7 @@ int paro_grid_init(paro_ctx* ctx, int subdivisions, double lo, double hi) {
     g.lo = lo;
     g.hi = hi;
     ctx->c.grid_set = true;
+    ctx->c.mass_state = 0;
     return kOk;
   });
 }
@@ -671,7 +672,13 @@ int paro_assemble_mass(paro_ctx* ctx, paro_op** out) {
   return guarded(ctx, [&] {
     AssembleSpec s;
     s.kind = kAsmMass;
-    return assemble_new(ctx, s, true, out);
+    const int st = assemble_new(ctx, s, true, out);
+    // a constant mass stencil lets integrate / norm_l2 / integrate_product run as nodal sums (fields.cu)
+    const Op& m = (*out)->o;
+    ctx->c.mass_state = m.var ? 2 : 1;
+    if (!m.var)
+      for (int o = 0; o < kSlots; ++o) ctx->c.mass_w[o] = m.w[o];
+    return st;
   });
 }
 

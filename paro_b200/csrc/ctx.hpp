@@ -93,8 +93,9 @@ struct Ctx {
   // [3] const-op seconds [4] const-op bytes [5] const-op column-iterations
   double stats[8] = {};
 
-  double mass_w[kSlots] = {};        // reference mass stencil on this grid
-  bool mass_set = false;
+  double mass_w[kSlots] = {};        // the P1 mass stencil of this grid when it is constant (fields.cu)
+  bool nodal_sums = true;            // integrate / norm_l2 / integrate_product as nodal sums when the mass is constant
+  int mass_state = 0;                // 0: mass not assembled yet, 1: constant (mass_w valid), 2: varies per dof
 
   void check_grid() const {
     if (!grid_set) throw ParoError(kInvalidArgument, "paro_b200: grid not initialised");

@@ -1,13 +1,15 @@
-// K x K dense kernels of Step 4, one warp per launch (compiled -fmad=false).
+// K x K dense kernels of Step 4, one block per launch (compiled -fmad=false).
 //
 // The reference solves the projected pencil with Cholesky + cyclic Jacobi +
 // back-substitution (dense_sym_geneig, proj/src/linalg.cpp:341-393;
 // jacobi_eig :243-302; cholesky :307-323; fix_sign :229-241). These kernels
 // perform the same floating-point operations in the same order (inner loops
-// that are independent across rows/columns are spread over the 32 lanes; the
-// order-sensitive sums run on one lane), so for an identical pencil the
+// that are independent across rows/columns are spread over the threads; the
+// order-sensitive sums stay sequential), so for an identical pencil the
 // eigenpairs are bit-identical to the CPU reference. K is at most a few
-// hundred, so a single warp keeps the whole solve in one launch.
+// hundred, so a single block keeps the whole solve in one launch: rows /
+// columns that are independent in the reference's loops go to different
+// threads, every element keeps its own summation order.
 #include "dense.hpp"
 
 namespace paro_b200 {
@@ -16,52 +18,56 @@ namespace {
 
 __device__ __forceinline__ double& at(double* m, int n, int i, int j) { return m[i * n + j]; }
 
-__device__ void warp_fill(double* m, int count, double v) {
-  for (int i = threadIdx.x; i < count; i += 32) m[i] = v;
-  __syncwarp();
-}
-
-// cholesky (linalg.cpp:307-323) on lane 0; returns false on a non-positive pivot.
-__device__ bool warp_cholesky(int n, const double* b, double* l) {
-  warp_fill(l, n * n, 0.0);
-  int ok = 1;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < n && ok; ++i) {
-      for (int j = 0; j <= i; ++j) {
-        double s = b[i * n + j];
-        for (int k = 0; k < j; ++k) s -= l[i * n + k] * l[j * n + k];
-        if (i == j) {
-          if (s <= 0.0) {
-            ok = 0;
-            break;
-          }
-          l[i * n + i] = sqrt(s);
-        } else {
-          l[i * n + j] = s / l[j * n + j];
-        }
-      }
+// cholesky (linalg.cpp:307-323), block-wide; returns false on a non-positive
+// pivot. Column by column: once columns < j are final, every row i >= j forms
+// s = b_ij - sum_{k<j} l_ik l_jk with k ascending, the reference's own sum
+// for that element, on its own thread.
+__device__ bool block_cholesky(int n, const double* b, double* l) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  __shared__ int chol_ok;
+  for (int i = tid; i < n * n; i += nt) l[i] = 0.0;
+  if (tid == 0) chol_ok = 1;
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    for (int i = j + tid; i < n; i += nt) {
+      double s = b[i * n + j];
+      for (int k = 0; k < j; ++k) s -= l[i * n + k] * l[j * n + k];
+      l[i * n + j] = s;
     }
+    __syncthreads();
+    if (tid == 0) {
+      const double s = l[j * n + j];
+      if (s <= 0.0) chol_ok = 0;
+      else l[j * n + j] = sqrt(s);
+    }
+    __syncthreads();
+    if (!chol_ok) return false;
+    const double d = l[j * n + j];
+    for (int i = j + 1 + tid; i < n; i += nt) l[i * n + j] = l[i * n + j] / d;
+    __syncthreads();
   }
-  ok = __shfl_sync(0xffffffffu, ok, 0);
-  __syncwarp();
-  return ok != 0;
+  return true;
 }
 
-// check_symmetric (linalg.cpp:325-337)
-__device__ bool warp_symmetric(int n, const double* m) {
-  int ok = 1;
-  if (threadIdx.x == 0) {
-    double scale = 0.0;
-    for (int i = 0; i < n; ++i)
-      for (int j = 0; j < n; ++j) scale = fmax(scale, fabs(m[i * n + j]));
-    for (int i = 0; i < n && ok; ++i)
-      for (int j = i + 1; j < n; ++j)
-        if (fabs(m[i * n + j] - m[j * n + i]) > 1e-12 * fmax(1.0, scale)) {
-          ok = 0;
-          break;
-        }
+// check_symmetric (linalg.cpp:325-337), block-wide (a max and an any: order-free)
+__device__ bool block_symmetric(int n, const double* m) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  __shared__ double sym_max[32];
+  double scale = 0.0;
+  for (int i = tid; i < n * n; i += nt) scale = fmax(scale, fabs(m[i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) scale = fmax(scale, __shfl_xor_sync(0xffffffffu, scale, o));
+  if ((tid & 31) == 0) sym_max[tid >> 5] = scale;
+  __syncthreads();
+  scale = 0.0;
+  for (int w = 0; w < (nt + 31) / 32; ++w) scale = fmax(scale, sym_max[w]);
+  const double bar = 1e-12 * fmax(1.0, scale);
+  int bad = 0;
+  for (int idx = tid; idx < n * n; idx += nt) {
+    const int i = idx / n, j = idx % n;
+    if (j > i && fabs(m[i * n + j] - m[j * n + i]) > bar) bad = 1;
   }
-  return __shfl_sync(0xffffffffu, ok, 0) != 0;
+  return __syncthreads_or(bad) == 0;
 }
 
 // fix_sign (linalg.cpp:229-241) on a strided vector, single thread.
@@ -192,59 +198,49 @@ __device__ void block_jacobi(int n, double* a_g, double* v_g, double tol, int ma
 // vals (n), X row-major n x n (columns = B-orthonormal eigenvectors).
 __device__ int dense_sym_geneig_warp(int n, const double* A, const double* B, double* vals, double* X,
                                      const DenseScratch& w) {
-  // launched with a whole block: the order-sensitive / small parts run on warp
-  // 0, the Jacobi rotations on every thread
-  const int lane = threadIdx.x;
-  __shared__ int st_sh;
-  if (threadIdx.x < 32) {
-    int st = kOk;
-    if (!warp_symmetric(n, A) || !warp_symmetric(n, B)) st = kPencil;
-    else if (!warp_cholesky(n, B, w.l)) st = kPencil;
-    if (st == kOk) {
-      // W = L^{-1} A, column j independent
-      for (int j = lane; j < n; j += 32) {
-        for (int i = 0; i < n; ++i) {
-          double s = A[i * n + j];
-          for (int k = 0; k < i; ++k) s -= w.l[i * n + k] * w.w[k * n + j];
-          w.w[i * n + j] = s / w.l[i * n + i];
-        }
-      }
-      __syncwarp();
-      // C = W L^{-T}, row i independent
-      for (int i = lane; i < n; i += 32) {
-        for (int j = 0; j < n; ++j) {
-          double s = w.w[i * n + j];
-          for (int k = 0; k < j; ++k) s -= w.c[i * n + k] * w.l[j * n + k];
-          w.c[i * n + j] = s / w.l[j * n + j];
-        }
-      }
-      __syncwarp();
-      for (int idx = lane; idx < n * n; idx += 32) {
-        const int i = idx / n, j = idx % n;
-        if (j > i) {
-          const double avg = 0.5 * (w.c[i * n + j] + w.c[j * n + i]);
-          w.a[i * n + j] = avg;
-          w.a[j * n + i] = avg;
-        } else if (j == i) {
-          w.a[i * n + i] = w.c[i * n + i];
-        }
-      }
+  // launched with a whole block; every phase spreads the reference's
+  // independent rows / columns over the threads
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (!block_symmetric(n, A) || !block_symmetric(n, B)) return kPencil;
+  if (!block_cholesky(n, B, w.l)) return kPencil;
+  // W = L^{-1} A, column j independent
+  for (int j = tid; j < n; j += nt) {
+    for (int i = 0; i < n; ++i) {
+      double s = A[i * n + j];
+      for (int k = 0; k < i; ++k) s -= w.l[i * n + k] * w.w[k * n + j];
+      w.w[i * n + j] = s / w.l[i * n + i];
     }
-    if (lane == 0) st_sh = st;
   }
   __syncthreads();
-  if (st_sh != kOk) return st_sh;
-  block_jacobi(n, w.a, w.v, 1e-12, 60, vals, X, w.order);
-  if (threadIdx.x < 32) {
-    // x = L^{-T} y per column, then fix_sign
-    for (int col = lane; col < n; col += 32) {
-      for (int ii = n - 1; ii >= 0; --ii) {
-        double s = X[ii * n + col];
-        for (int k = ii + 1; k < n; ++k) s -= w.l[k * n + ii] * X[k * n + col];
-        X[ii * n + col] = s / w.l[ii * n + ii];
-      }
-      fix_sign_seq(n, X + col, n);
+  // C = W L^{-T}, row i independent
+  for (int i = tid; i < n; i += nt) {
+    for (int j = 0; j < n; ++j) {
+      double s = w.w[i * n + j];
+      for (int k = 0; k < j; ++k) s -= w.c[i * n + k] * w.l[j * n + k];
+      w.c[i * n + j] = s / w.l[j * n + j];
     }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < n * n; idx += nt) {
+    const int i = idx / n, j = idx % n;
+    if (j > i) {
+      const double avg = 0.5 * (w.c[i * n + j] + w.c[j * n + i]);
+      w.a[i * n + j] = avg;
+      w.a[j * n + i] = avg;
+    } else if (j == i) {
+      w.a[i * n + i] = w.c[i * n + i];
+    }
+  }
+  __syncthreads();
+  block_jacobi(n, w.a, w.v, 1e-12, 60, vals, X, w.order);
+  // x = L^{-T} y per column, then fix_sign
+  for (int col = tid; col < n; col += nt) {
+    for (int ii = n - 1; ii >= 0; --ii) {
+      double s = X[ii * n + col];
+      for (int k = ii + 1; k < n; ++k) s -= w.l[k * n + ii] * X[k * n + col];
+      X[ii * n + col] = s / w.l[ii * n + ii];
+    }
+    fix_sign_seq(n, X + col, n);
   }
   __syncthreads();
   return kOk;
@@ -272,131 +268,175 @@ __global__ void geneig_kernel(int n, const double* A, const double* B, double* v
 // host re-checks near-threshold decisions with an explicit CGS2 pass).
 __global__ void ortho_from_gram_kernel(int K, const double* G, double drop_tol, int allow_drop, double* C,
                                        int* acc, int* kout, double* min_ratio, DenseScratch w, int* status) {
-  const int lane = threadIdx.x;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  __shared__ int sh_k, sh_st, sh_serial;
+  __shared__ double sh_rmin;
   // symmetric Gram (row-major) in w.a
-  for (int idx = lane; idx < K * K; idx += 32) {
+  for (int idx = tid; idx < K * K; idx += nt) {
     const int i = idx / K, j = idx % K;
     w.a[i * K + j] = 0.5 * (G[i + j * K] + G[j + i * K]);
+    w.l[idx] = 0.0;
   }
-  warp_fill(w.l, K * K, 0.0);
-  int k = 0;
-  int st = kOk;
-  double rmin = 1e300;
-  if (lane == 0) {
-    double* lrow = w.w;  // tentative row
-    for (int j = 0; j < K; ++j) {
-      const double g = w.a[j * K + j];
+  if (tid == 0) {
+    sh_k = 0;
+    sh_st = kOk;
+    sh_serial = 0;
+    sh_rmin = 1e300;
+  }
+  __syncthreads();
+  // Without drops (the usual case) the ordered Cholesky is a plain one: run it
+  // column by column with row j on its own thread -- l_jc = (a_jc - sum_{m<c}
+  // l_jm l_cm) / l_cc, d2_j -= l_jc^2 with c ascending, exactly the sequence
+  // of the row loop below -- and fall back to that loop from scratch at the
+  // first candidate that would be dropped.
+  double* d2 = w.v;  // remaining squared B-norm per candidate
+  for (int j = tid; j < K; j += nt) d2[j] = w.a[j * K + j];
+  __syncthreads();
+  for (int c = 0; c < K; ++c) {
+    if (tid == 0) {
+      const double g = w.a[c * K + c];
       const double orig = sqrt(fmax(0.0, g));
       if (!(orig > 0.0)) {
-        if (!allow_drop) {
-          st = kPencil;
-          break;
+        sh_serial = 1;
+      } else {
+        const double nb = sqrt(fmax(0.0, d2[c]));
+        sh_rmin = fmin(sh_rmin, nb / orig);
+        if (nb <= drop_tol * orig) sh_serial = 1;
+        else w.l[c * K + c] = nb;
+      }
+    }
+    __syncthreads();
+    if (sh_serial) break;
+    const double lcc = w.l[c * K + c];
+    for (int j = c + 1 + tid; j < K; j += nt) {
+      double sv = w.a[j * K + c];
+      for (int m = 0; m < c; ++m) sv -= w.l[j * K + m] * w.l[c * K + m];
+      const double v = sv / lcc;
+      w.l[j * K + c] = v;
+      d2[j] -= v * v;
+    }
+    __syncthreads();
+  }
+  if (!sh_serial) {
+    for (int j = tid; j < K; j += nt) acc[j] = j;
+    if (tid == 0) sh_k = K;
+  } else {
+    // ordered Cholesky with drops, one candidate row after the other
+    __syncthreads();
+    for (int idx = tid; idx < K * K; idx += nt) w.l[idx] = 0.0;
+    __syncthreads();
+    if (tid == 0) {
+      int k = 0, st = kOk;
+      double rmin = 1e300;
+      double* lrow = w.w;  // tentative row
+      for (int j = 0; j < K; ++j) {
+        const double g = w.a[j * K + j];
+        const double orig = sqrt(fmax(0.0, g));
+        if (!(orig > 0.0)) {
+          if (!allow_drop) {
+            st = kPencil;
+            break;
+          }
+          rmin = 0.0;
+          continue;
         }
-        rmin = 0.0;
-        continue;
-      }
-      double d2 = g;
-      for (int c = 0; c < k; ++c) {
-        double s = w.a[j * K + acc[c]];
-        for (int m = 0; m < c; ++m) s -= lrow[m] * w.l[c * K + m];
-        lrow[c] = s / w.l[c * K + c];
-        d2 -= lrow[c] * lrow[c];
-      }
-      const double nb = sqrt(fmax(0.0, d2));
-      const double ratio = nb / orig;
-      rmin = fmin(rmin, ratio);
-      if (nb <= drop_tol * orig) {
-        if (!allow_drop) {
-          st = kPencil;
-          break;
+        double dd = g;
+        for (int c = 0; c < k; ++c) {
+          double sv = w.a[j * K + acc[c]];
+          for (int m = 0; m < c; ++m) sv -= lrow[m] * w.l[c * K + m];
+          lrow[c] = sv / w.l[c * K + c];
+          dd -= lrow[c] * lrow[c];
         }
-        continue;
+        const double nb = sqrt(fmax(0.0, dd));
+        const double ratio = nb / orig;
+        rmin = fmin(rmin, ratio);
+        if (nb <= drop_tol * orig) {
+          if (!allow_drop) {
+            st = kPencil;
+            break;
+          }
+          continue;
+        }
+        for (int c = 0; c < k; ++c) w.l[k * K + c] = lrow[c];
+        w.l[k * K + k] = nb;
+        acc[k] = j;
+        ++k;
       }
-      for (int c = 0; c < k; ++c) w.l[k * K + c] = lrow[c];
-      w.l[k * K + k] = nb;
-      acc[k] = j;
-      ++k;
+      sh_k = k;
+      sh_st = st;
+      sh_rmin = rmin;
     }
   }
-  k = __shfl_sync(0xffffffffu, k, 0);
-  st = __shfl_sync(0xffffffffu, st, 0);
-  __syncwarp();
+  __syncthreads();
+  const int k = sh_k;
   // Linv = L^{-1} (lower), column j independent
-  for (int j = lane; j < k; j += 32) {
+  for (int j = tid; j < k; j += nt) {
     for (int i = 0; i < k; ++i) {
-      double s = i == j ? 1.0 : 0.0;
-      for (int m = j; m < i; ++m) s -= w.l[i * K + m] * w.c[m * K + j];
-      w.c[i * K + j] = i < j ? 0.0 : s / w.l[i * K + i];
+      double sv = i == j ? 1.0 : 0.0;
+      for (int m = j; m < i; ++m) sv -= w.l[i * K + m] * w.c[m * K + j];
+      w.c[i * K + j] = i < j ? 0.0 : sv / w.l[i * K + i];
     }
   }
-  __syncwarp();
   // C[acc[i], j] = Linv^T[i][j] = Linv[j][i]
-  for (int idx = lane; idx < K * k; idx += 32) {
-    const int r = idx % K, j = idx / K;
-    C[r + j * K] = 0.0;
-  }
-  __syncwarp();
-  for (int idx = lane; idx < k * k; idx += 32) {
+  for (int idx = tid; idx < K * k; idx += nt) C[idx] = 0.0;
+  __syncthreads();
+  for (int idx = tid; idx < k * k; idx += nt) {
     const int i = idx / k, j = idx % k;
     C[acc[i] + j * K] = w.c[j * K + i];
   }
-  if (lane == 0) {
+  if (tid == 0) {
     *kout = k;
-    *min_ratio = rmin;
-    *status = st;
+    *min_ratio = sh_rmin;
+    *status = sh_st;
   }
 }
 
 // Second CholQR pass on G2 = Q1^T B Q1 (k x k, column-major): L2 = chol(G2),
 // C2 = L2^{-T} (column-major k x k), Bt = L2^{-1} G2 L2^{-T} (row-major, ~I).
 __global__ void second_pass_kernel(int k, const double* G2, double* C2, double* Bt, DenseScratch w, int* status) {
-  const int lane = threadIdx.x;
-  for (int idx = lane; idx < k * k; idx += 32) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int idx = tid; idx < k * k; idx += nt) {
     const int i = idx / k, j = idx % k;
     w.a[i * k + j] = 0.5 * (G2[i + j * k] + G2[j + i * k]);
   }
-  __syncwarp();
-  if (!warp_cholesky(k, w.a, w.l)) {
-    if (lane == 0) *status = kPencil;
+  __syncthreads();
+  if (!block_cholesky(k, w.a, w.l)) {
+    if (tid == 0) *status = kPencil;
     return;
   }
   // Linv
-  for (int j = lane; j < k; j += 32) {
+  for (int j = tid; j < k; j += nt) {
     for (int i = 0; i < k; ++i) {
       double s = i == j ? 1.0 : 0.0;
       for (int m = j; m < i; ++m) s -= w.l[i * k + m] * w.c[m * k + j];
       w.c[i * k + j] = i < j ? 0.0 : s / w.l[i * k + i];
     }
   }
-  __syncwarp();
-  for (int idx = lane; idx < k * k; idx += 32) {
+  __syncthreads();
+  for (int idx = tid; idx < k * k; idx += nt) {
     const int i = idx / k, j = idx % k;
     C2[i + j * k] = w.c[j * k + i];  // L2^{-T}
   }
   // Bt = Linv * Gs * Linv^T
-  for (int idx = lane; idx < k * k; idx += 32) {
+  for (int idx = tid; idx < k * k; idx += nt) {
     const int i = idx / k, j = idx % k;
     double s = 0.0;
     for (int m = 0; m <= i; ++m) s += w.c[i * k + m] * w.a[m * k + j];
     w.w[i * k + j] = s;
   }
-  __syncwarp();
-  for (int idx = lane; idx < k * k; idx += 32) {
+  __syncthreads();
+  for (int idx = tid; idx < k * k; idx += nt) {
     const int i = idx / k, j = idx % k;
     double s = 0.0;
     for (int m = 0; m <= j; ++m) s += w.w[i * k + m] * w.c[j * k + m];
-    Bt[i * k + j] = s;
+    w.v[i * k + j] = s;
   }
-  __syncwarp();
-  for (int idx = lane; idx < k * k; idx += 32) {
+  __syncthreads();
+  for (int idx = tid; idx < k * k; idx += nt) {
     const int i = idx / k, j = idx % k;
-    if (j > i) {
-      const double avg = 0.5 * (Bt[i * k + j] + Bt[j * k + i]);
-      Bt[i * k + j] = avg;
-      Bt[j * k + i] = avg;
-    }
+    Bt[i * k + j] = i == j ? w.v[idx] : 0.5 * (w.v[i * k + j] + w.v[j * k + i]);
   }
-  if (lane == 0) *status = kOk;
+  if (tid == 0) *status = kOk;
 }
 
 // One-pass basis change: Bt = sym(C^T sym(G) C) (row-major k x k) for the raw

@@ -573,7 +573,7 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
     // CholQR pass 1: Gram of the candidates, ordered Cholesky with drops
     apply_op(ctx, B, nullptr, 0.0, K, U, ld, W, n);
     gram(ctx, K, U, ld, W, n, s.G);
-    ortho_from_gram_kernel<<<1, 32, 0, st>>>(K, s.G, drop_tol, 1, s.C1, s.acc, s.kout, s.rmin, s.w, s.status);
+    ortho_from_gram_kernel<<<1, kDenseThreads, 0, st>>>(K, s.G, drop_tol, 1, s.C1, s.acc, s.kout, s.rmin, s.w, s.status);
     ++ctx.launches;
     PARO_CUDA(cudaGetLastError());
     k = read_int(ctx, s.kout);
@@ -614,7 +614,7 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
     // pass 2
     apply_op(ctx, B, nullptr, 0.0, k, Q1, n, W, n);
     gram(ctx, k, Q1, n, W, n, s.G2);
-    second_pass_kernel<<<1, 32, 0, st>>>(k, s.G2, s.C2, s.Bt, s.w, s.status);
+    second_pass_kernel<<<1, kDenseThreads, 0, st>>>(k, s.G2, s.C2, s.Bt, s.w, s.status);
     ++ctx.launches;
     if (read_int(ctx, s.status) != kOk) {
       use_cgs = true;
@@ -668,7 +668,7 @@ int rayleigh_ritz(Ctx& ctx, const Op& A, const Op& B, int K, const double* U, lo
 // before each stage; every rank then runs the same stage on the same input).
 int ritz_ortho(Ctx& ctx, int K, const double* G, double drop_tol, double* C1, int* k_out, double* min_ratio) {
   Small s = small_buffers(ctx, K);
-  ortho_from_gram_kernel<<<1, 32, 0, ctx.stream>>>(K, G, drop_tol, 1, C1, s.acc, s.kout, s.rmin, s.w, s.status);
+  ortho_from_gram_kernel<<<1, kDenseThreads, 0, ctx.stream>>>(K, G, drop_tol, 1, C1, s.acc, s.kout, s.rmin, s.w, s.status);
   ++ctx.launches;
   PARO_CUDA(cudaGetLastError());
   *k_out = read_int(ctx, s.kout);
@@ -678,7 +678,7 @@ int ritz_ortho(Ctx& ctx, int K, const double* G, double drop_tol, double* C1, in
 
 int ritz_second_pass(Ctx& ctx, int k, const double* G2, double* C2, double* Bt) {
   Small s = small_buffers(ctx, k);
-  second_pass_kernel<<<1, 32, 0, ctx.stream>>>(k, G2, C2, Bt, s.w, s.status);
+  second_pass_kernel<<<1, kDenseThreads, 0, ctx.stream>>>(k, G2, C2, Bt, s.w, s.status);
   ++ctx.launches;
   PARO_CUDA(cudaGetLastError());
   if (read_int(ctx, s.status) != kOk) {

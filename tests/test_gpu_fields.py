@@ -98,3 +98,32 @@ def test_ks_form_and_fields(ref, gpu_ctx_factory):
     mixed = core.mix_density(ctx, _dev(rho_ref), _dev(r2), 0.3).cpu().numpy()
     np.testing.assert_array_equal(mixed, ref.mix(sp, rho_ref, r2, 0.3))
     assert abs(core.norm_l2(ctx, _dev(r2)) - ref.norm_l2(sp, r2)) <= 1e-13 * ref.norm_l2(sp, r2)
+
+
+@pytest.mark.parametrize("s,lo,hi,uniform", [(12, -6.0, 6.0, True), (16, -10.0, 10.0, True), (10, -7.0, 7.0, False)])
+def test_nodal_sums_match_element_sums(ref, gpu_ctx_factory, s, lo, hi, uniform):
+    """integrate / norm_l2 / integrate_product (fem.cpp:419-448, model.cpp:306-327):
+    once the context knows the grid's mass as one constant stencil
+    (exact-binary spacings) they run as nodal sums f' M g / (int phi) sum f;
+    both forms against the reference's element loops, and against each other
+    (a second context that never assembled the mass stays on the element loop)."""
+    from paro_b200 import core
+
+    sp = ref.Space(s, lo, hi)
+    ctx_el = gpu_ctx_factory(s, lo, hi)          # element loops
+    ctx = gpu_ctx_factory(s, lo, hi)
+    m = core.assemble_mass(ctx)                  # records the stencil
+    assert m.variable is (not uniform)
+    rng = np.random.default_rng(s)
+    f = rng.uniform(0.0, 2.0, sp.n)
+    g = rng.standard_normal(sp.n)
+    fd, gd = _dev(f), _dev(g)
+    mass = ref.Op.mass(sp)
+    for c in (ctx, ctx_el):
+        i_ref = ref.integrate(sp, f)
+        assert abs(core.integrate(c, fd) - i_ref) <= 1e-13 * abs(i_ref)
+        n_ref = ref.norm_l2(sp, g)
+        assert abs(core.norm_l2(c, gd) - n_ref) <= 1e-13 * n_ref
+        p_ref = float(f @ mass.matvec(g))        # integrate_product == f' M g on Dirichlet functions
+        scale = float(np.abs(f) @ mass.matvec(np.abs(g)))
+        assert abs(core.integrate_product(c, fd, gd) - p_ref) <= 1e-13 * scale

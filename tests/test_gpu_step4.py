@@ -22,7 +22,7 @@ def test_dense_sym_geneig_bit_exact(ref, gpu_ctx_factory):
 
     ctx = gpu_ctx_factory(4, 0.0, 1.0)
     rng = np.random.default_rng(5)
-    for m in (1, 2, 7, 12, 40):
+    for m in (1, 2, 7, 12, 40, 76, 131):  # 131 > the block's thread count: strided rows
         X = rng.standard_normal((m, m))
         A = X + X.T
         Y = rng.standard_normal((m, m))
@@ -40,6 +40,12 @@ def test_dense_sym_geneig_bit_exact(ref, gpu_ctx_factory):
 
     with pytest.raises(PencilError):
         core.dense_sym_geneig(ctx, np.eye(2), np.diag([1.0, -1.0]))
+    with pytest.raises(PencilError):  # check_symmetric (linalg.cpp:325-337)
+        core.dense_sym_geneig(ctx, np.array([[1.0, 2.0], [2.0 + 1e-6, 1.0]]), np.eye(2))
+    B40 = np.eye(40)
+    B40[37, 37] = -1.0  # the pivot fails late: every earlier column is already final
+    with pytest.raises(PencilError):
+        core.dense_sym_geneig(ctx, np.eye(40), B40)
 
 
 def test_rayleigh_ritz_matches_reference(ref, gpu_ctx_factory):

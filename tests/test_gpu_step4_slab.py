@@ -208,3 +208,38 @@ def test_one_pass_ritz_matches_two_pass():
     r2 = core.rayleigh_ritz(half, a_half, be.mass, K, w.drop_tol)
     be.ctx.set_ritz_mode("cholqr")
     assert l2 == r2.lambdas and torch.equal(o2, r2.orbitals)
+
+
+@pytest.mark.parametrize("K,dependent", [(9, ()), (76, ()), (140, ()), (12, (5,)), (40, (0, 17, 39))])
+def test_ritz_ortho_parallel_and_drop_paths(K, dependent):
+    """ortho_from_gram_kernel: the column-parallel Cholesky (no drops) and the
+    ordered row loop (taken from the first dropped candidate on) against the
+    numpy restatement of the same ordered Cholesky (tests/portbackend.py):
+    same accepted set, pivot ratio and basis change."""
+    from portbackend import PortBackend
+
+    from paro_b200 import core
+
+    ctx = core.Context(0).grid(8, -1.0, 1.0)
+    rng = np.random.default_rng(K)
+    n = 400
+    U = rng.standard_normal((n, K))
+    for j in dependent:  # candidate j in the span of the others (dropped), or zero (j == 0)
+        U[:, j] = 0.0 if j == 0 else U[:, :j] @ rng.standard_normal(j)
+    G = U.T @ U
+    Gd = torch.as_tensor(G.T.reshape(-1).copy(), device="cuda")  # column-major
+    C1 = torch.zeros(K * K, dtype=torch.float64, device="cuda")
+    k, rmin = core.ritz_ortho(ctx, Gd, K, 1e-6, C1)
+    pb = PortBackend.__new__(PortBackend)
+    C1p = torch.zeros(K * K, dtype=torch.float64)
+    kp, rminp = PortBackend.ritz_ortho(pb, torch.as_tensor(G.T.reshape(-1).copy()), K, 1e-6, C1p)
+    assert k == kp == K - len(dependent)
+    if dependent:
+        assert rmin <= 1e-6 and rminp <= 1e-6     # a dropped candidate: ratio at rounding level (~1e-8)
+    else:
+        assert abs(rmin - rminp) <= 1e-12 * rminp
+    Cg = C1.cpu().numpy()[: K * k].reshape(k, K).T
+    Cp = C1p.numpy()[: K * k].reshape(k, K).T
+    np.testing.assert_allclose(Cg, Cp, rtol=0, atol=1e-9 * np.abs(Cp).max())
+    Q = U @ Cg
+    np.testing.assert_allclose(Q.T @ Q, np.eye(k), atol=1e-8)
