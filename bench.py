@@ -201,6 +201,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=int(os.environ.get("PARO_E2E_CHUNKS", "2")),
                     help="column chunks of the host->device orbital copy in the e2e replay")
+    ap.add_argument("--e2e-blocking", action="store_true",
+                    help="e2e replay with blocking step_host calls (no overlap of a step's copy-out with the next copy-in)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -326,7 +328,9 @@ def main():
         else:
             e0.record()
             for i in range(args.steps):
-                tr = run.step_host(args.warmup + i, h_orb, h_rho, chunks=args.e2e_chunks)
+                tr = run.step_host(args.warmup + i, h_orb, h_rho, chunks=args.e2e_chunks,
+                                   pipelined=not args.e2e_blocking)
+            run.host_join()  # the last step's copy-out ends inside the timed region
             e1.record()
             torch.cuda.synchronize()
             e_ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda", dtype=torch.float64)
@@ -337,8 +341,11 @@ def main():
         e2e = {"value": 1000.0 / float(e_ms.item()), "unit": UNIT, "h2d_bytes_per_step": bytes_in,
                "d2h_bytes_per_step": bytes_in, "replay_identical": tr.lambdas == traces[-1].lambdas,
                "path": "ParoRun.step_host (paro_b200 C ABI) replaying the timed steps: pinned host orbitals + "
-                       "density in, new orbitals + mixed density out, copies on a side stream overlapping the "
-                       "density-only work and the Step-3 solves of already-arrived column chunks"}
+                       "density in, new orbitals + mixed density out, copies on side streams overlapping the "
+                       "density-only work and the Step-3 solves of already-arrived column chunks"
+                       + ("" if args.e2e_blocking or single else "; calls are stream-ordered: a step's copy-out "
+                          "overlaps the next step's copy-in chunk by chunk (each chunk's copy-in waits for its "
+                          "copy-out), the last copy-out is inside the timed region")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

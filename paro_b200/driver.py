@@ -480,6 +480,13 @@ class ParoRun:
         self._chunks = None      # step_host: (c0, c1, copy event) of the local Step-3 columns
         self._waited = set()     # step_host: ids of the chunk events the compute stream already waits on
         self._copy_stream = None
+        # step_host(pipelined=True): copy-out stream, the previous step's copy-out events per column
+        # chunk / of the density, and the compute stream's last read of the device state
+        self._out_stream = None
+        self._later_out = None
+        self._d2h_events = []
+        self._rho_out_event = None
+        self._post_read = None
         self.timeline = None     # profiling: list of (label, CUDA event) marks, or None
 
     def _mark(self, label, stream=None):
@@ -596,9 +603,10 @@ class ParoRun:
     def _wait_chunk(self, ev):
         """step_host: make the compute stream wait for one column chunk's host
         copy (once per step, whichever attempt or probe first needs it)."""
-        if ev is not None and id(ev) not in self._waited:
-            torch.cuda.current_stream(self.be.device).wait_event(ev)
-            self._waited.add(id(ev))
+        for e in (ev if isinstance(ev, (list, tuple)) else [ev]):
+            if e is not None and id(e) not in self._waited:
+                torch.cuda.current_stream(self.be.device).wait_event(e)
+                self._waited.add(id(e))
 
     def _wait_chunks(self):
         for _, _, ev in self._chunks or ():
@@ -635,21 +643,44 @@ class ParoRun:
         self._hooked = False
         if self._out is None or self.dist.world > 1:
             return None
-        cs, h_orb = self._out
+        cs, h_orb = self._out[:2]
         main = torch.cuda.current_stream(self.be.device)
 
         def hook(V, k):
-            o0, o1, _ = self.dist.shard(k)
             cs.wait_stream(main)
             with torch.cuda.stream(cs):
                 self._mark("d2h_start", cs)
-                h_orb[o0:o1].copy_(V[o0:o1], non_blocking=True)
-                ev = cs.record_event()
+                ev = self._copy_out_chunks(cs, h_orb, V, k)
                 self._mark("d2h_end", cs)
             self._hooked = True
             return lambda: main.wait_event(ev)
 
         return hook
+
+    def _copy_out_chunks(self, cs, h_orb, V, k):
+        """This rank's block of the new orbitals to the host on stream cs (current),
+        in the column chunks of the pipelined step_host when it set them (one
+        event per chunk: the next step's copy-in of a chunk waits only for that
+        chunk's copy-out). Returns the event after the last copy."""
+        o0, o1, _ = self.dist.shard(k)
+        pipelined = len(self._out) > 2
+        ranges = self._out[2] if pipelined and self._out[2] else [(o0, o1)]
+        self._d2h_events = []
+        self._later_out = None
+        ev = None
+        for i, (k0, k1) in enumerate(ranges):
+            a, b = max(k0, o0), min(k1, o1)
+            if b <= a:
+                continue
+            if pipelined and i > 0:
+                # the DMA queue is first-in first-out: the later pieces are queued at the end of
+                # the step, behind the density's copy-out, which the next step needs first
+                self._later_out = (V, [(max(p, o0), min(q, o1)) for p, q in ranges[i:]])
+                break
+            h_orb[a:b].copy_(V[a:b], non_blocking=True)
+            ev = cs.record_event()
+            self._d2h_events.append((a, b, ev))
+        return ev if ev is not None else cs.record_event()
 
     def _to_columns(self):
         """Step 4's row slabs back to column shards for the next Step 3 (one
@@ -662,16 +693,15 @@ class ParoRun:
 
     def _copy_out(self, orb):
         """step_host: this rank's block of the new orbitals to the host (side stream)."""
-        cs, h_orb = self._out
-        o0, o1, _ = self.dist.shard(orb.shape[0])
+        cs, h_orb = self._out[:2]
         cs.wait_stream(torch.cuda.current_stream(self.be.device))
         with torch.cuda.stream(cs):
             self._mark("d2h_start", cs)
-            h_orb[o0:o1].copy_(orb[o0:o1], non_blocking=True)
+            self._copy_out_chunks(cs, h_orb, orb, orb.shape[0])
             self._mark("d2h_end", cs)
 
     def step_host(self, it: int, h_orb: torch.Tensor, h_rho: torch.Tensor | None = None,
-                  chunks: int = 2) -> Trace:
+                  chunks: int = 2, pipelined: bool = False) -> Trace:
         """One outer iteration with the state in (pinned) host memory, the way
         a host caller of the reference interface holds it: the orbitals (and,
         for Kohn-Sham, the input density) are copied in, the new orbitals and
@@ -679,7 +709,15 @@ class ParoRun:
         the orbitals arrive in column chunks while the density-only work and
         the Step-3 solves of the earlier chunks run, and leave while the
         post-Step-4 density work runs. Returns when everything is back on the
-        host side (h_orb, h_rho updated in place)."""
+        host side (h_orb, h_rho updated in place).
+
+        pipelined=True makes the call stream-ordered instead: the copy-out runs
+        on its own stream and the call returns without waiting for it; the next
+        pipelined call's copy-in of a column chunk waits (on the device) for that
+        chunk's copy-out only, so over PCIe's two directions a step's copy-out
+        overlaps the next step's copy-in and first solves. The data still make
+        the round trip through h_orb / h_rho every step; call host_join() before
+        reading or writing them from the host."""
         be, d = self.be, self.dist
         dev = be.device
         main = torch.cuda.current_stream(dev)
@@ -688,7 +726,19 @@ class ParoRun:
         cs = self._copy_stream
         K = self.k
         c0, c1, _ = d.shard(K)
-        cs.wait_stream(main)
+        if pipelined:
+            if self._out_stream is None:
+                self._out_stream = torch.cuda.Stream(dev)
+            # the copy-in overwrites device state the previous step still read at its end
+            if self._post_read is not None:
+                cs.wait_event(self._post_read)
+            else:
+                cs.wait_stream(main)
+            if self._rho_out_event is not None:
+                cs.wait_event(self._rho_out_event)
+        else:
+            self.host_join()
+            cs.wait_stream(main)
         with torch.cuda.stream(cs):
             if h_rho is not None:
                 self.rho_in.copy_(h_rho, non_blocking=True)
@@ -705,24 +755,63 @@ class ParoRun:
             else:
                 bounds = [c0 + (kl * i) // chunks for i in range(chunks + 1)]
             ranges = [(bounds[i], bounds[i + 1]) for i in range(chunks) if bounds[i + 1] > bounds[i]]
+            # pipelined: the copies move in finer pieces than the solves (a piece's copy-in
+            # starts as soon as the previous step's copy-out of that piece is done), the
+            # Step-3 batches stay the `ranges` and wait for every piece they contain
+            pieces = ranges
+            if pipelined:
+                pieces = []
+                for k0, k1 in ranges:
+                    m = max(1, -(-(k1 - k0) // 20))
+                    pieces += [(k0 + ((k1 - k0) * i) // m, k0 + ((k1 - k0) * (i + 1)) // m) for i in range(m)]
             evs = []
             self._mark("h2d_start", cs)
-            for k0, k1 in ranges:
+            for k0, k1 in pieces:
+                for a, b, ev in self._d2h_events:  # pipelined: the previous step's copy-out of these columns
+                    if a < k1 and k0 < b:
+                        cs.wait_event(ev)
                 self.orb[k0:k1].copy_(h_orb[k0:k1], non_blocking=True)
                 evs.append(cs.record_event())
                 self._mark(f"h2d_cols_{k0}_{k1}", cs)
-        self._chunks = [(k0, k1, ev) for (k0, k1), ev in zip(ranges, evs)]
+        self._d2h_events = []
+        self._chunks = [(k0, k1, [ev for (a, b), ev in zip(pieces, evs) if a < k1 and k0 < b]) for k0, k1 in ranges]
         self._waited = set()
-        self._out = (cs, h_orb)
+        self._out = (self._out_stream, h_orb, pieces) if pipelined else (cs, h_orb)
         try:
             tr = self.step(it)
         finally:
             self._chunks, self._out = None, None
         main.wait_event(evs[-1])
-        if h_rho is not None:
-            h_rho.copy_(self.rho_in, non_blocking=True)
-        main.wait_stream(cs)
+        if not pipelined:
+            if h_rho is not None:
+                h_rho.copy_(self.rho_in, non_blocking=True)
+            main.wait_stream(cs)
+            self._d2h_events = []
+            return tr
+        self._post_read = main.record_event()  # every read of the device orbitals / densities of this step
+        co = self._out_stream
+        with torch.cuda.stream(co):
+            if h_rho is not None:
+                co.wait_event(self._post_read)
+                h_rho.copy_(self.rho_in, non_blocking=True)
+                self._rho_out_event = co.record_event()
+            if self._later_out is not None:  # the rest of the orbitals (the first piece left inside Step 4)
+                V, rest = self._later_out
+                for a, b in rest:
+                    if b > a:
+                        h_orb[a:b].copy_(V[a:b], non_blocking=True)
+                        self._d2h_events.append((a, b, co.record_event()))
+                self._later_out = None
         return tr
+
+    def host_join(self):
+        """Make the current stream wait for the copy-outs of pipelined step_host
+        calls (then a device synchronise makes h_orb / h_rho readable)."""
+        if self._out_stream is not None:
+            torch.cuda.current_stream(self.be.device).wait_stream(self._out_stream)
+        self._d2h_events = []
+        self._rho_out_event = None
+        self._post_read = None
 
     def _ks_step(self, it: int) -> Trace:
         """paro.cpp:514-638 with adaptive = false; no stop tests."""

@@ -104,3 +104,49 @@ def test_step_host_matches_device_step(name, chunks):
         b.orb.normal_()
     if w.kind == "linear":
         assert b.probe_hits >= 1 and b.probe_hits == a.probe_hits
+
+
+@pytest.mark.parametrize("name,chunks", [("h2@s16", 2), ("water@s24", 2), ("source64@s24", 3)])
+def test_step_host_pipelined_matches_device_step(name, chunks):
+    """step_host(pipelined=True): stream-ordered calls whose copy-out overlaps
+    the next call's copy-in piece by piece. Four back-to-back steps with no
+    host synchronisation in between follow the device-resident trajectory bit
+    for bit (the state makes the round trip through the host buffers: the
+    device copies are scrambled on the compute stream after every step, in
+    order after the step's own reads), and after host_join + synchronise the
+    host buffers hold the last step's orbitals and density."""
+    from paro_b200 import configs
+    from paro_b200.driver import GpuBackend, ParoRun
+
+    w = configs.get(name)
+    a = ParoRun(w, GpuBackend(w))
+    b = ParoRun(w, GpuBackend(w))
+    h_orb = torch.empty((b.k, b.be.n), dtype=torch.float64, pin_memory=True)
+    h_orb.copy_(b.orb[: b.k])
+    h_rho = None
+    if w.kind == "ks":
+        h_rho = torch.empty((b.be.n,), dtype=torch.float64, pin_memory=True)
+        h_rho.copy_(b.rho_in)
+    torch.cuda.synchronize()
+    ta, tb = [], []
+    for it in range(4):
+        ta.append(a.step(it))
+    for it in range(4):
+        tb.append(b.step_host(it, h_orb, h_rho, chunks=chunks, pipelined=True))
+        # what the next step must NOT use: the device copies, scrambled on the compute stream
+        # once this step's copy-out has read them
+        if it < 3:
+            main = torch.cuda.current_stream()
+            main.wait_stream(b._out_stream)
+            b.orb.normal_()
+            if h_rho is not None:
+                b.rho_in.normal_()
+            b._post_read = main.record_event()  # the next copy-in follows the scramble (event chain kept)
+    b.host_join()
+    torch.cuda.synchronize()
+    for x, y in zip(ta, tb):
+        assert x.lambdas == y.lambdas and x.e_tot == y.e_tot and x.cg_iterations == y.cg_iterations
+        assert x.sigma == y.sigma
+    assert torch.equal(h_orb[: a.k], a.orb[: a.k].cpu())
+    if h_rho is not None:
+        assert torch.equal(h_rho, a.rho_in.cpu())
