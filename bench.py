@@ -311,6 +311,8 @@ def main():
         del snap
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0_, c1_, _ = dist.shard(K0)
+        pipelined = False
         if world > 1:
             td.barrier()
         if single:
@@ -326,10 +328,12 @@ def main():
                 e_tot_ms += e0.elapsed_time(e1)
             e_ms = torch.tensor([e_tot_ms / args.steps], device="cuda", dtype=torch.float64)
         else:
+            # stream-ordered calls pay off when the copies are long (>= 64 MB of orbitals per
+            # rank); steps of a few ms keep the blocking calls (fewer events and streams)
+            pipelined = not args.e2e_blocking and h_orb[c0_:c1_].numel() * 8 >= (64 << 20)
             e0.record()
             for i in range(args.steps):
-                tr = run.step_host(args.warmup + i, h_orb, h_rho, chunks=args.e2e_chunks,
-                                   pipelined=not args.e2e_blocking)
+                tr = run.step_host(args.warmup + i, h_orb, h_rho, chunks=args.e2e_chunks, pipelined=pipelined)
             run.host_join()  # the last step's copy-out ends inside the timed region
             e1.record()
             torch.cuda.synchronize()
@@ -343,7 +347,7 @@ def main():
                "path": "ParoRun.step_host (paro_b200 C ABI) replaying the timed steps: pinned host orbitals + "
                        "density in, new orbitals + mixed density out, copies on side streams overlapping the "
                        "density-only work and the Step-3 solves of already-arrived column chunks"
-                       + ("" if args.e2e_blocking or single else "; calls are stream-ordered: a step's copy-out "
+                       + ("" if not pipelined else "; calls are stream-ordered: a step's copy-out "
                           "overlaps the next step's copy-in chunk by chunk (each chunk's copy-in waits for its "
                           "copy-out), the last copy-out is inside the timed region")}
 

@@ -478,6 +478,7 @@ class ParoRun:
         self._fail_attempts = 0  # NotSpd attempts of the last Step 3 (the probe runs for that many)
         self.stops = StopTests(w)  # the reference's stop decisions, logged per Trace row
         self._chunks = None      # step_host: (c0, c1, copy event) of the local Step-3 columns
+        self._pieces = None      # step_host: (c0, c1, copy event) of every copied piece
         self._waited = set()     # step_host: ids of the chunk events the compute stream already waits on
         self._copy_stream = None
         # step_host(pipelined=True): copy-out stream, the previous step's copy-out events per column
@@ -583,7 +584,8 @@ class ParoRun:
         mine = [c for c in self._notspd_probe if c0 <= c < c1]
         hit, done = 0, {}
         if mine:
-            for k0, k1, ev in chunks:  # step_host: the probe columns' copies must have landed
+            # step_host: the probe columns' copies must have landed (their pieces, not their whole batch)
+            for k0, k1, ev in (self._pieces if self._pieces is not None else chunks):
                 if any(k0 <= c < k1 for c in mine):
                     self._wait_chunk(ev)
             # device-side gather (a host->device index upload would queue on the
@@ -761,9 +763,16 @@ class ParoRun:
             pieces = ranges
             if pipelined:
                 pieces = []
-                for k0, k1 in ranges:
+                for i0, (k0, k1) in enumerate(ranges):
+                    # <= 20 columns per piece; the first batch in halves, so that its first half's
+                    # copy-out (queued ahead of the density's) is short and its copy-in starts early
                     m = max(1, -(-(k1 - k0) // 20))
+                    if i0 == 0 and k1 - k0 >= 8:
+                        m = max(m, 2)
                     pieces += [(k0 + ((k1 - k0) * i) // m, k0 + ((k1 - k0) * (i + 1)) // m) for i in range(m)]
+                # the NotSpd probe opens Step 3: the pieces that hold its columns travel first
+                probe = [c for c in self._notspd_probe if c0 <= c < c1]
+                pieces.sort(key=lambda r: not any(r[0] <= c < r[1] for c in probe))
             evs = []
             self._mark("h2d_start", cs)
             for k0, k1 in pieces:
@@ -775,12 +784,13 @@ class ParoRun:
                 self._mark(f"h2d_cols_{k0}_{k1}", cs)
         self._d2h_events = []
         self._chunks = [(k0, k1, [ev for (a, b), ev in zip(pieces, evs) if a < k1 and k0 < b]) for k0, k1 in ranges]
+        self._pieces = [(a, b, ev) for (a, b), ev in zip(pieces, evs)]
         self._waited = set()
         self._out = (self._out_stream, h_orb, pieces) if pipelined else (cs, h_orb)
         try:
             tr = self.step(it)
         finally:
-            self._chunks, self._out = None, None
+            self._chunks, self._out, self._pieces = None, None, None
         main.wait_event(evs[-1])
         if not pipelined:
             if h_rho is not None:
