@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kCT) spmv_kernel(CsrView A, int K, const doubl
       }
     }
   }
-  if (MODE == kSpApply) return;
+  if constexpr (MODE == kSpApply) return;
 #pragma unroll
   for (int q = 0; q < NQ; ++q) red[q * kCT + tid] = valid ? acc[q] : 0.0;
   __syncthreads();

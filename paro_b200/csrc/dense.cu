@@ -16,8 +16,6 @@ namespace paro_b200 {
 
 namespace {
 
-__device__ __forceinline__ double& at(double* m, int n, int i, int j) { return m[i * n + j]; }
-
 // cholesky (linalg.cpp:307-323), block-wide; returns false on a non-positive
 // pivot. Column by column: once columns < j are final, every row i >= j forms
 // s = b_ij - sum_{k<j} l_ik l_jk with k ascending, the reference's own sum

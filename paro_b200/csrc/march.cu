@@ -46,9 +46,6 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// fl(a + fl(b*c)) with no contraction: the reference's `s += v * x`.
-__device__ __forceinline__ double madd(double s, double w, double x) { return __dadd_rn(s, __dmul_rn(w, x)); }
-
 template <int MODE>
 struct Cfg {
   static constexpr int NA = MODE == kApply ? 1 : MODE == kK1 ? 1 : MODE == kK2 ? 2 : 3;  // partial sums

@@ -1493,7 +1493,6 @@ bool apply_flat_ok(bool var, const MarchArgs& a) {
   if (rows / 2 + 1 > (1ll << 31) - 1) return false;
   // an odd row count leaves the last lattice row in a half-filled view row:
   // it is read only if the allocation extends S doubles past the operand
-  const long long vrows = (rows + 1) / 2;
   if ((rows & 1) != 0) {
     static PFN_cuMemGetAddressRange_v3020 range = [] {
       void* f = nullptr;
