@@ -1529,8 +1529,12 @@ void launch_apply_flat(bool var, int cb, const MarchArgs& a, const double* coefp
   else mc = mx;
   const int c = cb;
   if (var) {
+    // 8 columns per CTA halve the coefficient-box traffic per point-column; the two CTAs of an
+    // SM then fit with a 2-slot x ring (a step is twice as long, so one plane of lead covers
+    // the x stream) and a 3-slot coefficient ring (two planes of lead: profiles/r02/APPLY_EXPERIMENTS.md)
     if (c == 1) launch_k3f<true, 1>(a, mx, mc, st);
     else if (c == 2) launch_k3f<true, 2>(a, mx, mc, st);
+    else if (c >= 8) launch_k3f<true, 8, 2, 3>(a, mx, mc, st);
     else launch_k3f<true, 4>(a, mx, mc, st);
   } else {  // constant stencil: no coefficient ring, so the x ring runs a plane deeper (4.48 -> 4.17 ms at 257^3 x 76)
     if (c == 1) launch_k3f<false, 1, 4, 1>(a, mx, mc, st);
