@@ -123,9 +123,10 @@ def cpu_sample_rate(workload: str, sample_s: int, steps: int = 1, workers: int |
 
 
 def ref_sample_subdivisions(full, override: int = 0) -> int:
-    """The reduced mesh both CPU legs time the reference on (the reference
-    cannot build the 257^3 Kuhn mesh in the host RAM budget: its face map
-    alone is ~4e8 std::map entries); full size below 128 subdivisions."""
+    """The reduced mesh both CPU legs time the reference on (at 257^3 the
+    reference needs 108 s and 31 GB for the mesh alone and over an hour per
+    outer iteration: profiles/ref_fullsize_cpu.py checks the extrapolation
+    there); full size below 128 subdivisions."""
     return override or (48 if full.subdivisions >= 128 else full.subdivisions)
 
 

@@ -1,6 +1,6 @@
 """Full-size checks (BASELINE configs[4]: the 32-atom cluster, 257^3 nodes,
-76 orbitals, FP64) through size-independent properties: the reference cannot
-build this mesh in the host memory budget, so here the path is
+76 orbitals, FP64) through size-independent properties: one reference outer
+iteration takes over an hour at this size, so here the path is
 held to what must be true at any size -- the Step-3 solutions satisfy their
 source problems to the CG tolerance under the bit-exact operator apply, the
 Step-4 orbitals are B-orthonormal and diagonalise the projected form, the
