@@ -249,6 +249,11 @@ int paro_op_add_scaled(paro_ctx* ctx, paro_op* a, const paro_op* b, double s);
  * out: variable operator (paro_op_create_var); clamped: host, may be NULL. */
 int paro_ks_form(paro_ctx* ctx, const paro_op* kinetic, const paro_op* vext_mass, const double* rho,
                  const double* vh, int exchange_only, paro_op* out, long long* clamped);
+/* the same for the dofs of lattice planes [z0, z1) only (a rank's slab of a row-sharded run; the
+ * other coefficients of out are left as they are); clamped counts the cells of layers [z0, z1),
+ * plus the top layer when z1 is the last plane, so the ranks' counts add up to paro_ks_form's. */
+int paro_ks_form_planes(paro_ctx* ctx, const paro_op* kinetic, const paro_op* vext_mass, const double* rho,
+                        const double* vh, int exchange_only, int z0, int z1, paro_op* out, long long* clamped);
 
 /* ---------------------------------------------------------- fields ------- */
 /* density_from_orbitals (model.cpp:192-223): rho = sum_i occ_i u_i^2

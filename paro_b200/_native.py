@@ -151,6 +151,7 @@ SIGNATURES = {
     "paro_csr_cg_solve": (_I, [_P, _P, _I, _P, _P, _LL, _D, _SZ, _I, _P, _SZP, _DP]),
     "paro_csr_source_solve_step": (_I, [_P, _P, _P, _I, _P, _LL, _DP, _D, _SZ, _D, _P, _SZP, _DP]),
     "paro_ks_form": (_I, [_P, _P, _P, _P, _P, _I, _P, C.POINTER(_LL)]),
+    "paro_ks_form_planes": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _P, C.POINTER(_LL)]),
     "paro_density": (_I, [_P, _I, _P, _LL, _DP, _P, _DP]),
     "paro_mix_density": (_I, [_P, _P, _P, _D, _P]),
     "paro_density_rows": (_I, [_P, _I, _P, _LL, _DP, _LL, _LL, _P]),

@@ -455,6 +455,17 @@ def ks_form_matrix(kinetic: Operator, vext: Operator, rho: torch.Tensor, vh: tor
     return op, cl.value
 
 
+def ks_form_planes(kinetic: Operator, vext: Operator, rho: torch.Tensor, vh: torch.Tensor, z0: int, z1: int,
+                   out: Operator, exchange_only: bool = False) -> int:
+    """ks_form_matrix for the dofs of lattice planes [z0, z1) only (a rank's row slab); returns the
+    clamp count of the slab's cells (the ranks' counts add up to the full form's)."""
+    ctx = kinetic.ctx
+    cl = C.c_longlong(0)
+    ctx.check(N.lib().paro_ks_form_planes(ctx.h, kinetic.h, vext.h, _ptr(rho), _ptr(vh), int(exchange_only),
+                                          int(z0), int(z1), out.h, C.byref(cl)))
+    return cl.value
+
+
 # ------------------------------------------------------------------ fields --
 
 def density_from_orbitals(ctx: Context, orbitals: torch.Tensor, occupations, out: torch.Tensor | None = None):

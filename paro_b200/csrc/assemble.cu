@@ -46,6 +46,9 @@ struct AsmArgs {
   int* flags = nullptr;      // bit0 singular point hit, bit1 non-finite weight
   const double* wtab = nullptr;  // 4-point rules: precomputed w(x_q) per (cell, tet, point)
   unsigned long long* clamps = nullptr;  // Scf: count of rho(x_q) < 0
+  // plane-restricted assembly: cells [cell0, cell1) feed the table, cells [ccnt0, ccnt1) the
+  // clamp count, dofs [dof0, dof1) are gathered
+  long long cell0 = 0, cell1 = 0, ccnt0 = 0, ccnt1 = 0, dof0 = 0, dof1 = 0;
 };
 
 __device__ __forceinline__ double eval_in_element(const double* f, int s, const int (&vtx)[4][3],
@@ -95,9 +98,8 @@ __device__ double weight_at(const AsmArgs& a, const V3 (&P)[4], const int (&vtx)
 // the gather of a weighted mass needs no element geometry at all.
 __global__ void __launch_bounds__(128) wtable_kernel(const AsmArgs a, double* wtab) {
   const int s = a.box.s;
-  const long long ncell = static_cast<long long>(s) * s * s;
-  const long long cidx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (cidx >= ncell) return;
+  const long long cidx = a.cell0 + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (cidx >= a.cell1) return;
   const int ci = static_cast<int>(cidx % s), cj = static_cast<int>((cidx / s) % s),
             ck = static_cast<int>(cidx / (static_cast<long long>(s) * s));
   unsigned nneg = 0;
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(128) wtable_kernel(const AsmArgs a, double* wt
       wtab[(cidx * 6 + p) * 4 + q] = a.qw[q] * vol * wq;
     }
   }
-  if (nneg && a.clamps) atomicAdd(a.clamps, static_cast<unsigned long long>(nneg));
+  if (nneg && a.clamps && cidx >= a.ccnt0 && cidx < a.ccnt1) atomicAdd(a.clamps, static_cast<unsigned long long>(nneg));
 }
 
 // Weighted-mass gather from the quadrature table with the cell / tet loops
@@ -184,8 +186,8 @@ __device__ __forceinline__ void gather_cell(const AsmArgs& a, const double (&qp)
 }
 
 __global__ void __launch_bounds__(128) table_gather_kernel(const AsmArgs a) {
-  const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (t >= a.n) return;
+  const long long t = a.dof0 + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (t >= a.dof1) return;
   const int s = a.box.s;
   const long long S = s - 1;
   const int I = static_cast<int>(t % S) + 1;
@@ -437,17 +439,37 @@ void assemble(Ctx& ctx, const AssembleSpec& spec, Op& out) {
     PARO_CUDA(cudaMemsetAsync(clamps, 0, sizeof(unsigned long long), ctx.stream));
     a.clamps = clamps;
   }
-  if (wmass && !singular && a.nq == 4) {
-    const long long ncell = static_cast<long long>(g.s) * g.s * g.s;
+  const long long ncell = static_cast<long long>(g.s) * g.s * g.s;
+  const long long cplane = static_cast<long long>(g.s) * g.s, dplane = static_cast<long long>(g.S) * g.S;
+  a.cell0 = a.ccnt0 = 0;
+  a.cell1 = a.ccnt1 = ncell;
+  a.dof0 = 0;
+  a.dof1 = g.n;
+  const bool table = wmass && !singular && a.nq == 4;
+  if (spec.z1 >= 0) {  // a slab of lattice planes [z0, z1): dof plane z is touched by the cell layers z and z + 1
+    if (!table || spec.kind != kAsmScf) throw ParoError(kInvalidArgument, "assemble: plane ranges need the KS form");
+    if (spec.z0 < 0 || spec.z1 > g.S || spec.z0 > spec.z1) throw ParoError(kInvalidArgument, "assemble: bad plane range");
+    a.dof0 = spec.z0 * dplane;
+    a.dof1 = spec.z1 * dplane;
+    a.cell0 = spec.z0 * cplane;
+    a.cell1 = std::min<long long>(ncell, (static_cast<long long>(spec.z1) + 1) * cplane);
+    a.ccnt0 = spec.z0 * cplane;
+    a.ccnt1 = spec.z1 == g.S ? ncell : spec.z1 * cplane;
+  }
+  if (table) {
     double* wt = ctx.wtab.get<double>(static_cast<size_t>(ncell) * 24);
-    wtable_kernel<<<static_cast<unsigned>((ncell + 127) / 128), 128, 0, ctx.stream>>>(a, wt);
-    ++ctx.launches;
+    if (a.cell1 > a.cell0) {
+      wtable_kernel<<<static_cast<unsigned>((a.cell1 - a.cell0 + 127) / 128), 128, 0, ctx.stream>>>(a, wt);
+      ++ctx.launches;
+    }
     a.wtab = wt;
   }
-  const long long blocks = (g.n + 127) / 128;
-  if (a.wtab) table_gather_kernel<<<static_cast<unsigned>(blocks), 128, 0, ctx.stream>>>(a);
-  else assemble_kernel<<<static_cast<unsigned>(blocks), 128, 0, ctx.stream>>>(a);
-  ++ctx.launches;
+  const long long blocks = (a.dof1 - a.dof0 + 127) / 128;
+  if (blocks > 0) {
+    if (a.wtab) table_gather_kernel<<<static_cast<unsigned>(blocks), 128, 0, ctx.stream>>>(a);
+    else assemble_kernel<<<static_cast<unsigned>(blocks), 128, 0, ctx.stream>>>(a);
+    ++ctx.launches;
+  }
   PARO_CUDA(cudaGetLastError());
   int hflags = 0;
   unsigned long long hclamps = 0;

@@ -28,6 +28,10 @@ struct AssembleSpec {
   const Op* kinetic = nullptr;
   const Op* vext = nullptr;
   long long* clamped = nullptr;  // Scf: (element, point) pairs with rho < 0 (the reference's clamp count)
+  // Scf on the table path: only the dofs of lattice planes [z0, z1) are assembled (z1 < 0: all) --
+  // a rank's slab of a row-sharded run; the clamp count then covers the cells k in [z0, z1)
+  // (and the top cell layer k = S when z1 == S), so the ranks' counts add up to the full one
+  int z0 = 0, z1 = -1;
 };
 
 void assemble(Ctx& ctx, const AssembleSpec& spec, Op& out);

@@ -740,6 +740,27 @@ int paro_ks_form(paro_ctx* ctx, const paro_op* kinetic, const paro_op* vext, con
   });
 }
 
+int paro_ks_form_planes(paro_ctx* ctx, const paro_op* kinetic, const paro_op* vext, const double* rho,
+                        const double* vh, int exchange_only, int z0, int z1, paro_op* out, long long* clamped) {
+  return guarded(ctx, [&] {
+    if (!out->o.var) throw ParoError(kInvalidArgument, "ks_form: output must be a variable operator");
+    AssembleSpec s;
+    s.kind = kAsmScf;
+    s.rho = rho;
+    s.vh = vh;
+    s.exchange_only = exchange_only;
+    s.kinetic = &kinetic->o;
+    s.vext = &vext->o;
+    s.z0 = z0;
+    s.z1 = z1;
+    long long cl = 0;
+    s.clamped = &cl;
+    assemble(ctx->c, s, out->o);
+    if (clamped) *clamped = cl;
+    return kOk;
+  });
+}
+
 int paro_density(paro_ctx* ctx, int nocc, const double* u, long long ld, const double* occ, double* rho,
                  double* raw_integral) {
   return guarded(ctx, [&] {

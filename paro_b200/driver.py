@@ -237,6 +237,16 @@ class GpuBackend:
         op, clamped = self.core.ks_form_matrix(self.kinetic, self.vext, rho, vh, out=self.forms[slot])
         return op, clamped
 
+    def ks_form_slab(self, rho, vh, slot, z0, z1):
+        """The KS form's coefficients on the dofs of planes [z0, z1) (the rest of forms[slot] is
+        left as it is) and the clamp count of the slab's cells."""
+        cl = self.core.ks_form_planes(self.kinetic, self.vext, rho, vh, z0, z1, self.forms[slot])
+        return self.forms[slot], cl
+
+    def form_slots(self, op):
+        """[8, n] view of a variable operator's coefficient slots."""
+        return op.coefficients()
+
     # steps
     def hartree(self, rho, out=None):
         return self.core.hartree_solve_with(self.poisson, self.mass, rho, 1e-11, out=out)
@@ -639,6 +649,20 @@ class ParoRun:
         be.density_normalize(total, out)
         return out
 
+    def _ks_form(self, rho, vh, slot):
+        """ks_form_matrix (paro.cpp:433-454). Sharded runs assemble the form on this rank's row slab
+        (24 LDA evaluations per cell: the largest term that would otherwise be replicated) and
+        all-gather the 8 coefficient slots; the clamp counts of the slabs' cells add up."""
+        be, d = self.be, self.dist
+        if d.solo or not hasattr(be, "ks_form_slab"):
+            return be.ks_form(rho, vh, slot)
+        op, cl = be.ks_form_slab(rho, vh, slot, self.slab.z0, self.slab.z1)
+        slots = be.form_slots(op)
+        for o in range(slots.shape[0]):
+            d.allgather_rows(slots[o], self.slabs)
+        cl = sum(d.allgather_ints([cl], [1] * d.world, self._idev()))
+        return op, cl
+
     def _final_hook(self):
         """step_host at world size 1: Step 4 starts the host copy-out of the new
         orbitals as soon as they are final (before its Gram certificate)."""
@@ -835,7 +859,7 @@ class ParoRun:
             self._wait_chunks()  # step_host: the estimator reads every orbital
         eta = be.estimate(self.orb[:N_], self.lambdas[:N_], self.rho_in, vh_in) if self.estimate else None
         t_meshgen = time.perf_counter() - t2
-        a_in, cl = be.ks_form(self.rho_in, vh_in, "in")
+        a_in, cl = self._ks_form(self.rho_in, vh_in, "in")
         self.clamped += cl
         self._mark("step3_start")
         ts = time.perf_counter()
@@ -847,7 +871,7 @@ class ParoRun:
         half = self.half[: self.k]
         rho_half = self._density(half[:N_], self.rho_half)
         vh_half = be.hartree(rho_half, out=self.vh)
-        a_half, cl = be.ks_form(rho_half, vh_half, "half")
+        a_half, cl = self._ks_form(rho_half, vh_half, "half")
         self.clamped += cl
         orb, lam, defect = self.s4.ritz(half, a_half, be.mass_op(), N_, w.drop_tol, self.orb,
                                         on_final=self._final_hook())

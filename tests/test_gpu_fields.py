@@ -127,3 +127,40 @@ def test_nodal_sums_match_element_sums(ref, gpu_ctx_factory, s, lo, hi, uniform)
         p_ref = float(f @ mass.matvec(g))        # integrate_product == f' M g on Dirichlet functions
         scale = float(np.abs(f) @ mass.matvec(np.abs(g)))
         assert abs(core.integrate_product(c, fd, gd) - p_ref) <= 1e-13 * scale
+
+
+@pytest.mark.parametrize("s,parts", [(12, 3), (17, 4), (9, 8)])
+def test_ks_form_planes_union_is_the_full_form(ref, gpu_ctx_factory, s, parts):
+    """paro_ks_form_planes: the KS form assembled slab by slab (the row-sharded
+    run: each rank its planes, then an all-gather of the 8 coefficient slots)
+    is the full form bit for bit, the slabs' clamp counts add up to the full
+    count (a density with negative lobes, so the count is not zero), and a slab
+    call leaves the other planes' coefficients untouched."""
+    from paro_b200 import core
+    from paro_b200.step4 import RowSlab
+
+    sp = ref.Space(s, -6.0, 6.0)
+    ctx = gpu_ctx_factory(s, -6.0, 6.0)
+    rng = np.random.default_rng(s)
+    rho = _dev(rng.uniform(-0.05, 1.0, sp.n))          # some quadrature points interpolate below zero
+    vh = _dev(rng.standard_normal(sp.n))
+    kin = core.assemble_stiffness(ctx, 0.5)
+    vext = core.assemble_vext(ctx, H2_Z, H2_R, 0.0)
+    full, cl_full = core.ks_form_matrix(kin, vext, rho, vh)
+    assert cl_full > 0
+    S = ctx.S
+    out = core.Operator.variable_empty(ctx)
+    coef = out.coefficients()
+    coef.fill_(123.0)
+    total = 0
+    for r in range(parts):
+        sl = RowSlab.split(S, parts, r)
+        total += core.ks_form_planes(kin, vext, rho, vh, sl.z0, sl.z1, out)
+        assert torch.equal(coef[:, sl.r0:sl.r1], full.coefficients()[:, sl.r0:sl.r1])
+        if sl.r1 < ctx.n:
+            assert bool((coef[:, sl.r1:] == 123.0).all())   # later slabs not written yet
+    assert torch.equal(coef, full.coefficients())
+    assert total == cl_full
+    # an empty slab (more ranks than planes) is a no-op
+    assert core.ks_form_planes(kin, vext, rho, vh, 3, 3, out) == 0
+    assert torch.equal(coef, full.coefficients())
