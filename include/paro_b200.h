@@ -292,6 +292,12 @@ int paro_estimate_eta(paro_ctx* ctx, int N, const double* U, long long ld, const
 int paro_total_energy(paro_ctx* ctx, int n_lambdas, const double* lambdas, int nocc, const double* occ,
                       const double* rho, const double* vh, int exchange_only, int nnuc, const double* charges,
                       const double* positions, double* e_out);
+/* the same in two steps for a run sharded over row slabs: the XC term int rho (e_xc - v_xc) of the
+ * cell layers [k0, k1) (the ranks' partial sums add up), and the total with the summed term */
+int paro_energy_xc_layers(paro_ctx* ctx, const double* rho, int exchange_only, int k0, int k1, double* out);
+int paro_total_energy_with_xc(paro_ctx* ctx, int n_lambdas, const double* lambdas, int nocc, const double* occ,
+                              const double* rho, const double* vh, int nnuc, const double* charges,
+                              const double* positions, double xc_term, double* e_out);
 
 /* ---------------------------------------------- general CSR operators ---- */
 /* SparseOperator (linalg.hpp:14-50) for matrices that are not the uniform

@@ -161,6 +161,8 @@ SIGNATURES = {
     "paro_integrate_product": (_I, [_P, _P, _P, _DP]),
     "paro_rho_residual": (_I, [_P, _P, _P, _P, _DP]),
     "paro_total_energy": (_I, [_P, _I, _DP, _I, _DP, _P, _P, _I, _I, _DP, _DP, _DP]),
+    "paro_energy_xc_layers": (_I, [_P, _P, _I, _I, _I, _DP]),
+    "paro_total_energy_with_xc": (_I, [_P, _I, _DP, _I, _DP, _P, _P, _I, _DP, _DP, C.c_double, _DP]),
     "paro_estimate_eta": (_I, [_P, _I, _P, _LL, _DP, _D, _I, _D, _I, _DP, _DP, _D, _P, _P, _I, _P, _DP]),
 }
 

@@ -523,6 +523,22 @@ def total_energy(ctx: Context, lambdas, occupations, rho: torch.Tensor, vh: torc
                    int(exchange_only), len(Z), Z.ctypes.data_as(_DP), R.ctypes.data_as(_DP))
 
 
+def energy_xc_layers(ctx: Context, rho: torch.Tensor, k0: int, k1: int, exchange_only: bool = False) -> float:
+    """The XC term of total_energy, int rho (e_xc - v_xc), over the cell layers [k0, k1)."""
+    return _scalar(ctx, N.lib().paro_energy_xc_layers, _ptr(rho), int(exchange_only), int(k0), int(k1))
+
+
+def total_energy_with_xc(ctx: Context, lambdas, occupations, rho: torch.Tensor, vh: torch.Tensor, charges, positions,
+                         xc_term: float) -> float:
+    """total_energy (model.cpp:329-360) with the XC term summed elsewhere (energy_xc_layers over the ranks)."""
+    lam = (C.c_double * len(lambdas))(*[float(v) for v in lambdas])
+    occ = (C.c_double * len(occupations))(*[float(v) for v in occupations])
+    Z = np.ascontiguousarray(charges, np.float64)
+    R = np.ascontiguousarray(positions, np.float64).reshape(-1)
+    return _scalar(ctx, N.lib().paro_total_energy_with_xc, len(lambdas), lam, len(occupations), occ, _ptr(rho),
+                   _ptr(vh), len(Z), Z.ctypes.data_as(_DP), R.ctypes.data_as(_DP), float(xc_term))
+
+
 def estimate_eta(ctx: Context, orbitals: torch.Tensor, lambdas, *, diffusion: float = 0.5, reaction: str = "ks",
                  c: float = 0.0, charges=(), positions=(), eps: float = 0.0, rho: torch.Tensor | None = None,
                  vh: torch.Tensor | None = None, exchange_only: bool = False, with_eta: bool = False):

@@ -860,6 +860,27 @@ int paro_total_energy(paro_ctx* ctx, int n_lambdas, const double* lambdas, int n
   });
 }
 
+int paro_energy_xc_layers(paro_ctx* ctx, const double* rho, int exchange_only, int k0, int k1, double* out) {
+  return guarded(ctx, [&] {
+    *out = energy_xc_term(ctx->c, rho, exchange_only, k0, k1);
+    return kOk;
+  });
+}
+
+int paro_total_energy_with_xc(paro_ctx* ctx, int n_lambdas, const double* lambdas, int nocc, const double* occ,
+                              const double* rho, const double* vh, int nnuc, const double* charges,
+                              const double* positions, double xc_term, double* e_out) {
+  return guarded(ctx, [&] {
+    std::vector<double> nuc;
+    for (int k = 0; k < nnuc; ++k) {
+      nuc.push_back(charges[k]);
+      for (int c = 0; c < 3; ++c) nuc.push_back(positions[3 * k + c]);
+    }
+    *e_out = total_energy(ctx->c, n_lambdas, lambdas, nocc, occ, rho, vh, 0, nnuc, nuc.data(), &xc_term);
+    return kOk;
+  });
+}
+
 int paro_fix_sign(paro_ctx* ctx, int k, double* v, long long ld) {
   return guarded(ctx, [&] {
     fix_sign_columns(ctx->c, v, ld, k);

@@ -59,6 +59,7 @@ struct CellArgs {
   int exchange_only;
   double cx;
   double* partials;
+  long long cell0, cell1;  // cells [cell0, cell1) are summed (a slab's cell layers)
 };
 
 __device__ __forceinline__ double vval(const double* f, int s, int vx, int vy, int vz) {
@@ -69,10 +70,9 @@ __device__ __forceinline__ double vval(const double* f, int s, int vx, int vy, i
 __global__ void __launch_bounds__(kRedThreads) cell_reduce_kernel(const CellArgs a) {
   __shared__ double sh[kRedThreads / 32];
   const int s = a.box.s;
-  const long long ncell = static_cast<long long>(s) * s * s;
-  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const long long c = a.cell0 + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   double acc = 0.0;
-  if (c < ncell) {
+  if (c < a.cell1) {
     const int ci = static_cast<int>(c % s), cj = static_cast<int>((c / s) % s), ck = static_cast<int>(c / (static_cast<long long>(s) * s));
     // the cell's corner coordinates, once (coord() divides by s)
     const double x0c = a.box.coord(ci), x1c = a.box.coord(ci + 1), y0c = a.box.coord(cj), y1c = a.box.coord(cj + 1);
@@ -241,11 +241,14 @@ double node_reduce(Ctx& ctx, int mode, const double* f, const double* g) {
 
 }  // namespace
 
-double cell_reduce(Ctx& ctx, int mode, const double* f, const double* g, int exchange_only) {
+double cell_reduce(Ctx& ctx, int mode, const double* f, const double* g, int exchange_only, int k0, int k1) {
   ctx.check_grid();
-  if ((mode == kCellIntegrate || mode == kCellNorm2 || mode == kCellProduct) && ctx.nodal_sums && uniform_mass(ctx))
+  const bool all = k1 < 0;
+  if (all && (mode == kCellIntegrate || mode == kCellNorm2 || mode == kCellProduct) && ctx.nodal_sums &&
+      uniform_mass(ctx))
     return node_reduce(ctx, mode, f, g);
   const Grid& gr = ctx.grid;
+  if (!all && (k0 < 0 || k1 > gr.s || k0 > k1)) throw ParoError(kInvalidArgument, "cell sum: bad cell-layer range");
   static thread_local DevBuf rule, part;
   const Rule& r4 = simplex_rule3(2);
   std::vector<double> host(20);
@@ -255,10 +258,13 @@ double cell_reduce(Ctx& ctx, int mode, const double* f, const double* g, int exc
   }
   double* drule = rule.get<double>(20);
   small_h2d(ctx, drule, host.data(), sizeof(double) * 20);
-  const long long ncell = static_cast<long long>(gr.s) * gr.s * gr.s;
-  const long long blocks = (ncell + kRedThreads - 1) / kRedThreads;
+  const long long layer = static_cast<long long>(gr.s) * gr.s;
+  const long long cell0 = all ? 0 : k0 * layer, cell1 = all ? layer * gr.s : k1 * layer;
+  if (cell1 <= cell0) return 0.0;
+  const long long blocks = (cell1 - cell0 + kRedThreads - 1) / kRedThreads;
   double* partials = part.get<double>(blocks + 1);
-  CellArgs a{Box{gr.s, gr.lo, gr.hi}, mode, f, g, drule, drule + 16, exchange_only, std::cbrt(3.0 / M_PI), partials};
+  CellArgs a{Box{gr.s, gr.lo, gr.hi}, mode, f, g, drule, drule + 16, exchange_only, std::cbrt(3.0 / M_PI), partials,
+             cell0, cell1};
   cell_reduce_kernel<<<static_cast<unsigned>(blocks), kRedThreads, 0, ctx.stream>>>(a);
   sum_kernel<<<1, 1024, 0, ctx.stream>>>(partials, blocks, partials + blocks);
   ctx.launches += 2;
@@ -326,13 +332,19 @@ void diff(Ctx& ctx, const double* a, const double* b, double* out) {
 
 double norm_l2(Ctx& ctx, const double* f) { return std::sqrt(std::max(0.0, cell_reduce(ctx, kCellNorm2, f, nullptr, 0))); }
 
+// the XC term of total_energy, int rho (e_xc - v_xc), over the cell layers [k0, k1) (k1 < 0: all)
+double energy_xc_term(Ctx& ctx, const double* rho, int exchange_only, int k0, int k1) {
+  return cell_reduce(ctx, kCellExc, rho, nullptr, exchange_only, k0, k1);
+}
+
 double total_energy(Ctx& ctx, int nl, const double* lambdas, int nocc, const double* occ, const double* rho,
-                    const double* vh, int exchange_only, int nnuc, const double* nuclei) {
+                    const double* vh, int exchange_only, int nnuc, const double* nuclei, const double* xc_term) {
   if (nl < nocc) throw ParoError(kInvalidArgument, "total_energy: missing eigenvalue estimates");
   double e_band = 0.0;
   for (int i = 0; i < nocc; ++i) e_band += occ[i] * lambdas[i];
   const double e_hartree = 0.5 * cell_reduce(ctx, kCellProduct, vh, rho, 0);
-  const double e_xc = cell_reduce(ctx, kCellExc, rho, nullptr, exchange_only);
+  // a sharded run passes the XC term it summed over the ranks' cell layers
+  const double e_xc = xc_term ? *xc_term : cell_reduce(ctx, kCellExc, rho, nullptr, exchange_only);
   // nuclear_repulsion (model.cpp:177-186)
   double enn = 0.0;
   for (int k = 0; k < nnuc; ++k)

@@ -274,6 +274,13 @@ class GpuBackend:
     def energy(self, lambdas, occ, rho, vh):
         return self.core.total_energy(self.ctx, lambdas, occ, rho, vh, self.w.charges, self.w.positions)
 
+    def energy_xc_layers(self, rho, k0, k1):
+        return self.core.energy_xc_layers(self.ctx, rho, k0, k1)
+
+    def energy_with_xc(self, lambdas, occ, rho, vh, xc_term):
+        return self.core.total_energy_with_xc(self.ctx, lambdas, occ, rho, vh, self.w.charges, self.w.positions,
+                                              xc_term)
+
     def mix(self, rin, rout, alpha, out):
         return self.core.mix_density(self.ctx, rin, rout, alpha, out=out)
 
@@ -663,6 +670,18 @@ class ParoRun:
         cl = sum(d.allgather_ints([cl], [1] * d.world, self._idev()))
         return op, cl
 
+    def _energy(self, lam, rho, vh):
+        """total_energy (model.cpp:329-360). Sharded runs sum the XC term (24 LDA evaluations per
+        cell) over the ranks' cell layers, added in rank order."""
+        be, d = self.be, self.dist
+        if d.solo or not hasattr(be, "energy_xc_layers"):
+            return be.energy(lam, self.occ, rho, vh)
+        # cell layers of this rank's slab; the top layer (k = S) goes with the last slab
+        k1 = self.slab.z1 + 1 if self.slab.z1 == be.S else self.slab.z1
+        part = torch.tensor([be.energy_xc_layers(rho, self.slab.z0, k1)], dtype=torch.float64, device=self._idev())
+        d.allsum_(part)
+        return be.energy_with_xc(lam, self.occ, rho, vh, float(part.item()))
+
     def _final_hook(self):
         """step_host at world size 1: Step 4 starts the host copy-out of the new
         orbitals as soon as they are final (before its Gram certificate)."""
@@ -882,7 +901,7 @@ class ParoRun:
         t_project = time.perf_counter() - tp
         rho_out = self._density(orb[:N_], self.rho_out)
         vh_out = be.hartree(rho_out, out=self.vh)
-        e_tot = be.energy(lam, self.occ, rho_out, vh_out)
+        e_tot = self._energy(lam, rho_out, vh_out)
         res = be.rho_residual(rho_out, self.rho_in)
         be.mix(self.rho_in, rho_out, w.mixing_alpha, out=self.rho_in)
         self._mark("step_end")

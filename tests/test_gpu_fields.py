@@ -164,3 +164,32 @@ def test_ks_form_planes_union_is_the_full_form(ref, gpu_ctx_factory, s, parts):
     # an empty slab (more ranks than planes) is a no-op
     assert core.ks_form_planes(kin, vext, rho, vh, 3, 3, out) == 0
     assert torch.equal(coef, full.coefficients())
+
+
+def test_energy_xc_layers_add_up(ref, gpu_ctx_factory):
+    """The XC term of total_energy summed over cell-layer slabs (the sharded
+    run) against the one-call form: equal to rounding, and with the full layer
+    range bit for bit; total_energy_with_xc with that term is total_energy."""
+    from paro_b200 import core
+    from paro_b200.step4 import RowSlab
+
+    s = 14
+    sp = ref.Space(s, -6.0, 6.0)
+    ctx = gpu_ctx_factory(s, -6.0, 6.0)
+    rng = np.random.default_rng(3)
+    rho = _dev(rng.uniform(0.0, 1.0, sp.n))
+    vh = _dev(rng.standard_normal(sp.n))
+    lam, occ = [-0.7, -0.3], [2.0, 2.0]
+    full = core.energy_xc_layers(ctx, rho, 0, s)
+    S = ctx.S
+    for parts in (2, 5):
+        tot = 0.0
+        for r in range(parts):
+            sl = RowSlab.split(S, parts, r)
+            tot += core.energy_xc_layers(ctx, rho, sl.z0, sl.z1 + 1 if sl.z1 == S else sl.z1)
+        assert abs(tot - full) <= 1e-13 * abs(full)
+    assert core.energy_xc_layers(ctx, rho, 4, 4) == 0.0
+    e = core.total_energy(ctx, lam, occ, rho, vh, H2_Z, H2_R)
+    assert core.total_energy_with_xc(ctx, lam, occ, rho, vh, H2_Z, H2_R, full) == e
+    e_ref = ref.total_energy(sp, lam, 2, rho.cpu().numpy(), vh.cpu().numpy(), H2_Z, H2_R)
+    assert abs(e - e_ref) <= 1e-12 * abs(e_ref)
