@@ -331,7 +331,8 @@ def main():
         else:
             # stream-ordered calls pay off when the copies are long (>= 64 MB of orbitals per
             # rank); steps of a few ms keep the blocking calls (fewer events and streams)
-            pipelined = not args.e2e_blocking and h_orb[c0_:c1_].numel() * 8 >= (64 << 20)
+            # (one rank: with the orbitals sharded the per-rank copies are short and the calls stay blocking)
+            pipelined = not args.e2e_blocking and world == 1 and h_orb[c0_:c1_].numel() * 8 >= (64 << 20)
             e0.record()
             for i in range(args.steps):
                 tr = run.step_host(args.warmup + i, h_orb, h_rho, chunks=args.e2e_chunks, pipelined=pipelined)
