@@ -369,6 +369,20 @@ def main():
                              f"--impl reference"}
         except Exception as exc:  # the oracle build is test/baseline infrastructure only
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {exc}"}
+        # the committed direct measurement of the reference's Step-3 cg_solve at the full 257^3 mesh
+        # (profiles/ref_fullsize_cpu.py, run once on the GPU box's host cores): a check of the model above
+        if w.subdivisions == 256:
+            try:
+                chk = json.loads((ROOT / "profiles" / "r02" / "ref_fullsize_cpu.json").read_text())
+                cpu["fullsize_check"] = {
+                    "step3_s_per_outer_iteration": chk["step3_s_per_outer_iteration"],
+                    "col_iters_per_s": max(r["col_iters_per_s"] for r in chk["pinned"]),
+                    "workers": chk["workers"],
+                    "note": "reference cg_solve at a pinned iteration count on the full mesh (Step 3 only; the "
+                            "reference's Hartree PCG needs ~1,236 single-thread iterations = ~720 s per solve, "
+                            "three per outer iteration); profiles/r02/ref_fullsize_cpu.json"}
+            except (OSError, ValueError, KeyError):
+                pass
 
     # Step 2 (the residual estimator) is excluded from the metric on both sides
     # (on a fixed mesh it only feeds eta_total); timed once here
